@@ -25,6 +25,7 @@ embc_status match_stats(embc_ctx* ctx, const int32_t* d_codes, uint32_t dim, uin
 embc_status pattern_counts(embc_ctx* ctx, const float* d_x, uint32_t dim, uint32_t rows, double eb,
                            uint64_t* h_orig, uint64_t* h_quant, cudaStream_t stream);
 cudaError_t encode_set_attributes();
+cudaError_t decode_set_attributes();
 
 std::string fmt_double(double v) {  // std::to_string(double) == "%f"
   char buf[512];
@@ -288,7 +289,10 @@ embc_status embc_ctx_create(int device, embc_ctx** out) {
   *out = nullptr;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return EMBC_ERR_CUDA;
-  std::call_once(g_attr_once, [] { g_attr_err = encode_set_attributes(); });
+  std::call_once(g_attr_once, [] {
+    g_attr_err = encode_set_attributes();
+    if (g_attr_err == cudaSuccess) g_attr_err = decode_set_attributes();
+  });
   if (g_attr_err != cudaSuccess) return EMBC_ERR_CUDA;
   embc_ctx* ctx = new embc_ctx();
   ctx->device = device;

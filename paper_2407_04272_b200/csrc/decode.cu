@@ -18,6 +18,9 @@
 
 namespace embc_dev {
 
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
+
 __device__ __forceinline__ void dec_fail(DecState& S, uint64_t index, uint32_t reason, uint64_t a,
                                          uint64_t b) {
   if (S.err == ~0ull) {
@@ -169,12 +172,12 @@ __device__ __forceinline__ bool rd_varint(const uint8_t* p, uint64_t L, uint64_t
 }
 
 __global__ void k_dec_vlz_seq(const DChunk* __restrict__ ch, DecState* __restrict__ st,
-                              const uint32_t* __restrict__ list) {
+                              const uint32_t* __restrict__ list, const uint32_t* __restrict__ vflag) {
   if (threadIdx.x != 0) return;
   const uint32_t c = list[blockIdx.x];
   const DChunk C = ch[c];
   DecState& S = st[c];
-  if (S.err != ~0ull) return;
+  if (S.err != ~0ull || !(C.seq || vflag[c])) return;  // only chunks the parallel path did not finish
   const uint8_t* p = C.in + S.pay_off;
   const uint64_t L = S.pay_len;
   const double w = 2.0 * S.eb;
@@ -212,12 +215,384 @@ __global__ void k_dec_vlz_seq(const DChunk* __restrict__ ch, DecState* __restric
   }
   if (pos != L) dec_fail(S, 0, EMBC_R_VLZ_TRAILING, L - pos, n);
 }
+// ===========================================================================
+// VLZ parallel decode (vlz.hpp:129-158 without its sequential dependency).
+//
+// A valid token stream is a sequence of "units": maximal byte runs ending in a
+// byte with bit 7 clear.  Tags are one-byte units (0x00 / 0x01); every varint
+// is one unit.  The token chain over units is next(u) = u + (tag ? 2 : dim+1),
+// so token boundaries are recovered in parallel without side-band offsets:
+//   V1 k_vlz_map    per 2 KiB byte segment: unit table, then pointer jumping
+//                   gives, for each possible entry offset e in [0, dim], the
+//                   exit offset into the next segment and the tokens crossed.
+//   V2 k_vlz_chain  per chunk: walk the segment maps -> true entry + first row
+//                   of every segment; checks the token count and the end.
+//   V3 k_vlz_rows   per segment: binary lifting enumerates the chain's tags ->
+//                   per row: tag unit, reference source row (offset validated).
+//   V4 k_vlz_roots  per chunk: pointer jumping resolves reference chains to the
+//                   root literal row.
+//   V5 k_vlz_out    per element: varint of the root literal -> zigzag ->
+//                   dequantize -> output tensor.
+// Any anomaly flags the chunk; k_dec_vlz_seq then re-walks it sequentially to
+// report the reference's exact error.
+// ===========================================================================
+constexpr uint32_t kSeg = 2048;        // bytes (>= units) per segment
+constexpr uint32_t kVlzMaxDim = 1023;  // larger dims use the sequential walker
+constexpr int kLift = 11;              // 2^11 > kSeg / 2 chain steps
+constexpr uint16_t kInv = 0xFFFF;
 
-// ---------------------------------------------------------------------------
-// D3: huffman codebook (read_codebook + from_lengths + finalize,
-// huffman.hpp:132-148, :165-186, :213-222) -- one CTA per chunk -- followed
-// by the bit-serial canonical decode (huffman.hpp:254-291).
-// ---------------------------------------------------------------------------
+struct SegPair {
+  uint32_t chunk, seg;
+};
+
+// unit kinds: 0 = tag 0x00, 1 = tag 0x01, 2 = not a valid tag
+__global__ void __launch_bounds__(kBlock) k_vlz_map(const DChunk* __restrict__ ch,
+                                                    const DecState* __restrict__ st,
+                                                    const SegPair* __restrict__ segs,
+                                                    uint32_t* __restrict__ ustart,
+                                                    uint8_t* __restrict__ ukind,
+                                                    uint32_t* __restrict__ seg_units,
+                                                    uint64_t* __restrict__ maps,
+                                                    uint32_t* __restrict__ vflag) {
+  __shared__ uint16_t J[kSeg], Cn[kSeg];
+  __shared__ uint32_t uend[kSeg];
+  __shared__ uint32_t s_tmp32[33];
+  __shared__ int s_bad;
+  const SegPair sp = segs[blockIdx.x];
+  const DChunk& C = ch[sp.chunk];
+  if (st[sp.chunk].err != ~0ull || C.seq) return;
+  const DecState& S = st[sp.chunk];
+  const uint8_t* p = C.in + S.pay_off;
+  const uint64_t L = S.pay_len;
+  const uint32_t b0 = sp.seg * kSeg;
+  const uint32_t nb = static_cast<uint32_t>(umin64(kSeg, L > b0 ? L - b0 : 0));
+  const uint32_t D = C.dim;
+  if (threadIdx.x == 0) s_bad = 0;
+  // terminal bytes, 8 consecutive bytes per thread
+  const uint32_t i0 = threadIdx.x * 8;
+  uint32_t mask = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t i = i0 + k;
+    if (i < nb && !(p[b0 + i] & 0x80)) mask |= 1u << k;
+  }
+  uint32_t U;
+  uint32_t k0 = block_excl_scan<uint32_t>(__popc(mask), s_tmp32, &U);
+  {
+    uint32_t m = mask, k = k0;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      uend[k++] = b0 + i0 + b;
+    }
+  }
+  __syncthreads();
+  const uint64_t ubase = static_cast<uint64_t>(C.seg0 + sp.seg) * kSeg;
+  for (uint32_t k = threadIdx.x; k < U; k += blockDim.x) {
+    uint32_t start;
+    if (k > 0) {
+      start = uend[k - 1] + 1;
+    } else {  // the first unit may begin in the previous segment
+      start = b0;
+      while (start > 0 && (p[start - 1] & 0x80) && b0 - start <= 10) --start;
+    }
+    const uint32_t len = uend[k] - start + 1;
+    if (len > 10) s_bad = 1;  // neither a tag nor a <= 10-byte varint (bytes.hpp:139-147)
+    const uint8_t v = p[start];
+    const uint8_t kind = (len == 1 && v <= 1) ? v : 2;
+    ustart[ubase + k] = start;
+    ukind[ubase + k] = kind;
+    J[k] = kind == 2 ? kInv : static_cast<uint16_t>(k + (kind == 0 ? D + 1 : 2));
+    Cn[k] = 1;
+  }
+  // a trailing partial unit can never be consumed by a valid parse
+  if (threadIdx.x == 0 && b0 + nb == L && nb > 0 && (p[L - 1] & 0x80)) s_bad = 1;
+  if (threadIdx.x == 0) seg_units[C.seg0 + sp.seg] = U;
+  __syncthreads();
+  // pointer jumping: J[k] -> first chain unit outside the segment (or kInv),
+  // Cn[k] -> tags visited from k
+  for (int r = 0; r < kLift; ++r) {
+    uint16_t nj[kSeg / kBlock], nc[kSeg / kBlock];
+#pragma unroll
+    for (uint32_t q = 0; q < kSeg / kBlock; ++q) {
+      const uint32_t k = threadIdx.x + q * kBlock;
+      nj[q] = 0;
+      nc[q] = 0;
+      if (k < U) {
+        const uint16_t j = J[k];
+        nj[q] = j;
+        nc[q] = Cn[k];
+        if (j < U) {
+          nj[q] = J[j];
+          nc[q] = Cn[k] + Cn[j];
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t q = 0; q < kSeg / kBlock; ++q) {
+      const uint32_t k = threadIdx.x + q * kBlock;
+      if (k < U) {
+        J[k] = nj[q];
+        Cn[k] = nc[q];
+      }
+    }
+    __syncthreads();
+  }
+  uint64_t* m = maps + C.map_base + static_cast<uint64_t>(sp.seg) * (D + 1);
+  for (uint32_t e = threadIdx.x; e <= D; e += blockDim.x) {
+    uint32_t exit_off, cnt;
+    if (e < U) {
+      const uint16_t j = J[e];
+      exit_off = j == kInv ? 0xFFFFFFFFu : j - U;
+      cnt = Cn[e];
+    } else {
+      exit_off = e - U;
+      cnt = 0;
+    }
+    m[e] = (static_cast<uint64_t>(cnt) << 32) | exit_off;
+  }
+  if (threadIdx.x == 0 && s_bad) vflag[sp.chunk] = 1;
+}
+
+__global__ void k_vlz_chain(const DChunk* __restrict__ ch, const DecState* __restrict__ st,
+                            const uint32_t* __restrict__ list, uint32_t nlist,
+                            const uint64_t* __restrict__ maps, uint32_t* __restrict__ seg_entry,
+                            uint32_t* __restrict__ seg_row0, uint32_t* __restrict__ vflag) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nlist) return;
+  const uint32_t c = list[q];
+  const DChunk& C = ch[c];
+  if (st[c].err != ~0ull || C.seq || vflag[c]) return;
+  const uint32_t D = C.dim;
+  uint32_t e = 0, row = 0;
+  bool bad = false;
+  for (uint32_t s = 0; s < C.nseg; ++s) {
+    seg_entry[C.seg0 + s] = e;
+    seg_row0[C.seg0 + s] = row;
+    const uint64_t m = maps[C.map_base + static_cast<uint64_t>(s) * (D + 1) + e];
+    const uint32_t exit_off = static_cast<uint32_t>(m);
+    if (exit_off == 0xFFFFFFFFu) {
+      bad = true;
+      break;
+    }
+    row += static_cast<uint32_t>(m >> 32);
+    e = exit_off;
+    if (row > C.count) {
+      bad = true;
+      break;
+    }
+  }
+  if (bad || row != C.count || e != 0) vflag[c] = 1;
+}
+
+__device__ __forceinline__ uint32_t unit_advance(const uint32_t* __restrict__ seg_units, uint32_t seg0,
+                                                 uint32_t nseg, uint32_t addr, uint32_t k, bool* ok) {
+  uint32_t s = addr / kSeg, l = addr % kSeg;
+  while (s < nseg) {
+    const uint32_t U = seg_units[seg0 + s];
+    if (l + k < U) return s * kSeg + l + k;
+    k -= U - l;
+    l = 0;
+    ++s;
+  }
+  *ok = false;
+  return 0;
+}
+
+// varint at unit start (bytes.hpp:139-147 semantics: bits past 64 dropped)
+__device__ __forceinline__ uint64_t unit_varint(const uint8_t* p, uint32_t start) {
+  uint64_t v = 0;
+#pragma unroll 1
+  for (int shift = 0; shift < 70; shift += 7) {
+    const uint8_t b = p[start++];
+    if (shift < 64) v |= static_cast<uint64_t>(b & 0x7F) << shift;
+    if (!(b & 0x80)) break;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(kBlock) k_vlz_rows(const DChunk* __restrict__ ch,
+                                                     const DecState* __restrict__ st,
+                                                     const SegPair* __restrict__ segs,
+                                                     const uint32_t* __restrict__ ustart,
+                                                     const uint8_t* __restrict__ ukind,
+                                                     const uint32_t* __restrict__ seg_units,
+                                                     const uint32_t* __restrict__ seg_entry,
+                                                     const uint32_t* __restrict__ seg_row0,
+                                                     uint32_t* __restrict__ row_tag,
+                                                     uint32_t* __restrict__ row_src,
+                                                     uint32_t* __restrict__ vflag) {
+  __shared__ uint16_t Jt[kLift][kSeg];
+  const SegPair sp = segs[blockIdx.x];
+  const DChunk& C = ch[sp.chunk];
+  if (st[sp.chunk].err != ~0ull || C.seq || vflag[sp.chunk]) return;
+  const DecState& S = st[sp.chunk];
+  const uint8_t* p = C.in + S.pay_off;
+  const uint32_t D = C.dim;
+  const uint32_t g = C.seg0 + sp.seg;
+  const uint32_t U = seg_units[g];
+  const uint32_t e = seg_entry[g];
+  const uint32_t row0 = seg_row0[g];
+  const uint32_t rowN = sp.seg + 1 < C.nseg ? seg_row0[g + 1] : C.count;
+  const uint32_t T = rowN - row0;
+  if (T == 0) return;
+  const uint64_t ubase = static_cast<uint64_t>(g) * kSeg;
+  for (uint32_t k = threadIdx.x; k < U; k += blockDim.x) {
+    const uint8_t kind = ukind[ubase + k];
+    Jt[0][k] = kind == 2 ? kInv : static_cast<uint16_t>(umin32(k + (kind == 0 ? D + 1 : 2), kInv - 1));
+  }
+  __syncthreads();
+  for (int r = 1; r < kLift; ++r) {
+    for (uint32_t k = threadIdx.x; k < U; k += blockDim.x) {
+      const uint16_t j = Jt[r - 1][k];
+      Jt[r][k] = j < U ? Jt[r - 1][j] : j;
+    }
+    __syncthreads();
+  }
+  const uint64_t rb = C.row_base;
+  bool bad = false;
+  for (uint32_t t = threadIdx.x; t < T; t += blockDim.x) {
+    uint32_t pos = e;
+    for (int r = 0; r < kLift && pos < U; ++r)
+      if ((t >> r) & 1) pos = Jt[r][pos];
+    if (pos >= U) {
+      bad = true;
+      continue;
+    }
+    const uint32_t row = row0 + t;
+    const uint32_t addr = sp.seg * kSeg + pos;
+    row_tag[rb + row] = addr;
+    if (ukind[ubase + pos] == 1) {  // reference token: validate (vlz.hpp:141-145)
+      bool ok = true;
+      const uint32_t ga = unit_advance(seg_units, C.seg0, C.nseg, addr, 1, &ok);
+      uint64_t off = 0;
+      if (ok) off = unit_varint(p, ustart[static_cast<uint64_t>(C.seg0) * kSeg + ga]);
+      if (!ok || off < 1 || off > row || off > kMaxWindow) {
+        bad = true;
+        row_src[rb + row] = row;
+      } else {
+        row_src[rb + row] = row - static_cast<uint32_t>(off);
+      }
+    } else {
+      row_src[rb + row] = row;
+    }
+  }
+  if (bad) vflag[sp.chunk] = 1;
+}
+
+constexpr uint32_t kRootSmem = 12288;
+
+__global__ void __launch_bounds__(1024) k_vlz_roots(const DChunk* __restrict__ ch,
+                                                    const DecState* __restrict__ st,
+                                                    const uint32_t* __restrict__ list,
+                                                    const uint32_t* __restrict__ vflag,
+                                                    uint32_t* __restrict__ row_src,
+                                                    uint32_t* __restrict__ row_tag,
+                                                    uint32_t* __restrict__ row_root) {
+  __shared__ uint32_t sh[kRootSmem];
+  const uint32_t c = list[blockIdx.x];
+  const DChunk& C = ch[c];
+  if (st[c].err != ~0ull || C.seq || vflag[c]) return;
+  const uint32_t n = C.count;
+  uint32_t* src = row_src + C.row_base;
+  uint32_t* a = n <= kRootSmem ? sh : src;
+  if (n <= kRootSmem)
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) sh[i] = src[i];
+  __syncthreads();
+  for (;;) {  // pointer jumping to the root literal (every source is an earlier row)
+    bool changed = false;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t s = a[i];
+      const uint32_t ss = a[s];
+      if (ss != s) {
+        a[i] = ss;
+        changed = true;
+      }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+    row_root[C.row_base + i] = row_tag[C.row_base + a[i]];
+}
+
+struct ElemTile {
+  uint32_t chunk, pad;
+  uint64_t e0, ne;
+};
+
+__global__ void __launch_bounds__(kBlock) k_vlz_out(const DChunk* __restrict__ ch,
+                                                    const DecState* __restrict__ st,
+                                                    const ElemTile* __restrict__ tiles,
+                                                    const uint32_t* __restrict__ vflag,
+                                                    const uint32_t* __restrict__ ustart,
+                                                    const uint32_t* __restrict__ seg_units,
+                                                    const uint32_t* __restrict__ row_root) {
+  const ElemTile T = tiles[blockIdx.x];
+  const DChunk& C = ch[T.chunk];
+  if (st[T.chunk].err != ~0ull || C.seq || vflag[T.chunk]) return;
+  const DecState& S = st[T.chunk];
+  const uint8_t* p = C.in + S.pay_off;
+  const double w = 2.0 * S.eb;
+  const uint32_t D = C.dim;
+  const uint32_t* us = ustart + static_cast<uint64_t>(C.seg0) * kSeg;
+  for (uint64_t e = T.e0 + threadIdx.x; e < T.e0 + T.ne; e += blockDim.x) {
+    const uint32_t row = fdiv(static_cast<uint32_t>(e), C.fd);
+    const uint32_t col = static_cast<uint32_t>(e) - row * D;
+    bool ok = true;
+    const uint32_t ga = unit_advance(seg_units, C.seg0, C.nseg, row_root[C.row_base + row], 1 + col, &ok);
+    const uint64_t v = unit_varint(p, us[ga]);
+    store_value(C, e, unzigzag(static_cast<uint32_t>(v)), w);
+  }
+}
+
+// ===========================================================================
+// Huffman: codebook tables (read_codebook + from_lengths + finalize,
+// huffman.hpp:132-148, :165-186, :213-222), then a self-synchronising
+// parallel decode of the MSB-first bitstream (huffman.hpp:254-291):
+//   H0 k_huff_tables  per chunk: validate the codebook exactly as the
+//                     reference does; canonical first/count/base per length, a
+//                     2^11-entry prefix LUT and the per-entry output values.
+//   H1 k_huff_spec    one thread per 256-bit subsequence decodes
+//                     speculatively from the subsequence start to the first
+//                     codeword boundary past its end.
+//   H2 k_huff_sync    per chunk: re-decode subsequences whose true start (the
+//                     predecessor's exit) differs until a fixpoint; scan the
+//                     symbol counts into output offsets; check count/validity.
+//   H3 k_huff_out     decode again from the true starts and write values.
+// Failures flag the chunk; k_dec_huff_seq then reproduces the exact error.
+// ===========================================================================
+constexpr int kL0 = 11;
+constexpr uint32_t kSubBits = 256;
+constexpr uint32_t kLong = 63;
+
+struct HTab {
+  uint32_t first[33], count[33], base[33];
+  uint32_t max_len, nent;
+  uint64_t nsym, bit_off, nbits;
+};
+
+__host__ __device__ inline uint64_t htab_bytes(uint32_t cap) {
+  return ((sizeof(HTab) + 4u * (1u << kL0) + 4ull * cap + 8ull * cap) + 15) & ~uint64_t(15);
+}
+
+struct HView {
+  HTab* tab;
+  uint32_t* lut;
+  int32_t* syms;
+  uint64_t* vals;
+};
+
+__device__ __forceinline__ HView hview(uint8_t* tabs, const DChunk& C) {
+  HView v;
+  uint8_t* b = tabs + C.tab_off;
+  v.tab = reinterpret_cast<HTab*>(b);
+  v.lut = reinterpret_cast<uint32_t*>(b + sizeof(HTab));
+  v.syms = reinterpret_cast<int32_t*>(b + sizeof(HTab) + 4u * (1u << kL0));
+  v.vals = reinterpret_cast<uint64_t*>(b + sizeof(HTab) + 4u * (1u << kL0) + 4ull * C.book_cap);
+  return v;
+}
+
 __device__ void bitonic_sort_u64(uint64_t* key, uint32_t p2) {
   for (uint32_t k = 2; k <= p2; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
@@ -237,27 +612,30 @@ __device__ void bitonic_sort_u64(uint64_t* key, uint32_t p2) {
   }
 }
 
-struct HuffTables {
-  uint32_t first[33], count[33], base[33];
-};
+__device__ __forceinline__ uint64_t value_bits(int32_t code, double w, int kind) {
+  if (kind == EMBC_OUT_F32) return __float_as_uint(__double2float_rn(reconstruct(code, w)));
+  if (kind == EMBC_OUT_F64) return static_cast<uint64_t>(__double_as_longlong(reconstruct(code, w)));
+  return static_cast<uint32_t>(code);
+}
 
-__global__ void __launch_bounds__(kBlock) k_dec_huff_seq(const DChunk* __restrict__ ch,
-                                                         DecState* __restrict__ st,
-                                                         const uint32_t* __restrict__ list,
-                                                         uint64_t* __restrict__ keys,
-                                                         int32_t* __restrict__ syms) {
+__global__ void __launch_bounds__(kBlock) k_huff_tables(const DChunk* __restrict__ ch,
+                                                        DecState* __restrict__ st,
+                                                        const uint32_t* __restrict__ list,
+                                                        uint64_t* __restrict__ keys,
+                                                        uint8_t* __restrict__ tabs,
+                                                        uint32_t* __restrict__ hflag) {
   __shared__ unsigned long long s_tmp64[33];
   __shared__ unsigned long long s_bad;
   __shared__ int s_stop;
-  __shared__ HuffTables tb;
+  __shared__ HTab tb;
   const uint32_t c = list[blockIdx.x];
   const DChunk C = ch[c];
   DecState& S = st[c];
   if (S.err != ~0ull) return;
   const uint8_t* p = C.in + S.pay_off;
   const uint64_t L = S.pay_len;
-  uint64_t* key = keys + C.book_off;
-  int32_t* sym = syms + C.book_off;
+  HView hv = hview(tabs, C);
+  uint64_t* key = keys + (C.tab_off / 8);  // keys region mirrors the table offsets (sized >= p2)
   if (threadIdx.x == 0) {
     s_stop = 0;
     s_bad = ~0ull;
@@ -323,16 +701,16 @@ __global__ void __launch_bounds__(kBlock) k_dec_huff_seq(const DChunk* __restric
   }
   __syncthreads();
   bitonic_sort_u64(key, p2);
-  // duplicate symbols (huffman.hpp:183-185): the map in finalize catches
-  // duplicates across lengths too, so test in symbol order.
-  for (uint32_t i = threadIdx.x; i < nent; i += blockDim.x) sym[i] = static_cast<int32_t>(static_cast<uint32_t>(key[i]) ^ 0x80000000u);
+  for (uint32_t i = threadIdx.x; i < nent; i += blockDim.x)
+    hv.syms[i] = static_cast<int32_t>(static_cast<uint32_t>(key[i]) ^ 0x80000000u);
   if (threadIdx.x < 33) {
     tb.count[threadIdx.x] = 0;
     tb.first[threadIdx.x] = 0;
     tb.base[threadIdx.x] = 0;
   }
   __syncthreads();
-  // canonical codes per length: first code of each length and its entry index
+  // canonical codes (closed form of finalize's shift-and-increment)
+  const double w = 2.0 * S.eb;
   unsigned long long carry = 0;
   for (uint32_t i0 = 0; i0 < nent; i0 += blockDim.x) {
     const uint32_t i = i0 + threadIdx.x;
@@ -352,34 +730,343 @@ __global__ void __launch_bounds__(kBlock) k_dec_huff_seq(const DChunk* __restric
         tb.base[len] = i;
       }
       atomicAdd(&tb.count[len], 1u);
+      hv.vals[i] = value_bits(hv.syms[i], w, C.out_kind);
     }
     carry += tot;
   }
   __syncthreads();
-  // duplicate check by symbol
+  // left-aligned code starts, ascending in canonical order -> prefix LUT
+  for (uint32_t i = threadIdx.x; i < nent; i += blockDim.x) {
+    const uint32_t len = static_cast<uint32_t>(key[i] >> 32);
+    // code_i = first[len] + (i - base[len])
+    const uint64_t code = tb.first[len] + (i - tb.base[len]);
+    key[i] = (code << (32 - len)) | (static_cast<uint64_t>(len) << 56);  // start < 2^32; len in top byte
+  }
+  __syncthreads();
+  for (uint32_t s = threadIdx.x; s < (1u << kL0); s += blockDim.x) {
+    const uint64_t V = static_cast<uint64_t>(s) << (32 - kL0);
+    const uint64_t Vend = V + (1ull << (32 - kL0));
+    // last entry with start <= V
+    int lo = 0, hi = static_cast<int>(nent) - 1, f = -1;
+    while (lo <= hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((key[mid] & 0xFFFFFFFFFFull) <= V) {
+        f = mid;
+        lo = mid + 1;
+      } else {
+        hi = mid - 1;
+      }
+    }
+    uint32_t ent = 0;
+    if (f >= 0) {
+      const uint32_t len = static_cast<uint32_t>(key[f] >> 56);
+      const uint64_t a = key[f] & 0xFFFFFFFFFFull;
+      if (V < a + (1ull << (32 - len))) ent = len <= kL0 ? (static_cast<uint32_t>(f) << 6) | len : kLong;
+    }
+    if (!ent && f + 1 < static_cast<int>(nent) && (key[f + 1] & 0xFFFFFFFFFFull) < Vend) ent = kLong;
+    hv.lut[s] = ent;
+  }
+  // duplicate symbols (huffman.hpp:183-185) across all lengths
   for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x)
-    key[i] = i < nent ? (static_cast<uint64_t>(static_cast<uint32_t>(sym[i]) ^ 0x80000000u) << 32) | i : ~0ull;
+    key[i] = i < nent ? (static_cast<uint64_t>(static_cast<uint32_t>(hv.syms[i]) ^ 0x80000000u) << 32) | i : ~0ull;
   __syncthreads();
   bitonic_sort_u64(key, p2);
   bool dup = false;
-  for (uint32_t i = 1 + threadIdx.x; i < nent; i += blockDim.x)
-    dup |= (key[i] >> 32) == (key[i - 1] >> 32);
+  for (uint32_t i = 1 + threadIdx.x; i < nent; i += blockDim.x) dup |= (key[i] >> 32) == (key[i - 1] >> 32);
   dup = __syncthreads_or(dup);
   if (dup) {
     if (threadIdx.x == 0) dec_fail(S, 0, EMBC_R_HUF_DUP, 0, 0);
     return;
   }
+  if (threadIdx.x == 0) {
+    uint32_t max_len = 0;  // entries().back().length (huffman.hpp:257)
+    for (uint32_t l = 1; l <= 32; ++l)
+      if (tb.count[l]) max_len = l;
+    tb.max_len = max_len;
+    tb.nent = nent;
+    tb.nsym = S.nsym;
+    tb.bit_off = 12 + 5ull * nent;
+    tb.nbits = 8 * (L - tb.bit_off);
+    *hv.tab = tb;
+    S.max_len = max_len;
+    S.bit_off = tb.bit_off;
+    if (S.nsym != C.N) hflag[c] = 1;  // decoded count != dim*count (container.hpp:169-172)
+  }
+}
+
+// 32 bits starting at bit `pos` of the stream (zeros past the end).
+__device__ __forceinline__ uint32_t peek32(const uint8_t* s, uint64_t nbytes, uint64_t pos) {
+  const uint64_t byte = pos >> 3;
+  const uint32_t sh = static_cast<uint32_t>(pos & 7);
+  uint64_t w = 0;
+  if (byte + 5 <= nbytes) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) w = (w << 8) | s[byte + k];
+  } else {
+    for (int k = 0; k < 5; ++k) w = (w << 8) | (byte + k < nbytes ? s[byte + k] : 0);
+  }
+  return static_cast<uint32_t>(w >> (8 - sh));
+}
+
+// One canonical codeword at `pos`: returns entry index and sets *len, or -1
+// if no codeword matches (invalid prefix).
+__device__ __forceinline__ int decode_one(const uint32_t* lut, const HTab& t, uint32_t bits, uint32_t* len) {
+  const uint32_t e = lut[bits >> (32 - kL0)];
+  if (e != kLong) {
+    if (!e) return -1;
+    *len = e & 63;
+    return static_cast<int>(e >> 6);
+  }
+  for (uint32_t l = kL0 + 1; l <= t.max_len; ++l) {
+    const uint32_t code = bits >> (32 - l);
+    if (t.count[l] && code >= t.first[l] && code - t.first[l] < t.count[l]) {
+      *len = l;
+      return static_cast<int>(t.base[l] + (code - t.first[l]));
+    }
+  }
+  return -1;
+}
+
+enum : uint32_t { HF_INVALID = 1, HF_ENDED = 2, HF_DEAD = 4 };
+
+// Decode from `pos` until crossing `end` (or the stream end / an invalid code).
+__device__ __forceinline__ void decode_run(const uint8_t* s, uint64_t nbytes, uint64_t nbits,
+                                           const uint32_t* lut, const HTab& t, uint64_t pos, uint64_t end,
+                                           uint64_t* x, uint32_t* cnt, uint32_t* flags) {
+  uint32_t c = 0, f = 0;
+  while (pos < end) {
+    if (pos >= nbits) {
+      f |= HF_ENDED;
+      break;
+    }
+    uint32_t len = 0;
+    const int ent = decode_one(lut, t, peek32(s, nbytes, pos), &len);
+    if (ent < 0) {
+      f |= HF_INVALID;
+      break;
+    }
+    if (pos + len > nbits) {
+      f |= HF_ENDED;
+      break;
+    }
+    pos += len;
+    ++c;
+  }
+  *x = pos;
+  *cnt = c;
+  *flags = f;
+}
+
+struct SubTile {
+  uint32_t chunk;
+  uint32_t first;  // first subsequence of this CTA (multiple of kSubPerBlock)
+};
+
+constexpr uint32_t kSubPerBlock = 128;
+constexpr uint32_t kMapsSmem = kSubPerBlock * kSubBits * sizeof(uint16_t);
+
+// Packed map entry: entry/exit bit offset (5 bits) | termination kind (2 bits)
+// | symbol count (25 bits).  Termination: 0 live, 1 invalid prefix, 2 stream end.
+__device__ __forceinline__ uint32_t pk(uint32_t off, uint32_t term, uint32_t cnt) {
+  return off | (term << 5) | (cnt << 7);
+}
+__device__ __forceinline__ uint32_t pk_off(uint32_t v) { return v & 31; }
+__device__ __forceinline__ uint32_t pk_term(uint32_t v) { return (v >> 5) & 3; }
+__device__ __forceinline__ uint32_t pk_cnt(uint32_t v) { return v >> 7; }
+
+// H1: for each subsequence i (bits [iK, iK+K)) and each possible entry offset
+// r < max_len, F_i(r) = (exit offset past (i+1)K, symbols decoded, termination).
+// Chains from different offsets are decoded one after another; a chain that
+// lands on a codeword boundary an earlier chain already visited has merged with
+// it and inherits its result (self-synchronising codes merge within a few
+// codewords; fixed-length codes need one full decode per residue class).
+// Then 32 lanes compose the block's maps: P_i(r) = F_{i-1} o ... o F_0 (r).
+__global__ void __launch_bounds__(kSubPerBlock) k_huff_maps(const DChunk* __restrict__ ch,
+                                                             const DecState* __restrict__ st,
+                                                             const SubTile* __restrict__ tiles,
+                                                             uint8_t* __restrict__ tabs,
+                                                             const uint32_t* __restrict__ hflag,
+                                                             uint32_t* __restrict__ pmaps,
+                                                             uint32_t* __restrict__ bmaps) {
+  __shared__ uint32_t lut[1 << kL0];
+  __shared__ HTab t;
+  // per thread: chain << 9 | count at each visited codeword boundary; after the
+  // thread's chains are done its row holds its 32 map entries (Fm)
+  extern __shared__ __align__(16) uint16_t marks_dyn[];
+  uint16_t (*marks)[kSubBits] = reinterpret_cast<uint16_t (*)[kSubBits]>(marks_dyn);
+  auto Fm = [&](uint32_t i, uint32_t r) -> uint32_t& { return reinterpret_cast<uint32_t*>(marks[i])[r]; };
+  const SubTile T = tiles[blockIdx.x];
+  const DChunk& C = ch[T.chunk];
+  if (st[T.chunk].err != ~0ull || hflag[T.chunk]) return;
+  HView hv = hview(tabs, C);
+  for (uint32_t i = threadIdx.x; i < (1u << kL0); i += blockDim.x) lut[i] = hv.lut[i];
+  if (threadIdx.x == 0) t = *hv.tab;
+  __syncthreads();
+  const uint8_t* s = C.in + st[T.chunk].pay_off + t.bit_off;
+  const uint64_t nbytes = t.nbits / 8;
+  const uint32_t R = t.max_len;
+  const uint32_t sub = T.first + threadIdx.x;
+  {
+    uint32_t visited[kSubBits / 32];
+#pragma unroll
+    for (int k = 0; k < kSubBits / 32; ++k) visited[k] = 0;
+    uint32_t res[32];
+    const uint64_t begin = static_cast<uint64_t>(sub) * kSubBits;
+    uint16_t* mk = marks[threadIdx.x];
+    for (uint32_t r = 0; r < 32; ++r) {
+      if (r >= R || sub >= C.nsub) {
+        res[r] = pk(0, 2, 0);
+        continue;
+      }
+      uint32_t p = r, cnt = 0, out = 0;
+      for (;;) {
+        if (p >= kSubBits) {
+          out = pk(p - kSubBits, 0, cnt);
+          break;
+        }
+        if ((visited[p >> 5] >> (p & 31)) & 1) {  // merged with an earlier chain
+          const uint32_t m = mk[p];
+          const uint32_t o = res[m >> 9];
+          out = pk(pk_off(o), pk_term(o), cnt + pk_cnt(o) - (m & 511));
+          break;
+        }
+        visited[p >> 5] |= 1u << (p & 31);
+        mk[p] = static_cast<uint16_t>((r << 9) | cnt);
+        const uint64_t pos = begin + p;
+        if (pos >= t.nbits) {
+          out = pk(0, 2, cnt);
+          break;
+        }
+        uint32_t len = 0;
+        if (decode_one(lut, t, peek32(s, nbytes, pos), &len) < 0) {
+          out = pk(0, 1, cnt);
+          break;
+        }
+        if (pos + len > t.nbits) {
+          out = pk(0, 2, cnt);
+          break;
+        }
+        p += len;
+        ++cnt;
+      }
+      res[r] = out;
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) Fm(threadIdx.x, r) = res[r];
+  }
+  __syncthreads();
+  // block prefix maps: lane r follows entry offset r through the block
+  if (threadIdx.x < 32) {
+    const uint32_t r = threadIdx.x;
+    uint32_t e = r, term = 0, cnt = 0;
+    const uint32_t nloc = min(kSubPerBlock, C.nsub - T.first);
+    for (uint32_t i = 0; i < nloc; ++i) {
+      pmaps[(C.sub0 + T.first + i) * 32 + r] = pk(e, term, cnt);
+      if (!term) {
+        const uint32_t f = Fm(i, e);
+        term = pk_term(f);
+        cnt += pk_cnt(f);
+        e = pk_off(f);
+      }
+    }
+    bmaps[((C.sub0 + T.first) / kSubPerBlock) * 32 + r] = pk(e, term, cnt);
+  }
+}
+
+// H2: per chunk, walk the block maps from entry offset 0: true entry offset and
+// output base of every block; then check that N symbols exist before the chain
+// terminates (huffman.hpp:274-288: exhaustion / invalid prefix).
+__global__ void k_huff_walk(const DChunk* __restrict__ ch, const DecState* __restrict__ st,
+                            const uint32_t* __restrict__ list, uint8_t* __restrict__ tabs,
+                            uint32_t* __restrict__ hflag, const uint32_t* __restrict__ bmaps,
+                            uint32_t* __restrict__ bentry, uint64_t* __restrict__ bbase) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t c = list[blockIdx.x];
+  const DChunk& C = ch[c];
+  if (st[c].err != ~0ull || hflag[c]) return;
+  const uint32_t nb = (C.nsub + kSubPerBlock - 1) / kSubPerBlock;
+  const uint32_t b0 = static_cast<uint32_t>(C.sub0 / kSubPerBlock);
+  for (uint32_t k = threadIdx.x; k < nb * 32; k += blockDim.x) sm[k] = bmaps[b0 * 32 + k];
+  __syncthreads();
   if (threadIdx.x != 0) return;
-  uint32_t max_len = 0;  // entries().back().length (huffman.hpp:257)
-  for (uint32_t l = 1; l <= 32; ++l)
-    if (tb.count[l]) max_len = l;
-  S.max_len = max_len;
-  S.bit_off = 12 + 5ull * nent;
-  // bit-serial decode (huffman.hpp:274-290)
-  const uint8_t* bits = p + S.bit_off;
-  const uint64_t nbytes = L - S.bit_off;
-  const uint64_t nsym = S.nsym;
-  const double w = 2.0 * S.eb;
+  HView hv = hview(tabs, C);
+  const uint64_t N = hv.tab->nsym;
+  uint32_t e = 0, term = 0;
+  uint64_t acc = 0;
+  for (uint32_t b = 0; b < nb; ++b) {
+    bentry[b0 + b] = term ? 0xFFFFFFFFu : e;
+    bbase[b0 + b] = acc;
+    if (term) continue;
+    const uint32_t m = sm[b * 32 + e];
+    acc += pk_cnt(m);
+    term = pk_term(m);
+    e = pk_off(m);
+  }
+  // every path terminates at the stream end (term 2) unless an invalid prefix
+  // comes first; either way fewer than N decodable symbols is an error
+  if (acc < N) hflag[c] = 1;
+}
+
+// H3: decode every subsequence from its true start and write the values.
+__global__ void __launch_bounds__(kSubPerBlock) k_huff_out(const DChunk* __restrict__ ch,
+                                                           const DecState* __restrict__ st,
+                                                           const SubTile* __restrict__ tiles,
+                                                           uint8_t* __restrict__ tabs,
+                                                           const uint32_t* __restrict__ hflag,
+                                                           const uint32_t* __restrict__ pmaps,
+                                                           const uint32_t* __restrict__ bentry,
+                                                           const uint64_t* __restrict__ bbase) {
+  __shared__ uint32_t lut[1 << kL0];
+  __shared__ HTab t;
+  const SubTile T = tiles[blockIdx.x];
+  const DChunk& C = ch[T.chunk];
+  if (st[T.chunk].err != ~0ull || hflag[T.chunk]) return;
+  HView hv = hview(tabs, C);
+  for (uint32_t i = threadIdx.x; i < (1u << kL0); i += blockDim.x) lut[i] = hv.lut[i];
+  if (threadIdx.x == 0) t = *hv.tab;
+  __syncthreads();
+  const uint32_t sub = T.first + threadIdx.x;
+  if (sub >= C.nsub) return;
+  const uint32_t bidx = static_cast<uint32_t>((C.sub0 + T.first) / kSubPerBlock);
+  const uint32_t be = bentry[bidx];
+  if (be == 0xFFFFFFFFu) return;
+  const uint32_t pm = pmaps[(C.sub0 + sub) * 32 + be];
+  if (pk_term(pm)) return;
+  const uint64_t base = bbase[bidx] + pk_cnt(pm);
+  if (base >= t.nsym) return;
+  const uint8_t* s = C.in + st[T.chunk].pay_off + t.bit_off;
+  const uint64_t nbytes = t.nbits / 8;
+  uint64_t pos = static_cast<uint64_t>(sub) * kSubBits + pk_off(pm);
+  const uint64_t end = static_cast<uint64_t>(sub + 1) * kSubBits;
+  const uint64_t stop = t.nsym - base;
+  const int kind = C.out_kind;
+  for (uint64_t k = 0; k < stop && pos < end && pos < t.nbits; ++k) {
+    uint32_t len = 0;
+    const int ent = decode_one(lut, t, peek32(s, nbytes, pos), &len);
+    if (ent < 0 || pos + len > t.nbits) break;
+    pos += len;
+    const uint64_t v = hv.vals[ent];
+    const uint64_t i = base + k;
+    if (kind == EMBC_OUT_F64) static_cast<uint64_t*>(C.out)[i] = v;
+    else static_cast<uint32_t*>(C.out)[i] = static_cast<uint32_t>(v);
+  }
+}
+
+// Exact sequential walk (huffman.hpp:274-290) for flagged chunks: reproduces
+// the reference's first error (exhaustion / invalid prefix / count).
+__global__ void k_dec_huff_seq(const DChunk* __restrict__ ch, DecState* __restrict__ st,
+                               const uint32_t* __restrict__ list, uint8_t* __restrict__ tabs,
+                               const uint32_t* __restrict__ hflag) {
+  if (threadIdx.x != 0) return;
+  const uint32_t c = list[blockIdx.x];
+  const DChunk C = ch[c];
+  DecState& S = st[c];
+  if (S.err != ~0ull || !hflag[c]) return;
+  HView hv = hview(tabs, C);
+  const HTab& tb = *hv.tab;
+  const uint8_t* bits = C.in + S.pay_off + tb.bit_off;
+  const uint64_t nbytes = tb.nbits / 8;
+  const uint64_t nsym = tb.nsym;
   uint64_t byte = 0;
   uint32_t shift = 0;
   for (uint64_t i = 0; i < nsym; ++i) {
@@ -397,10 +1084,14 @@ __global__ void __launch_bounds__(kBlock) k_dec_huff_seq(const DChunk* __restric
       code = (code << 1) | b;
       ++len;
       if (tb.count[len] != 0 && code >= tb.first[len] && code - tb.first[len] < tb.count[len]) {
-        if (i < C.N) store_value(C, i, sym[tb.base[len] + (code - tb.first[len])], w);
+        if (i < C.N) {
+          const uint64_t v = hv.vals[tb.base[len] + (code - tb.first[len])];
+          if (C.out_kind == EMBC_OUT_F64) static_cast<uint64_t*>(C.out)[i] = v;
+          else static_cast<uint32_t*>(C.out)[i] = static_cast<uint32_t>(v);
+        }
         break;
       }
-      if (len >= max_len) {
+      if (len >= tb.max_len) {
         dec_fail(S, i, EMBC_R_HUF_BAD_CODE, 0, 0);
         return;
       }
@@ -435,6 +1126,13 @@ __global__ void k_dec_fold(const DecState* __restrict__ st, uint32_t n, DevError
 
 }  // namespace embc_dev
 
+namespace embc_host {
+cudaError_t decode_set_attributes() {
+  return cudaFuncSetAttribute(embc_dev::k_huff_maps, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              embc_dev::kMapsSmem);
+}
+}  // namespace embc_host
+
 // ===========================================================================
 // host orchestration
 // ===========================================================================
@@ -450,12 +1148,17 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   if (!d_in) return set_error(ctx, EMBC_ERR_ARGUMENT, 0, 0, 0, 0, 0, "null input buffer");
   std::vector<DChunk> ch(n);
   std::vector<RawTile> raw_tiles;
+  std::vector<ElemTile> vlz_tiles;
+  std::vector<SegPair> segs;
+  std::vector<SubTile> subtiles;
   std::vector<uint32_t> vlz_list, huf_list;
-  uint64_t book_total = 0;
-  uint32_t max_p2 = 1;
+  uint64_t map_total = 0, row_total = 0, tab_total = 0, sub_total = 0;
+  uint32_t seg_total = 0, max_blocks = 1;
+  const uint64_t hdr = payload_only ? 0 : kHeader;
   for (uint32_t c = 0; c < n; ++c) {
     const embc_chunk_ref& r = refs[c];
     DChunk& C = ch[c];
+    std::memset(&C, 0, sizeof(C));
     if (r.codec > EMBC_CODEC_HUFFMAN || (!r.out && r.count && r.dim))
       return set_error(ctx, EMBC_ERR_ARGUMENT, 0, c, 0, 0, 0, "invalid chunk reference");
     C.in = d_in + r.offset;
@@ -468,41 +1171,72 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
     C.codec = r.codec;
     C.payload_only = payload_only ? 1 : 0;
     C.out_kind = static_cast<uint8_t>(out_kind);
-    C.book_off = 0;
-    C.book_cap = 0;
+    C.fd = make_fastdiv(r.dim);
+    const uint64_t pay = r.length > hdr ? r.length - hdr : 0;
     if (r.codec == EMBC_CODEC_RAW) {
       const uint64_t per = 8192;
       for (uint64_t e = 0; e < C.N; e += per) raw_tiles.push_back(RawTile{c, 0, e, std::min(per, C.N - e)});
     } else if (r.codec == EMBC_CODEC_VLZ) {
       vlz_list.push_back(c);
+      C.seq = (r.dim == 0 || r.dim > kVlzMaxDim || C.N >= (1ull << 31)) ? 1 : 0;
+      if (!C.seq) {
+        C.nseg = static_cast<uint32_t>((pay + kSeg - 1) / kSeg);
+        C.seg0 = seg_total;
+        seg_total += C.nseg;
+        C.map_base = map_total;
+        map_total += static_cast<uint64_t>(C.nseg) * (r.dim + 1);
+        C.row_base = row_total;
+        row_total += r.count;
+        for (uint32_t s = 0; s < C.nseg; ++s) segs.push_back(SegPair{c, s});
+        const uint64_t per = 8192;
+        for (uint64_t e = 0; e < C.N; e += per) vlz_tiles.push_back(ElemTile{c, 0, e, std::min(per, C.N - e)});
+      }
     } else {
-      const uint64_t hdr = payload_only ? 0 : kHeader;
-      const uint64_t cap = r.length > hdr + 12 ? (r.length - hdr - 12) / 5 + 1 : 1;
-      uint32_t p2 = 1;
+      const uint64_t cap = pay > 12 ? (pay - 12) / 5 + 1 : 1;
+      uint64_t p2 = 1;
       while (p2 < cap) p2 <<= 1;
-      C.book_off = static_cast<uint32_t>(book_total);
-      C.book_cap = static_cast<uint32_t>(cap);
-      book_total += p2;
-      max_p2 = std::max(max_p2, p2);
+      C.book_cap = static_cast<uint32_t>(std::max<uint64_t>(cap, p2));  // key region must hold p2
+      C.tab_off = tab_total;
+      tab_total += std::max<uint64_t>(htab_bytes(C.book_cap), 8 * p2 + 16);
+      C.nsub = static_cast<uint32_t>((8 * (pay > 12 ? pay - 12 : 0) + kSubBits - 1) / kSubBits);
+      C.sub0 = sub_total;  // block-aligned so each CTA's subsequences share one block map
+      sub_total += (C.nsub + kSubPerBlock - 1) / kSubPerBlock * kSubPerBlock;
+      max_blocks = std::max<uint32_t>(max_blocks, (C.nsub + kSubPerBlock - 1) / kSubPerBlock);
+      for (uint32_t s = 0; s < C.nsub; s += kSubPerBlock) subtiles.push_back(SubTile{c, s});
       huf_list.push_back(c);
     }
   }
   size_t off = 0;
-  const size_t o_ch = off;
-  off = align16(off + sizeof(DChunk) * n);
-  const size_t o_raw = off;
-  off = align16(off + sizeof(RawTile) * (raw_tiles.size() + 1));
-  const size_t o_vl = off;
-  off = align16(off + sizeof(uint32_t) * (vlz_list.size() + 1));
-  const size_t o_hl = off;
-  off = align16(off + sizeof(uint32_t) * (huf_list.size() + 1));
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align16(off + bytes);
+    return o;
+  };
+  const size_t o_ch = take(sizeof(DChunk) * n);
+  const size_t o_raw = take(sizeof(RawTile) * (raw_tiles.size() + 1));
+  const size_t o_vt = take(sizeof(ElemTile) * (vlz_tiles.size() + 1));
+  const size_t o_segs = take(sizeof(SegPair) * (segs.size() + 1));
+  const size_t o_st2 = take(sizeof(SubTile) * (subtiles.size() + 1));
+  const size_t o_vl = take(sizeof(uint32_t) * (vlz_list.size() + 1));
+  const size_t o_hl = take(sizeof(uint32_t) * (huf_list.size() + 1));
+  const size_t o_flags = take(sizeof(uint32_t) * 2 * n);  // vflag | hflag, zeroed by the upload
   const size_t host_bytes = off;
-  const size_t o_st = off;
-  off = align16(off + sizeof(DecState) * n);
-  const size_t o_keys = off;
-  off = align16(off + sizeof(uint64_t) * (book_total + 1));
-  const size_t o_syms = off;
-  off = align16(off + sizeof(int32_t) * (book_total + 1));
+  const size_t o_st = take(sizeof(DecState) * n);
+  const size_t o_ustart = take(sizeof(uint32_t) * (static_cast<size_t>(seg_total) * kSeg + 1));
+  const size_t o_ukind = take(static_cast<size_t>(seg_total) * kSeg + 1);
+  const size_t o_segu = take(sizeof(uint32_t) * (seg_total + 1));
+  const size_t o_sege = take(sizeof(uint32_t) * (seg_total + 1));
+  const size_t o_segr = take(sizeof(uint32_t) * (seg_total + 1));
+  const size_t o_maps = take(sizeof(uint64_t) * (map_total + 1));
+  const size_t o_rtag = take(sizeof(uint32_t) * (row_total + 1));
+  const size_t o_rsrc = take(sizeof(uint32_t) * (row_total + 1));
+  const size_t o_rroot = take(sizeof(uint32_t) * (row_total + 1));
+  const size_t o_tabs = take(tab_total + 16);
+  const size_t o_keys = take(tab_total + 16);
+  const size_t o_pmaps = take(sizeof(uint32_t) * 32 * (sub_total + 1));
+  const size_t o_bmaps = take(sizeof(uint32_t) * 32 * (sub_total / kSubPerBlock + 1));
+  const size_t o_bentry = take(sizeof(uint32_t) * (sub_total / kSubPerBlock + 1));
+  const size_t o_bbase = take(sizeof(uint64_t) * (sub_total / kSubPerBlock + 1));
   cudaError_t ce = ensure_scratch(ctx, off);
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "scratch allocation");
   uint8_t* hs = nullptr;
@@ -511,25 +1245,82 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "staging allocation");
   std::memcpy(hs + o_ch, ch.data(), sizeof(DChunk) * n);
   std::memcpy(hs + o_raw, raw_tiles.data(), sizeof(RawTile) * raw_tiles.size());
+  std::memcpy(hs + o_vt, vlz_tiles.data(), sizeof(ElemTile) * vlz_tiles.size());
+  std::memcpy(hs + o_segs, segs.data(), sizeof(SegPair) * segs.size());
+  std::memcpy(hs + o_st2, subtiles.data(), sizeof(SubTile) * subtiles.size());
   std::memcpy(hs + o_vl, vlz_list.data(), sizeof(uint32_t) * vlz_list.size());
   std::memcpy(hs + o_hl, huf_list.data(), sizeof(uint32_t) * huf_list.size());
+  std::memset(hs + o_flags, 0, sizeof(uint32_t) * 2 * n);
   uint8_t* d = ctx->d_scratch;
   ce = cudaMemcpyAsync(d, hs, host_bytes, cudaMemcpyHostToDevice, stream);
   if (ce == cudaSuccess) ce = stage_commit(ctx, slot, stream);
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "descriptor upload");
   const DChunk* d_ch = reinterpret_cast<const DChunk*>(d + o_ch);
   DecState* d_st = reinterpret_cast<DecState*>(d + o_st);
+  uint32_t* vflag = reinterpret_cast<uint32_t*>(d + o_flags);
+  uint32_t* hflag = vflag + n;
+  const uint32_t* d_vl = reinterpret_cast<const uint32_t*>(d + o_vl);
+  const uint32_t* d_hl = reinterpret_cast<const uint32_t*>(d + o_hl);
+  uint8_t* tabs = d + o_tabs;
   EMBC_TIMED(ctx, "k_dec_parse", stream, k_dec_parse<<<(n + 127) / 128, 128, 0, stream>>>(d_ch, d_st, n));
   if (!raw_tiles.empty())
-    EMBC_TIMED(ctx, "k_dec_raw", stream, k_dec_raw<<<static_cast<uint32_t>(raw_tiles.size()), kBlock, 0, stream>>>(
-        d_ch, d_st, reinterpret_cast<const RawTile*>(d + o_raw)));
-  if (!vlz_list.empty())
-    EMBC_TIMED(ctx, "k_dec_vlz_seq", stream, k_dec_vlz_seq<<<static_cast<uint32_t>(vlz_list.size()), 32, 0, stream>>>(
-        d_ch, d_st, reinterpret_cast<const uint32_t*>(d + o_vl)));
-  if (!huf_list.empty())
-    EMBC_TIMED(ctx, "k_dec_huff_seq", stream, k_dec_huff_seq<<<static_cast<uint32_t>(huf_list.size()), kBlock, 0, stream>>>(
-        d_ch, d_st, reinterpret_cast<const uint32_t*>(d + o_hl),
-        reinterpret_cast<uint64_t*>(d + o_keys), reinterpret_cast<int32_t*>(d + o_syms)));
+    EMBC_TIMED(ctx, "k_dec_raw", stream,
+               k_dec_raw<<<static_cast<uint32_t>(raw_tiles.size()), kBlock, 0, stream>>>(
+                   d_ch, d_st, reinterpret_cast<const RawTile*>(d + o_raw)));
+  if (!vlz_list.empty()) {
+    uint32_t* ustart = reinterpret_cast<uint32_t*>(d + o_ustart);
+    uint8_t* ukind = d + o_ukind;
+    uint32_t* segu = reinterpret_cast<uint32_t*>(d + o_segu);
+    uint32_t* sege = reinterpret_cast<uint32_t*>(d + o_sege);
+    uint32_t* segr = reinterpret_cast<uint32_t*>(d + o_segr);
+    uint64_t* maps = reinterpret_cast<uint64_t*>(d + o_maps);
+    uint32_t* rtag = reinterpret_cast<uint32_t*>(d + o_rtag);
+    uint32_t* rsrc = reinterpret_cast<uint32_t*>(d + o_rsrc);
+    uint32_t* rroot = reinterpret_cast<uint32_t*>(d + o_rroot);
+    const SegPair* d_segs = reinterpret_cast<const SegPair*>(d + o_segs);
+    const uint32_t nv = static_cast<uint32_t>(vlz_list.size());
+    if (!segs.empty())
+      EMBC_TIMED(ctx, "k_vlz_map", stream,
+                 k_vlz_map<<<static_cast<uint32_t>(segs.size()), kBlock, 0, stream>>>(
+                     d_ch, d_st, d_segs, ustart, ukind, segu, maps, vflag));
+    EMBC_TIMED(ctx, "k_vlz_chain", stream,
+               k_vlz_chain<<<(nv + 63) / 64, 64, 0, stream>>>(d_ch, d_st, d_vl, nv, maps, sege, segr, vflag));
+    if (!segs.empty())
+      EMBC_TIMED(ctx, "k_vlz_rows", stream,
+                 k_vlz_rows<<<static_cast<uint32_t>(segs.size()), kBlock, 0, stream>>>(
+                     d_ch, d_st, d_segs, ustart, ukind, segu, sege, segr, rtag, rsrc, vflag));
+    EMBC_TIMED(ctx, "k_vlz_roots", stream,
+               k_vlz_roots<<<nv, 1024, 0, stream>>>(d_ch, d_st, d_vl, vflag, rsrc, rtag, rroot));
+    if (!vlz_tiles.empty())
+      EMBC_TIMED(ctx, "k_vlz_out", stream,
+                 k_vlz_out<<<static_cast<uint32_t>(vlz_tiles.size()), kBlock, 0, stream>>>(
+                     d_ch, d_st, reinterpret_cast<const ElemTile*>(d + o_vt), vflag, ustart, segu, rroot));
+    EMBC_TIMED(ctx, "k_dec_vlz_seq", stream,
+               k_dec_vlz_seq<<<nv, 32, 0, stream>>>(d_ch, d_st, d_vl, vflag));
+  }
+  if (!huf_list.empty()) {
+    const uint32_t nh = static_cast<uint32_t>(huf_list.size());
+    uint32_t* pmaps = reinterpret_cast<uint32_t*>(d + o_pmaps);
+    uint32_t* bmaps = reinterpret_cast<uint32_t*>(d + o_bmaps);
+    uint32_t* bentry = reinterpret_cast<uint32_t*>(d + o_bentry);
+    uint64_t* bbase = reinterpret_cast<uint64_t*>(d + o_bbase);
+    const SubTile* d_subt = reinterpret_cast<const SubTile*>(d + o_st2);
+    EMBC_TIMED(ctx, "k_huff_tables", stream,
+               k_huff_tables<<<nh, kBlock, 0, stream>>>(d_ch, d_st, d_hl,
+                                                       reinterpret_cast<uint64_t*>(d + o_keys), tabs, hflag));
+    if (!subtiles.empty()) {
+      EMBC_TIMED(ctx, "k_huff_maps", stream,
+                 k_huff_maps<<<static_cast<uint32_t>(subtiles.size()), kSubPerBlock, kMapsSmem, stream>>>(
+                     d_ch, d_st, d_subt, tabs, hflag, pmaps, bmaps));
+      EMBC_TIMED(ctx, "k_huff_walk", stream,
+                 k_huff_walk<<<nh, 128, sizeof(uint32_t) * 32 * max_blocks, stream>>>(
+                     d_ch, d_st, d_hl, tabs, hflag, bmaps, bentry, bbase));
+      EMBC_TIMED(ctx, "k_huff_out", stream,
+                 k_huff_out<<<static_cast<uint32_t>(subtiles.size()), kSubPerBlock, 0, stream>>>(
+                     d_ch, d_st, d_subt, tabs, hflag, pmaps, bentry, bbase));
+    }
+    EMBC_TIMED(ctx, "k_dec_huff_seq", stream, k_dec_huff_seq<<<nh, 32, 0, stream>>>(d_ch, d_st, d_hl, tabs, hflag));
+  }
   EMBC_TIMED(ctx, "k_dec_fold", stream, k_dec_fold<<<1, 32, 0, stream>>>(d_st, n, ctx->d_err));
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "decode launch");

@@ -59,10 +59,17 @@ struct DChunk {
   uint64_t N;          // dim * count
   uint32_t dim, count;
   double eb;           // payload-only: the caller's bound (else read from the header)
-  uint8_t codec, payload_only, out_kind, pad;
-  uint32_t book_off;   // huffman: entry scratch offset
+  uint8_t codec, payload_only, out_kind, seq;  // seq: decode with the exact sequential walker
   uint32_t book_cap;   // huffman: entry capacity
-  uint32_t tile0;      // first decode tile
+  FastDiv fd;          // division by dim
+  // vlz plan
+  uint32_t seg0, nseg;     // global segment index range
+  uint64_t map_base;       // first segment-map entry
+  uint64_t row_base;       // first per-row entry
+  // huffman plan
+  uint64_t tab_off;        // byte offset of this chunk's decode tables
+  uint64_t sub0;           // first subsequence slot
+  uint32_t nsub, pad2;
 };
 
 // Per-chunk decode state (device).
