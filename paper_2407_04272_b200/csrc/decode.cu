@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(kBlock) k_vlz_out(const DChunk* __restrict__ c
 // Failures flag the chunk; k_dec_huff_seq then reproduces the exact error.
 // ===========================================================================
 constexpr int kL0 = 11;
-constexpr uint32_t kSubBits = 256;
+constexpr uint32_t kSubBits = 64;
 constexpr uint32_t kLong = 63;
 
 struct HTab {
@@ -862,8 +862,12 @@ struct SubTile {
   uint32_t first;  // first subsequence of this CTA (multiple of kSubPerBlock)
 };
 
-constexpr uint32_t kSubPerBlock = 128;
-constexpr uint32_t kMapsSmem = kSubPerBlock * kSubBits * sizeof(uint16_t);
+constexpr uint32_t kSubPerBlock = 256;                   // subsequences per CTA / block map
+constexpr uint32_t kGroup = 32;                          // subsequences per group map
+constexpr uint32_t kBlockBits = kSubBits * kSubPerBlock;  // bits staged per CTA
+constexpr uint32_t kStageWords = kBlockBits / 32 + 4;    // + look-ahead past the block
+constexpr int kClasses = 4;                              // distinct chains tracked per subsequence
+constexpr uint32_t kMapsSmem = 0;
 
 // Packed map entry: entry/exit bit offset (5 bits) | termination kind (2 bits)
 // | symbol count (25 bits).  Termination: 0 live, 1 invalid prefix, 2 stream end.
@@ -874,27 +878,54 @@ __device__ __forceinline__ uint32_t pk_off(uint32_t v) { return v & 31; }
 __device__ __forceinline__ uint32_t pk_term(uint32_t v) { return (v >> 5) & 3; }
 __device__ __forceinline__ uint32_t pk_cnt(uint32_t v) { return v >> 7; }
 
-// H1: for each subsequence i (bits [iK, iK+K)) and each possible entry offset
-// r < max_len, F_i(r) = (exit offset past (i+1)K, symbols decoded, termination).
-// Chains from different offsets are decoded one after another; a chain that
-// lands on a codeword boundary an earlier chain already visited has merged with
-// it and inherits its result (self-synchronising codes merge within a few
-// codewords; fixed-length codes need one full decode per residue class).
-// Then 32 lanes compose the block's maps: P_i(r) = F_{i-1} o ... o F_0 (r).
+// Stage the CTA's slice of the bitstream as big-endian 32-bit words.
+__device__ __forceinline__ void stage_bits(uint32_t* W, const uint8_t* s, uint64_t nbytes, uint64_t bit0) {
+  const uint64_t b0 = bit0 >> 3;  // bit0 is a multiple of 32
+  for (uint32_t w = threadIdx.x; w < kStageWords; w += blockDim.x) {
+    const uint64_t b = b0 + 4ull * w;
+    uint32_t v = 0;
+    if (b + 4 <= nbytes) {
+      v = (static_cast<uint32_t>(s[b]) << 24) | (static_cast<uint32_t>(s[b + 1]) << 16) |
+          (static_cast<uint32_t>(s[b + 2]) << 8) | s[b + 3];
+    } else {
+      for (int k = 0; k < 4; ++k) v = (v << 8) | (b + k < nbytes ? s[b + k] : 0);
+    }
+    W[w] = v;
+  }
+}
+
+// 32 bits at relative bit position p of the staged words.
+__device__ __forceinline__ uint32_t speek(const uint32_t* W, uint32_t p) {
+  const uint32_t i = p >> 5;
+  return __funnelshift_l(W[i + 1], W[i], p & 31);
+}
+
+__device__ __forceinline__ uint32_t popc_below(uint64_t bm, uint32_t p) {
+  return static_cast<uint32_t>(__popcll(bm & ((1ull << p) - 1ull)));
+}
+
+// H1: for subsequence i (bits [iK, iK+K)) and each possible entry offset
+// r < max_len: F_i(r) = (exit offset past (i+1)K, symbols, termination).
+// Chains are decoded one after another; the codeword starts of up to
+// kClasses distinct chains are kept as bitmaps in registers, and a chain that
+// lands on a start of a known chain has merged with it: its result follows by
+// a popcount.  (Self-synchronising codes merge within a few codewords;
+// fixed-length codes need one decode per residue class.)  Groups of 32
+// subsequences are then composed per entry offset (lane r), and the group maps
+// per block.
 __global__ void __launch_bounds__(kSubPerBlock) k_huff_maps(const DChunk* __restrict__ ch,
                                                              const DecState* __restrict__ st,
                                                              const SubTile* __restrict__ tiles,
                                                              uint8_t* __restrict__ tabs,
                                                              const uint32_t* __restrict__ hflag,
-                                                             uint32_t* __restrict__ pmaps,
+                                                             uint32_t* __restrict__ qmaps,
+                                                             uint32_t* __restrict__ gmaps,
                                                              uint32_t* __restrict__ bmaps) {
   __shared__ uint32_t lut[1 << kL0];
   __shared__ HTab t;
-  // per thread: chain << 9 | count at each visited codeword boundary; after the
-  // thread's chains are done its row holds its 32 map entries (Fm)
-  extern __shared__ __align__(16) uint16_t marks_dyn[];
-  uint16_t (*marks)[kSubBits] = reinterpret_cast<uint16_t (*)[kSubBits]>(marks_dyn);
-  auto Fm = [&](uint32_t i, uint32_t r) -> uint32_t& { return reinterpret_cast<uint32_t*>(marks[i])[r]; };
+  __shared__ uint32_t W[kStageWords];
+  __shared__ uint32_t Fm[kSubPerBlock][33];
+  __shared__ uint32_t G[kSubPerBlock / kGroup][32];
   const SubTile T = tiles[blockIdx.x];
   const DChunk& C = ch[T.chunk];
   if (st[T.chunk].err != ~0ull || hflag[T.chunk]) return;
@@ -902,74 +933,109 @@ __global__ void __launch_bounds__(kSubPerBlock) k_huff_maps(const DChunk* __rest
   for (uint32_t i = threadIdx.x; i < (1u << kL0); i += blockDim.x) lut[i] = hv.lut[i];
   if (threadIdx.x == 0) t = *hv.tab;
   __syncthreads();
-  const uint8_t* s = C.in + st[T.chunk].pay_off + t.bit_off;
-  const uint64_t nbytes = t.nbits / 8;
+  const uint64_t bit0 = static_cast<uint64_t>(T.first) * kSubBits;
+  stage_bits(W, C.in + st[T.chunk].pay_off + t.bit_off, t.nbits / 8, bit0);
+  __syncthreads();
   const uint32_t R = t.max_len;
   const uint32_t sub = T.first + threadIdx.x;
+  const uint64_t nbits = t.nbits;
   {
-    uint32_t visited[kSubBits / 32];
-#pragma unroll
-    for (int k = 0; k < kSubBits / 32; ++k) visited[k] = 0;
-    uint32_t res[32];
-    const uint64_t begin = static_cast<uint64_t>(sub) * kSubBits;
-    uint16_t* mk = marks[threadIdx.x];
+    static_assert(kSubBits == 64, "chain bitmaps are one 64-bit word");
+    uint64_t cbm[kClasses];
+    uint32_t cres[kClasses];
+    int ncls = 0;
+    const uint32_t base = threadIdx.x * kSubBits;  // relative bit of this subsequence
     for (uint32_t r = 0; r < 32; ++r) {
-      if (r >= R || sub >= C.nsub) {
-        res[r] = pk(0, 2, 0);
-        continue;
-      }
-      uint32_t p = r, cnt = 0, out = 0;
-      for (;;) {
-        if (p >= kSubBits) {
-          out = pk(p - kSubBits, 0, cnt);
-          break;
-        }
-        if ((visited[p >> 5] >> (p & 31)) & 1) {  // merged with an earlier chain
-          const uint32_t m = mk[p];
-          const uint32_t o = res[m >> 9];
-          out = pk(pk_off(o), pk_term(o), cnt + pk_cnt(o) - (m & 511));
-          break;
-        }
-        visited[p >> 5] |= 1u << (p & 31);
-        mk[p] = static_cast<uint16_t>((r << 9) | cnt);
-        const uint64_t pos = begin + p;
-        if (pos >= t.nbits) {
-          out = pk(0, 2, cnt);
-          break;
-        }
-        uint32_t len = 0;
-        if (decode_one(lut, t, peek32(s, nbytes, pos), &len) < 0) {
-          out = pk(0, 1, cnt);
-          break;
-        }
-        if (pos + len > t.nbits) {
-          out = pk(0, 2, cnt);
-          break;
-        }
-        p += len;
-        ++cnt;
-      }
-      res[r] = out;
-    }
+      uint32_t out = pk(0, 2, 0);
+      if (r < R && sub < C.nsub) {
+        int merged = -1;
+        uint32_t mpos = 0, cnt = 0;
+        uint64_t mine = 0;
+        uint32_t p = r;
+        for (;;) {
+          if (p >= kSubBits) {
+            out = pk(p - kSubBits, 0, cnt);
+            break;
+          }
 #pragma unroll
-    for (int r = 0; r < 32; ++r) Fm(threadIdx.x, r) = res[r];
+          for (int c = 0; c < kClasses; ++c)
+            if (merged < 0 && c < ncls && ((cbm[c] >> p) & 1)) merged = c;
+          if (merged >= 0) {
+            mpos = p;
+            break;
+          }
+          mine |= 1ull << p;
+          const uint64_t pos = bit0 + base + p;
+          if (pos >= nbits) {
+            out = pk(0, 2, cnt);
+            break;
+          }
+          uint32_t len = 0;
+          if (decode_one(lut, t, speek(W, base + p), &len) < 0) {
+            out = pk(0, 1, cnt);
+            break;
+          }
+          if (pos + len > nbits) {
+            out = pk(0, 2, cnt);
+            break;
+          }
+          p += len;
+          ++cnt;
+        }
+        if (merged >= 0) {
+#pragma unroll
+          for (int c = 0; c < kClasses; ++c) {
+            if (c == merged) {
+              const uint32_t o = cres[c];
+              out = pk(pk_off(o), pk_term(o), cnt + pk_cnt(o) - popc_below(cbm[c], mpos));
+            }
+          }
+        } else if (ncls < kClasses) {
+#pragma unroll
+          for (int c = 0; c < kClasses; ++c) {
+            if (c == ncls) {
+              cbm[c] = mine;
+              cres[c] = out;
+            }
+          }
+          ++ncls;
+        }
+      }
+      Fm[threadIdx.x][r] = out;
+    }
   }
   __syncthreads();
-  // block prefix maps: lane r follows entry offset r through the block
-  if (threadIdx.x < 32) {
-    const uint32_t r = threadIdx.x;
-    uint32_t e = r, term = 0, cnt = 0;
-    const uint32_t nloc = min(kSubPerBlock, C.nsub - T.first);
-    for (uint32_t i = 0; i < nloc; ++i) {
-      pmaps[(C.sub0 + T.first + i) * 32 + r] = pk(e, term, cnt);
-      if (!term) {
-        const uint32_t f = Fm(i, e);
+  // group prefix maps: warp g, lane r follows entry offset r through its 32 subsequences
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t nloc = min(kSubPerBlock, C.nsub - T.first);
+  {
+    uint32_t e = lane, term = 0, cnt = 0;
+    for (uint32_t j = 0; j < kGroup; ++j) {
+      const uint32_t i = warp * kGroup + j;
+      if (i < nloc) qmaps[(C.sub0 + T.first + i) * 32 + lane] = pk(e, term, cnt);
+      if (!term && i < nloc) {
+        const uint32_t f = Fm[i][e];
         term = pk_term(f);
         cnt += pk_cnt(f);
         e = pk_off(f);
       }
     }
-    bmaps[((C.sub0 + T.first) / kSubPerBlock) * 32 + r] = pk(e, term, cnt);
+    G[warp][lane] = pk(e, term, cnt);
+  }
+  __syncthreads();
+  if (warp == 0) {  // block prefix over groups
+    uint32_t e = lane, term = 0, cnt = 0;
+    const uint32_t gb = static_cast<uint32_t>((C.sub0 + T.first) / kGroup);
+    for (uint32_t g = 0; g < kSubPerBlock / kGroup; ++g) {
+      gmaps[(gb + g) * 32 + lane] = pk(e, term, cnt);
+      if (!term) {
+        const uint32_t f = G[g][e];
+        term = pk_term(f);
+        cnt += pk_cnt(f);
+        e = pk_off(f);
+      }
+    }
+    bmaps[((C.sub0 + T.first) / kSubPerBlock) * 32 + lane] = pk(e, term, cnt);
   }
 }
 
@@ -1013,38 +1079,46 @@ __global__ void __launch_bounds__(kSubPerBlock) k_huff_out(const DChunk* __restr
                                                            const SubTile* __restrict__ tiles,
                                                            uint8_t* __restrict__ tabs,
                                                            const uint32_t* __restrict__ hflag,
-                                                           const uint32_t* __restrict__ pmaps,
+                                                           const uint32_t* __restrict__ qmaps,
+                                                           const uint32_t* __restrict__ gmaps,
                                                            const uint32_t* __restrict__ bentry,
                                                            const uint64_t* __restrict__ bbase) {
   __shared__ uint32_t lut[1 << kL0];
   __shared__ HTab t;
+  __shared__ uint32_t W[kStageWords];
   const SubTile T = tiles[blockIdx.x];
   const DChunk& C = ch[T.chunk];
   if (st[T.chunk].err != ~0ull || hflag[T.chunk]) return;
+  const uint32_t bidx = static_cast<uint32_t>((C.sub0 + T.first) / kSubPerBlock);
+  const uint32_t be = bentry[bidx];
+  if (be == 0xFFFFFFFFu) return;
   HView hv = hview(tabs, C);
   for (uint32_t i = threadIdx.x; i < (1u << kL0); i += blockDim.x) lut[i] = hv.lut[i];
   if (threadIdx.x == 0) t = *hv.tab;
   __syncthreads();
+  const uint64_t bit0 = static_cast<uint64_t>(T.first) * kSubBits;
+  stage_bits(W, C.in + st[T.chunk].pay_off + t.bit_off, t.nbits / 8, bit0);
+  __syncthreads();
   const uint32_t sub = T.first + threadIdx.x;
   if (sub >= C.nsub) return;
-  const uint32_t bidx = static_cast<uint32_t>((C.sub0 + T.first) / kSubPerBlock);
-  const uint32_t be = bentry[bidx];
-  if (be == 0xFFFFFFFFu) return;
-  const uint32_t pm = pmaps[(C.sub0 + sub) * 32 + be];
-  if (pk_term(pm)) return;
-  const uint64_t base = bbase[bidx] + pk_cnt(pm);
+  const uint32_t gidx = static_cast<uint32_t>((C.sub0 + sub) / kGroup);
+  const uint32_t gm = gmaps[gidx * 32 + be];
+  if (pk_term(gm)) return;
+  const uint32_t qm = qmaps[(C.sub0 + sub) * 32 + pk_off(gm)];
+  if (pk_term(qm)) return;
+  const uint64_t base = bbase[bidx] + pk_cnt(gm) + pk_cnt(qm);
   if (base >= t.nsym) return;
-  const uint8_t* s = C.in + st[T.chunk].pay_off + t.bit_off;
-  const uint64_t nbytes = t.nbits / 8;
-  uint64_t pos = static_cast<uint64_t>(sub) * kSubBits + pk_off(pm);
-  const uint64_t end = static_cast<uint64_t>(sub + 1) * kSubBits;
+  const uint32_t rel0 = threadIdx.x * kSubBits;
+  uint32_t p = rel0 + pk_off(qm);
+  const uint32_t end = rel0 + kSubBits;
   const uint64_t stop = t.nsym - base;
+  const uint64_t nbits = t.nbits;
   const int kind = C.out_kind;
-  for (uint64_t k = 0; k < stop && pos < end && pos < t.nbits; ++k) {
+  for (uint64_t k = 0; k < stop && p < end && bit0 + p < nbits; ++k) {
     uint32_t len = 0;
-    const int ent = decode_one(lut, t, peek32(s, nbytes, pos), &len);
-    if (ent < 0 || pos + len > t.nbits) break;
-    pos += len;
+    const int ent = decode_one(lut, t, speek(W, p), &len);
+    if (ent < 0 || bit0 + p + len > nbits) break;
+    p += len;
     const uint64_t v = hv.vals[ent];
     const uint64_t i = base + k;
     if (kind == EMBC_OUT_F64) static_cast<uint64_t*>(C.out)[i] = v;
@@ -1128,8 +1202,7 @@ __global__ void k_dec_fold(const DecState* __restrict__ st, uint32_t n, DevError
 
 namespace embc_host {
 cudaError_t decode_set_attributes() {
-  return cudaFuncSetAttribute(embc_dev::k_huff_maps, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              embc_dev::kMapsSmem);
+  return cudaSuccess;
 }
 }  // namespace embc_host
 
@@ -1234,6 +1307,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   const size_t o_tabs = take(tab_total + 16);
   const size_t o_keys = take(tab_total + 16);
   const size_t o_pmaps = take(sizeof(uint32_t) * 32 * (sub_total + 1));
+  const size_t o_gmaps = take(sizeof(uint32_t) * 32 * (sub_total / kGroup + 1));
   const size_t o_bmaps = take(sizeof(uint32_t) * 32 * (sub_total / kSubPerBlock + 1));
   const size_t o_bentry = take(sizeof(uint32_t) * (sub_total / kSubPerBlock + 1));
   const size_t o_bbase = take(sizeof(uint64_t) * (sub_total / kSubPerBlock + 1));
@@ -1301,6 +1375,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   if (!huf_list.empty()) {
     const uint32_t nh = static_cast<uint32_t>(huf_list.size());
     uint32_t* pmaps = reinterpret_cast<uint32_t*>(d + o_pmaps);
+    uint32_t* gmaps = reinterpret_cast<uint32_t*>(d + o_gmaps);
     uint32_t* bmaps = reinterpret_cast<uint32_t*>(d + o_bmaps);
     uint32_t* bentry = reinterpret_cast<uint32_t*>(d + o_bentry);
     uint64_t* bbase = reinterpret_cast<uint64_t*>(d + o_bbase);
@@ -1310,14 +1385,14 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
                                                        reinterpret_cast<uint64_t*>(d + o_keys), tabs, hflag));
     if (!subtiles.empty()) {
       EMBC_TIMED(ctx, "k_huff_maps", stream,
-                 k_huff_maps<<<static_cast<uint32_t>(subtiles.size()), kSubPerBlock, kMapsSmem, stream>>>(
-                     d_ch, d_st, d_subt, tabs, hflag, pmaps, bmaps));
+                 k_huff_maps<<<static_cast<uint32_t>(subtiles.size()), kSubPerBlock, 0, stream>>>(
+                     d_ch, d_st, d_subt, tabs, hflag, pmaps, gmaps, bmaps));
       EMBC_TIMED(ctx, "k_huff_walk", stream,
                  k_huff_walk<<<nh, 128, sizeof(uint32_t) * 32 * max_blocks, stream>>>(
                      d_ch, d_st, d_hl, tabs, hflag, bmaps, bentry, bbase));
       EMBC_TIMED(ctx, "k_huff_out", stream,
                  k_huff_out<<<static_cast<uint32_t>(subtiles.size()), kSubPerBlock, 0, stream>>>(
-                     d_ch, d_st, d_subt, tabs, hflag, pmaps, bentry, bbase));
+                     d_ch, d_st, d_subt, tabs, hflag, pmaps, gmaps, bentry, bbase));
     }
     EMBC_TIMED(ctx, "k_dec_huff_seq", stream, k_dec_huff_seq<<<nh, 32, 0, stream>>>(d_ch, d_st, d_hl, tabs, hflag));
   }

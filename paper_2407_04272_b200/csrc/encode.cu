@@ -465,7 +465,28 @@ __global__ void __launch_bounds__(kBlock) k_sizes(const DJob* __restrict__ jobs,
       uint32_t found = 0;  // offset of the verified match, 0 = literal
       bool searching = active;
       // advance to the next hash candidate
+      // nearest candidate first; four independent hash loads per step
       auto next = [&]() {
+        while (k + 3 <= kmax) {
+          const uint32_t j = i - k;
+          uint64_t h0, h1, h2, h3;
+          if (staged) {
+            h0 = sh[j - lo];
+            h1 = sh[j - 1 - lo];
+            h2 = sh[j - 2 - lo];
+            h3 = sh[j - 3 - lo];
+          } else {
+            h0 = gh[j];
+            h1 = gh[j - 1];
+            h2 = gh[j - 2];
+            h3 = gh[j - 3];
+          }
+          if (h0 == h) return true;
+          if (h1 == h) { k += 1; return true; }
+          if (h2 == h) { k += 2; return true; }
+          if (h3 == h) { k += 3; return true; }
+          k += 4;
+        }
         while (k <= kmax) {
           const uint32_t j = i - k;
           const uint64_t hj = staged ? sh[j - lo] : gh[j];

@@ -1,0 +1,270 @@
+"""Compressed hybrid-parallel embedding all-to-all over torch.distributed
+(NCCL over NVLink on the B200 box; gloo in the CPU tests).
+
+Replaces the reference's in-process simulation (Simulator::rank_body,
+commsim.hpp:286-435) with a real exchange.  Layout:
+table t is owned by rank t mod R; in the forward pass the owner's lookup
+output [R*B, dim] is split into R slices of [B, dim], one per destination rank;
+every (destination, table) slice is one chunk.  Each rank:
+
+  stage 1  compresses its chunks in (destination, table) order into one send
+           buffer (one encode launch sequence, deterministic offsets);
+  stage 2  exchanges the 25-byte ChunkMetadata records (commsim.hpp:321-330,
+           the reference's two-round protocol) with a fixed-size
+           all-to-all, then reads the byte counts to the host (the one
+           synchronisation point per exchange);
+  stage 3  exchanges the variable-size payloads with all_to_all_single;
+  stage 4  decodes every received chunk straight into the consumer tensors,
+           verifying the metadata against each chunk header
+           (commsim.hpp:371-376).
+
+The backward pass sends each rank's [B, dim] gradient slice of every table to
+its owner through the same stages (a capability the reference only
+describes).  `uncompressed()` is the C3 baseline: raw fp32
+all-to-all of the same tensors.
+
+The codec backend is pluggable so the exchange logic can be tested on CPU:
+the product backend is GpuCodec (libembc_cuda.so); tests inject a CPU checker.
+"""
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import torch
+import torch.distributed as dist
+
+from . import codec as K
+from . import policy as P
+
+META = K.META_SIZE
+
+
+class GpuCodec:
+    """The product backend: sm_100a kernels through the C ABI."""
+
+    def __init__(self, ctx: Optional[K.Context] = None):
+        self.ctx = ctx or K.Context.default()
+
+    def encode(self, jobs: Sequence[K.EncodeJob], out: Optional[torch.Tensor] = None):
+        """-> (device uint8 buffer, device lengths int64 [njobs], device metadata uint8 [njobs, 25])."""
+        cj = [j.to_c() for j in jobs]
+        import ctypes as C
+        arr = (K._lib.Job * len(cj))(*cj)
+        bound = int(self.ctx._L.embc_encode_bound(arr, len(cj), K.LAYOUT_CHUNKS))
+        dev = jobs[0].batch.device
+        if out is None or out.numel() < bound:
+            out = torch.empty(max(bound, 1), dtype=torch.uint8, device=dev)
+        lens = torch.empty(len(cj), dtype=torch.int64, device=dev)
+        meta = torch.empty((len(cj), META), dtype=torch.uint8, device=dev)
+        self.ctx.encode_raw(cj, K.LAYOUT_CHUNKS, out, None, lens, meta, None)
+        del C
+        return out, lens, meta
+
+    def decode(self, buf: torch.Tensor, refs: Sequence[tuple], outs: Sequence[torch.Tensor]) -> None:
+        crefs = []
+        for (off, length, codec, dim, count), o in zip(refs, outs):
+            r = K._lib.ChunkRef()
+            r.offset, r.length, r.out = off, length, o.data_ptr() if o.numel() else None
+            r.dim, r.count, r.codec = dim, count, codec
+            crefs.append(r)
+        if crefs:
+            self.ctx.decode_raw(buf, crefs, K.OUT_F32, False)
+
+    def check(self) -> None:
+        self.ctx.sync()
+
+
+@dataclass
+class ExchangeStats:
+    """Per-rank accounting with the reference's definitions (commsim.hpp:68-83,
+    :322-353): bytes sent to other ranks only."""
+    uncompressed_bytes: int = 0
+    payload_bytes: int = 0
+    metadata_bytes: int = 0
+    times_ms: Dict[str, float] = field(default_factory=dict)
+
+    @property
+    def wire_bytes(self) -> int:
+        return self.payload_bytes + self.metadata_bytes
+
+    @property
+    def ratio(self) -> float:
+        return self.uncompressed_bytes / self.payload_bytes if self.payload_bytes else 1.0
+
+
+def _parse_meta(rec: bytes):
+    """parse_metadata (container.hpp:211-221)."""
+    clen, codec = struct.unpack_from("<QB", rec, 0)
+    eb, dim, count = struct.unpack_from("<dII", rec, 9)
+    return clen, codec, eb, dim, count
+
+
+class CompressedAllToAll:
+    def __init__(self, ntables: int, dim: int, batch: int, profiles: Dict[int, P.TableProfile],
+                 cfg: P.PolicyConfig, backend=None, group=None, device=None, window: int = 255,
+                 grad_profiles: Optional[Dict[int, P.TableProfile]] = None,
+                 grad_cfg: Optional[P.PolicyConfig] = None, timing: bool = False):
+        self.group = group
+        self.R = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.T, self.dim, self.B = ntables, dim, batch
+        self.profiles, self.cfg = profiles, cfg
+        self.grad_profiles = grad_profiles if grad_profiles is not None else profiles
+        self.grad_cfg = grad_cfg if grad_cfg is not None else cfg
+        self.backend = backend or GpuCodec()
+        self.device = device or (torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+                                 else torch.device("cpu"))
+        self.window = window
+        self.timing = timing and self.device.type == "cuda"
+        self.stats = ExchangeStats()
+        self._send_buf: Optional[torch.Tensor] = None
+
+    def owner(self, t: int) -> int:
+        return t % self.R
+
+    def owned(self, r: int) -> List[int]:
+        return [t for t in range(self.T) if t % self.R == r]
+
+    def _codec(self, profiles, t: int) -> int:
+        return profiles[t].codec if t in profiles else K.CODEC_RAW
+
+    # -- the four stages, shared by forward and backward ----------------------------
+    def _exchange(self, jobs: List[K.EncodeJob], job_dst: List[int], recv_plan: List[List[tuple]],
+                  outs: List[List[torch.Tensor]]) -> ExchangeStats:
+        """jobs are in (destination, table) order; recv_plan[src] lists the
+        (count, dim) of the chunks src sends here, in its job order; outs[src]
+        are the tensors they decode into."""
+        R = self.R
+        st = ExchangeStats()
+        ev = {}
+
+        def mark(name):
+            if self.timing:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                ev[name] = e
+
+        mark("start")
+        buf, lens, meta = self.backend.encode(jobs, self._send_buf)
+        self._send_buf = buf
+        mark("compressed")
+        # stage 2: metadata round (fixed 25 B per chunk)
+        send_cnt = [sum(1 for d in job_dst if d == r) for r in range(R)]
+        recv_cnt = [len(recv_plan[s]) for s in range(R)]
+        meta_recv = torch.empty((sum(recv_cnt), META), dtype=torch.uint8, device=meta.device)
+        if R > 1:
+            dist.all_to_all_single(meta_recv.view(-1), meta.view(-1), [c * META for c in recv_cnt],
+                                   [c * META for c in send_cnt], group=self.group)
+        else:
+            meta_recv.copy_(meta)
+        mark("metadata")
+        # the host needs the byte counts: one device -> host read per exchange
+        host = torch.cat([lens.view(-1), meta_recv.view(-1).to(torch.int64)]).cpu() if len(jobs) else \
+            torch.zeros(0, dtype=torch.int64)
+        lens_h = host[:len(jobs)].tolist()
+        meta_h = bytes(host[len(jobs):].to(torch.uint8).numpy().tobytes())
+        send_bytes = [0] * R
+        for l, d in zip(lens_h, job_dst):
+            send_bytes[d] += l
+        recs = [_parse_meta(meta_h[i * META:(i + 1) * META]) for i in range(sum(recv_cnt))]
+        recv_bytes = [0] * R
+        k = 0
+        for s in range(R):
+            for _ in range(recv_cnt[s]):
+                recv_bytes[s] += recs[k][0]
+                k += 1
+        total_send = sum(send_bytes)
+        recv = torch.empty(max(sum(recv_bytes), 1), dtype=torch.uint8, device=buf.device)
+        if R > 1:
+            dist.all_to_all_single(recv[:sum(recv_bytes)], buf[:total_send], recv_bytes, send_bytes,
+                                   group=self.group)
+        else:
+            recv[:total_send].copy_(buf[:total_send])
+        mark("payload")
+        # stage 4: decode into the consumer tensors; headers are checked
+        # against the metadata records on the device
+        refs, dst_tensors = [], []
+        off, k = 0, 0
+        for s in range(R):
+            for j, (count, dim) in enumerate(recv_plan[s]):
+                clen, codec, _eb, mdim, mcount = recs[k]
+                refs.append((off, clen, codec, mdim, mcount))
+                dst_tensors.append(outs[s][j])
+                if (mdim, mcount) != (dim, count):
+                    from ._lib import CodecFormatError
+                    raise CodecFormatError(f"rank {self.rank} decompress stage (from rank {s}): metadata from rank "
+                                           f"{s} disagrees with its chunk", status=2, reason=32)
+                off += clen
+                k += 1
+        self.backend.decode(recv, refs, dst_tensors)
+        mark("decompressed")
+        self.backend.check()
+        # accounting (reference definitions: d != src only)
+        for l, d, j in zip(lens_h, job_dst, jobs):
+            if d != self.rank:
+                st.payload_bytes += l
+                st.metadata_bytes += META
+                st.uncompressed_bytes += j.batch.numel() * 4
+        if self.timing:
+            names = list(ev)
+            for a, b in zip(names, names[1:]):
+                st.times_ms[b] = ev[a].elapsed_time(ev[b])
+            st.times_ms["total"] = ev[names[0]].elapsed_time(ev[names[-1]])
+        self.stats = st
+        return st
+
+    def forward(self, iteration: int, lookups: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
+        """lookups[t] for owned t: [R*B, dim] with rows d*B..(d+1)*B destined to
+        rank d.  Returns {t: [B, dim]} for every table (rank's data-parallel slice)."""
+        R, B = self.R, self.B
+        own = self.owned(self.rank)
+        jobs, job_dst = [], []
+        for d in range(R):
+            for t in own:
+                eb = P.eb_at(t, iteration, self.profiles, self.cfg)
+                jobs.append(K.EncodeJob(lookups[t][d * B:(d + 1) * B], eb, self._codec(self.profiles, t),
+                                        self.window))
+                job_dst.append(d)
+        out = {t: torch.empty((B, self.dim), dtype=torch.float32, device=self.device) for t in range(self.T)}
+        recv_plan = [[(B, self.dim) for _ in self.owned(s)] for s in range(R)]
+        outs = [[out[t] for t in self.owned(s)] for s in range(R)]
+        self._exchange(jobs, job_dst, recv_plan, outs)
+        return out
+
+    def backward(self, iteration: int, grads: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
+        """grads[t] for every table: [B, dim] local gradient slice.  Returns
+        {t: [R*B, dim]} for owned tables (rows s*B.. from rank s)."""
+        R, B = self.R, self.B
+        jobs, job_dst = [], []
+        for d in range(R):
+            for t in self.owned(d):
+                eb = P.eb_at(t, iteration, self.grad_profiles, self.grad_cfg)
+                jobs.append(K.EncodeJob(grads[t], eb, self._codec(self.grad_profiles, t), self.window))
+                job_dst.append(d)
+        own = self.owned(self.rank)
+        out = {t: torch.empty((R * B, self.dim), dtype=torch.float32, device=self.device) for t in own}
+        recv_plan = [[(B, self.dim) for _ in own] for s in range(R)]
+        outs = [[out[t][s * B:(s + 1) * B] for t in own] for s in range(R)]
+        self._exchange(jobs, job_dst, recv_plan, outs)
+        return out
+
+    def uncompressed(self, lookups: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
+        """C3 baseline: the same forward exchange as raw fp32 all_to_all_single."""
+        R, B, D = self.R, self.B, self.dim
+        own = self.owned(self.rank)
+        send = torch.cat([lookups[t][d * B:(d + 1) * B] for d in range(R) for t in own]) if own else \
+            torch.zeros((0, D), device=self.device)
+        recv_counts = [len(self.owned(s)) * B * D for s in range(R)]
+        recv = torch.empty(sum(recv_counts), dtype=torch.float32, device=self.device)
+        if R > 1:
+            dist.all_to_all_single(recv, send.reshape(-1), recv_counts, [len(own) * B * D] * R, group=self.group)
+        else:
+            recv.copy_(send.reshape(-1))
+        out, off = {}, 0
+        for s in range(R):
+            for t in self.owned(s):
+                out[t] = recv[off:off + B * D].view(B, D)
+                off += B * D
+        return out
