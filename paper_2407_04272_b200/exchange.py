@@ -70,7 +70,8 @@ class GpuCodec:
             r.dim, r.count, r.codec = dim, count, codec
             crefs.append(r)
         if crefs:
-            self.ctx.decode_raw(buf, crefs, K.OUT_F32, False)
+            kind = K.OUT_F64 if outs[0].dtype == torch.float64 else K.OUT_F32
+            self.ctx.decode_raw(buf, crefs, kind, False)
 
     def check(self) -> None:
         self.ctx.sync()
@@ -105,7 +106,8 @@ class CompressedAllToAll:
     def __init__(self, ntables: int, dim: int, batch: int, profiles: Dict[int, P.TableProfile],
                  cfg: P.PolicyConfig, backend=None, group=None, device=None, window: int = 255,
                  grad_profiles: Optional[Dict[int, P.TableProfile]] = None,
-                 grad_cfg: Optional[P.PolicyConfig] = None, timing: bool = False):
+                 grad_cfg: Optional[P.PolicyConfig] = None, timing: bool = False,
+                 out_dtype: torch.dtype = torch.float32):
         self.group = group
         self.R = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -118,6 +120,7 @@ class CompressedAllToAll:
                                  else torch.device("cpu"))
         self.window = window
         self.timing = timing and self.device.type == "cuda"
+        self.out_dtype = out_dtype  # float64 reproduces the reference's delivered doubles bit for bit
         self.stats = ExchangeStats()
         self._send_buf: Optional[torch.Tensor] = None
 
@@ -227,7 +230,7 @@ class CompressedAllToAll:
                 jobs.append(K.EncodeJob(lookups[t][d * B:(d + 1) * B], eb, self._codec(self.profiles, t),
                                         self.window))
                 job_dst.append(d)
-        out = {t: torch.empty((B, self.dim), dtype=torch.float32, device=self.device) for t in range(self.T)}
+        out = {t: torch.empty((B, self.dim), dtype=self.out_dtype, device=self.device) for t in range(self.T)}
         recv_plan = [[(B, self.dim) for _ in self.owned(s)] for s in range(R)]
         outs = [[out[t] for t in self.owned(s)] for s in range(R)]
         self._exchange(jobs, job_dst, recv_plan, outs)
@@ -244,7 +247,7 @@ class CompressedAllToAll:
                 jobs.append(K.EncodeJob(grads[t], eb, self._codec(self.grad_profiles, t), self.window))
                 job_dst.append(d)
         own = self.owned(self.rank)
-        out = {t: torch.empty((R * B, self.dim), dtype=torch.float32, device=self.device) for t in own}
+        out = {t: torch.empty((R * B, self.dim), dtype=self.out_dtype, device=self.device) for t in own}
         recv_plan = [[(B, self.dim) for _ in own] for s in range(R)]
         outs = [[out[t][s * B:(s + 1) * B] for t in own] for s in range(R)]
         self._exchange(jobs, job_dst, recv_plan, outs)
