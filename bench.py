@@ -273,15 +273,16 @@ def run_single(args):
     # algorithmic bytes per launch of the dominant kernel
     packed_mean = sum(s["packed"] for s in sets) / P
     n_by_codec = {c: sum(B * dim for t in range(T) if profiles[t].codec == c) for c in (0, 1, 2)}
-    algo = {
-        "k_quant_stats": 4 * T * B * dim,
-        "k_huff_hist": 4 * n_by_codec[2],
+    n_all = T * B * dim
+    s_vlz = packed_mean * n_by_codec[1] / max(1, n_all)  # compressed bytes of the vlz chunks (approx.)
+    s_huf = packed_mean * n_by_codec[2] / max(1, n_all)
+    algo = {  # compulsory bytes per launch ("Roofline")
+        "k_quant_stats": 4 * n_all,
         "k_sizes": 4 * (n_by_codec[1] + n_by_codec[2]),
-        "k_emit": 4 * T * B * dim + packed_mean,
-        "k_vlz_out": 4 * n_by_codec[1] + packed_mean * n_by_codec[1] / max(1, T * B * dim),
-        "k_huff_maps": packed_mean * n_by_codec[2] / max(1, T * B * dim),
-        "k_huff_out": 4 * n_by_codec[2] + packed_mean * n_by_codec[2] / max(1, T * B * dim),
-        "k_dec_raw": 8 * n_by_codec[0],
+        "k_emit": 4 * n_all + packed_mean,
+        "k_dec_s1": 8 * n_by_codec[0] + s_vlz,
+        "k_dec_s2": s_vlz + s_huf,
+        "k_dec_s3": 4 * (n_by_codec[1] + n_by_codec[2]) + s_vlz + s_huf,
     }
     hbm, peak_kind = peaks()
     ab = algo.get(dom)

@@ -208,6 +208,11 @@ embc_status embc_encode(embc_ctx* ctx, const embc_job* h_jobs, uint32_t njobs, i
 embc_status embc_decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* h_refs,
                         uint32_t nrefs, int out_kind, int payload_only, void* stream);
 
+/* Number of chunks of the last embc_decode call that took the exact
+ * sequential walker instead of the parallel decoders (malformed input, or a
+ * shape outside the parallel envelope).  Synchronous. */
+embc_status embc_decode_fallbacks(embc_ctx* ctx, uint32_t* h_count);
+
 /* ---- building blocks exposed for parity tests and the analysis path ---- */
 
 /* quantize() (quantizer.hpp:83-91) of fp32 (x_f64 == 0) or fp64 values. */

@@ -89,7 +89,7 @@ EXPORTS = [
     "embc_dequantize", "embc_match_stats", "embc_pattern_counts", "embc_decay_multiplier",
     "embc_classify_table", "embc_estimate_speedup", "embc_gen_table", "embc_gen_lookup_indices",
     "embc_mix_seed", "embc_gather_rows", "embc_reserve_capture", "embc_capture_reset",
-    "embc_timing_enable", "embc_timing_collect",
+    "embc_timing_enable", "embc_timing_collect", "embc_decode_fallbacks",
 ]
 
 _lock = threading.Lock()
@@ -136,6 +136,7 @@ def lib() -> C.CDLL:
                 "embc_capture_reset": (i32, [vp]),
                 "embc_timing_enable": (i32, [vp, i32]),
                 "embc_timing_collect": (i32, [vp, vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_float), i32]),
+                "embc_decode_fallbacks": (i32, [vp, C.POINTER(u32)]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)

@@ -384,3 +384,12 @@ def decode_packed(buf: bytes, out_kind: int = OUT_F32, ctx: Optional[Context] = 
         codec, dim, count = (CODEC_RAW, 0, 0) if h is None or h[0] > 2 else (h[0], h[2], h[3])
         refs.append((o, ln, codec, dim, count))
     return decode_chunks(buf, refs, out_kind, ctx=ctx)
+
+
+def decode_fallbacks(ctx: Optional[Context] = None) -> int:
+    """Chunks of the last decode that needed the exact sequential walker (0 for
+    valid streams inside the parallel envelope)."""
+    ctx = ctx or Context.default()
+    n = C.c_uint32()
+    ctx.check(ctx._L.embc_decode_fallbacks(ctx.handle, C.byref(n)))
+    return n.value

@@ -298,7 +298,8 @@ embc_status embc_ctx_create(int device, embc_ctx** out) {
   ctx->device = device;
   if (cudaMalloc(&ctx->d_err, sizeof(DevError)) != cudaSuccess ||
       cudaMemset(ctx->d_err, 0, sizeof(DevError)) != cudaSuccess ||
-      cudaMallocHost(&ctx->h_err, sizeof(DevError)) != cudaSuccess) {
+      cudaMallocHost(&ctx->h_err, sizeof(DevError)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_diag, 16) != cudaSuccess || cudaMemset(ctx->d_diag, 0, 16) != cudaSuccess) {
     embc_ctx_destroy(ctx);
     return EMBC_ERR_CUDA;
   }
@@ -310,6 +311,7 @@ void embc_ctx_destroy(embc_ctx* ctx) {
   if (!ctx) return;
   cudaDeviceSynchronize();
   if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->d_diag) cudaFree(ctx->d_diag);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->d_scratch) cudaFree(ctx->d_scratch);
   for (int k = 0; k < embc_ctx::kRing; ++k) {
@@ -457,6 +459,12 @@ embc_status embc_reserve_capture(embc_ctx* ctx, uint64_t bytes) {
   if (e != cudaSuccess) return cuda_fail(ctx, e, "embc_reserve_capture");
   ctx->arena_cap = bytes;
   return EMBC_OK;
+}
+
+embc_status embc_decode_fallbacks(embc_ctx* ctx, uint32_t* h_count) {
+  if (!ctx || !h_count) return EMBC_ERR_ARGUMENT;
+  cudaError_t e = cudaMemcpy(h_count, ctx->d_diag, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? EMBC_OK : cuda_fail(ctx, e, "embc_decode_fallbacks");
 }
 
 embc_status embc_capture_reset(embc_ctx* ctx) {

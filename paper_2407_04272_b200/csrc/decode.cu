@@ -132,10 +132,10 @@ struct RawTile {
   uint64_t e0, ne;
 };
 
-__global__ void __launch_bounds__(kBlock) k_dec_raw(const DChunk* __restrict__ ch,
+__device__ __forceinline__ void k_dec_raw_cta(uint32_t bid, const DChunk* __restrict__ ch,
                                                     const DecState* __restrict__ st,
                                                     const RawTile* __restrict__ tiles) {
-  const RawTile T = tiles[blockIdx.x];
+  const RawTile T = tiles[bid];
   const DChunk& C = ch[T.chunk];
   const DecState& S = st[T.chunk];
   if (S.err != ~0ull) return;
@@ -171,10 +171,10 @@ __device__ __forceinline__ bool rd_varint(const uint8_t* p, uint64_t L, uint64_t
   return false;
 }
 
-__global__ void k_dec_vlz_seq(const DChunk* __restrict__ ch, DecState* __restrict__ st,
+__device__ __forceinline__ void k_dec_vlz_seq_cta(uint32_t bid, const DChunk* __restrict__ ch, DecState* __restrict__ st,
                               const uint32_t* __restrict__ list, const uint32_t* __restrict__ vflag) {
   if (threadIdx.x != 0) return;
-  const uint32_t c = list[blockIdx.x];
+  const uint32_t c = bid;
   const DChunk C = ch[c];
   DecState& S = st[c];
   if (S.err != ~0ull || !(C.seq || vflag[c])) return;  // only chunks the parallel path did not finish
@@ -246,7 +246,7 @@ struct SegPair {
 };
 
 // unit kinds: 0 = tag 0x00, 1 = tag 0x01, 2 = not a valid tag
-__global__ void __launch_bounds__(kBlock) k_vlz_map(const DChunk* __restrict__ ch,
+__device__ __forceinline__ void k_vlz_map_cta(uint32_t bid, const DChunk* __restrict__ ch,
                                                     const DecState* __restrict__ st,
                                                     const SegPair* __restrict__ segs,
                                                     uint32_t* __restrict__ ustart,
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kBlock) k_vlz_map(const DChunk* __restrict__ c
   __shared__ uint32_t uend[kSeg];
   __shared__ uint32_t s_tmp32[33];
   __shared__ int s_bad;
-  const SegPair sp = segs[blockIdx.x];
+  const SegPair sp = segs[bid];
   const DChunk& C = ch[sp.chunk];
   if (st[sp.chunk].err != ~0ull || C.seq) return;
   const DecState& S = st[sp.chunk];
@@ -355,13 +355,10 @@ __global__ void __launch_bounds__(kBlock) k_vlz_map(const DChunk* __restrict__ c
   if (threadIdx.x == 0 && s_bad) vflag[sp.chunk] = 1;
 }
 
-__global__ void k_vlz_chain(const DChunk* __restrict__ ch, const DecState* __restrict__ st,
-                            const uint32_t* __restrict__ list, uint32_t nlist,
-                            const uint64_t* __restrict__ maps, uint32_t* __restrict__ seg_entry,
-                            uint32_t* __restrict__ seg_row0, uint32_t* __restrict__ vflag) {
-  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= nlist) return;
-  const uint32_t c = list[q];
+__device__ __forceinline__ void vlz_chain_one(const DChunk* __restrict__ ch, const DecState* __restrict__ st,
+                                              uint32_t c, const uint64_t* __restrict__ maps,
+                                              uint32_t* __restrict__ seg_entry, uint32_t* __restrict__ seg_row0,
+                                              uint32_t* __restrict__ vflag) {
   const DChunk& C = ch[c];
   if (st[c].err != ~0ull || C.seq || vflag[c]) return;
   const uint32_t D = C.dim;
@@ -412,7 +409,7 @@ __device__ __forceinline__ uint64_t unit_varint(const uint8_t* p, uint32_t start
   return v;
 }
 
-__global__ void __launch_bounds__(kBlock) k_vlz_rows(const DChunk* __restrict__ ch,
+__device__ __forceinline__ void k_vlz_rows_cta(uint32_t bid, uint8_t* dsm, const DChunk* __restrict__ ch,
                                                      const DecState* __restrict__ st,
                                                      const SegPair* __restrict__ segs,
                                                      const uint32_t* __restrict__ ustart,
@@ -423,8 +420,8 @@ __global__ void __launch_bounds__(kBlock) k_vlz_rows(const DChunk* __restrict__ 
                                                      uint32_t* __restrict__ row_tag,
                                                      uint32_t* __restrict__ row_src,
                                                      uint32_t* __restrict__ vflag) {
-  __shared__ uint16_t Jt[kLift][kSeg];
-  const SegPair sp = segs[blockIdx.x];
+  uint16_t (*Jt)[kSeg] = reinterpret_cast<uint16_t (*)[kSeg]>(dsm);
+  const SegPair sp = segs[bid];
   const DChunk& C = ch[sp.chunk];
   if (st[sp.chunk].err != ~0ull || C.seq || vflag[sp.chunk]) return;
   const DecState& S = st[sp.chunk];
@@ -481,17 +478,17 @@ __global__ void __launch_bounds__(kBlock) k_vlz_rows(const DChunk* __restrict__ 
   if (bad) vflag[sp.chunk] = 1;
 }
 
-constexpr uint32_t kRootSmem = 12288;
+constexpr uint32_t kRootSmem = 11264;  // rows resolved in shared memory (45 KiB of the stage-2 buffer)
 
-__global__ void __launch_bounds__(1024) k_vlz_roots(const DChunk* __restrict__ ch,
+__device__ __forceinline__ void k_vlz_roots_cta(uint32_t bid, uint8_t* dsm, const DChunk* __restrict__ ch,
                                                     const DecState* __restrict__ st,
                                                     const uint32_t* __restrict__ list,
                                                     const uint32_t* __restrict__ vflag,
                                                     uint32_t* __restrict__ row_src,
                                                     uint32_t* __restrict__ row_tag,
                                                     uint32_t* __restrict__ row_root) {
-  __shared__ uint32_t sh[kRootSmem];
-  const uint32_t c = list[blockIdx.x];
+  uint32_t* sh = reinterpret_cast<uint32_t*>(dsm);
+  const uint32_t c = bid;
   const DChunk& C = ch[c];
   if (st[c].err != ~0ull || C.seq || vflag[c]) return;
   const uint32_t n = C.count;
@@ -521,14 +518,14 @@ struct ElemTile {
   uint64_t e0, ne;
 };
 
-__global__ void __launch_bounds__(kBlock) k_vlz_out(const DChunk* __restrict__ ch,
+__device__ __forceinline__ void k_vlz_out_cta(uint32_t bid, const DChunk* __restrict__ ch,
                                                     const DecState* __restrict__ st,
                                                     const ElemTile* __restrict__ tiles,
                                                     const uint32_t* __restrict__ vflag,
                                                     const uint32_t* __restrict__ ustart,
                                                     const uint32_t* __restrict__ seg_units,
                                                     const uint32_t* __restrict__ row_root) {
-  const ElemTile T = tiles[blockIdx.x];
+  const ElemTile T = tiles[bid];
   const DChunk& C = ch[T.chunk];
   if (st[T.chunk].err != ~0ull || C.seq || vflag[T.chunk]) return;
   const DecState& S = st[T.chunk];
@@ -618,7 +615,7 @@ __device__ __forceinline__ uint64_t value_bits(int32_t code, double w, int kind)
   return static_cast<uint32_t>(code);
 }
 
-__global__ void __launch_bounds__(kBlock) k_huff_tables(const DChunk* __restrict__ ch,
+__device__ __forceinline__ void k_huff_tables_cta(uint32_t bid, const DChunk* __restrict__ ch,
                                                         DecState* __restrict__ st,
                                                         const uint32_t* __restrict__ list,
                                                         uint64_t* __restrict__ keys,
@@ -628,7 +625,7 @@ __global__ void __launch_bounds__(kBlock) k_huff_tables(const DChunk* __restrict
   __shared__ unsigned long long s_bad;
   __shared__ int s_stop;
   __shared__ HTab tb;
-  const uint32_t c = list[blockIdx.x];
+  const uint32_t c = list[bid];
   const DChunk C = ch[c];
   DecState& S = st[c];
   if (S.err != ~0ull) return;
@@ -766,6 +763,7 @@ __global__ void __launch_bounds__(kBlock) k_huff_tables(const DChunk* __restrict
     if (!ent && f + 1 < static_cast<int>(nent) && (key[f + 1] & 0xFFFFFFFFFFull) < Vend) ent = kLong;
     hv.lut[s] = ent;
   }
+  __syncthreads();  // the code starts in key[] are read above; reused below
   // duplicate symbols (huffman.hpp:183-185) across all lengths
   for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x)
     key[i] = i < nent ? (static_cast<uint64_t>(static_cast<uint32_t>(hv.syms[i]) ^ 0x80000000u) << 32) | i : ~0ull;
@@ -913,7 +911,7 @@ __device__ __forceinline__ uint32_t popc_below(uint64_t bm, uint32_t p) {
 // fixed-length codes need one decode per residue class.)  Groups of 32
 // subsequences are then composed per entry offset (lane r), and the group maps
 // per block.
-__global__ void __launch_bounds__(kSubPerBlock) k_huff_maps(const DChunk* __restrict__ ch,
+__device__ __forceinline__ void k_huff_maps_cta(uint32_t bid, uint8_t* dsm, const DChunk* __restrict__ ch,
                                                              const DecState* __restrict__ st,
                                                              const SubTile* __restrict__ tiles,
                                                              uint8_t* __restrict__ tabs,
@@ -921,12 +919,12 @@ __global__ void __launch_bounds__(kSubPerBlock) k_huff_maps(const DChunk* __rest
                                                              uint32_t* __restrict__ qmaps,
                                                              uint32_t* __restrict__ gmaps,
                                                              uint32_t* __restrict__ bmaps) {
-  __shared__ uint32_t lut[1 << kL0];
   __shared__ HTab t;
-  __shared__ uint32_t W[kStageWords];
-  __shared__ uint32_t Fm[kSubPerBlock][33];
-  __shared__ uint32_t G[kSubPerBlock / kGroup][32];
-  const SubTile T = tiles[blockIdx.x];
+  uint32_t* lut = reinterpret_cast<uint32_t*>(dsm);
+  uint32_t* W = lut + (1 << kL0);
+  uint32_t (*Fm)[33] = reinterpret_cast<uint32_t (*)[33]>(W + kStageWords);
+  uint32_t (*G)[32] = reinterpret_cast<uint32_t (*)[32]>(&Fm[kSubPerBlock][0]);
+  const SubTile T = tiles[bid];
   const DChunk& C = ch[T.chunk];
   if (st[T.chunk].err != ~0ull || hflag[T.chunk]) return;
   HView hv = hview(tabs, C);
@@ -1042,17 +1040,19 @@ __global__ void __launch_bounds__(kSubPerBlock) k_huff_maps(const DChunk* __rest
 // H2: per chunk, walk the block maps from entry offset 0: true entry offset and
 // output base of every block; then check that N symbols exist before the chain
 // terminates (huffman.hpp:274-288: exhaustion / invalid prefix).
-__global__ void k_huff_walk(const DChunk* __restrict__ ch, const DecState* __restrict__ st,
+__device__ __forceinline__ void k_huff_walk_cta(uint32_t bid, uint8_t* dsm, uint32_t dsm_words, const DChunk* __restrict__ ch, const DecState* __restrict__ st,
                             const uint32_t* __restrict__ list, uint8_t* __restrict__ tabs,
                             uint32_t* __restrict__ hflag, const uint32_t* __restrict__ bmaps,
                             uint32_t* __restrict__ bentry, uint64_t* __restrict__ bbase) {
-  extern __shared__ uint32_t sm[];
-  const uint32_t c = list[blockIdx.x];
+  uint32_t* sm = reinterpret_cast<uint32_t*>(dsm);
+  const uint32_t c = bid;
   const DChunk& C = ch[c];
   if (st[c].err != ~0ull || hflag[c]) return;
   const uint32_t nb = (C.nsub + kSubPerBlock - 1) / kSubPerBlock;
   const uint32_t b0 = static_cast<uint32_t>(C.sub0 / kSubPerBlock);
-  for (uint32_t k = threadIdx.x; k < nb * 32; k += blockDim.x) sm[k] = bmaps[b0 * 32 + k];
+  const bool in_smem = nb * 32 <= dsm_words;
+  if (in_smem)
+    for (uint32_t k = threadIdx.x; k < nb * 32; k += blockDim.x) sm[k] = bmaps[b0 * 32 + k];
   __syncthreads();
   if (threadIdx.x != 0) return;
   HView hv = hview(tabs, C);
@@ -1063,7 +1063,7 @@ __global__ void k_huff_walk(const DChunk* __restrict__ ch, const DecState* __res
     bentry[b0 + b] = term ? 0xFFFFFFFFu : e;
     bbase[b0 + b] = acc;
     if (term) continue;
-    const uint32_t m = sm[b * 32 + e];
+    const uint32_t m = in_smem ? sm[b * 32 + e] : bmaps[(b0 + b) * 32 + e];
     acc += pk_cnt(m);
     term = pk_term(m);
     e = pk_off(m);
@@ -1074,7 +1074,7 @@ __global__ void k_huff_walk(const DChunk* __restrict__ ch, const DecState* __res
 }
 
 // H3: decode every subsequence from its true start and write the values.
-__global__ void __launch_bounds__(kSubPerBlock) k_huff_out(const DChunk* __restrict__ ch,
+__device__ __forceinline__ void k_huff_out_cta(uint32_t bid, const DChunk* __restrict__ ch,
                                                            const DecState* __restrict__ st,
                                                            const SubTile* __restrict__ tiles,
                                                            uint8_t* __restrict__ tabs,
@@ -1086,7 +1086,7 @@ __global__ void __launch_bounds__(kSubPerBlock) k_huff_out(const DChunk* __restr
   __shared__ uint32_t lut[1 << kL0];
   __shared__ HTab t;
   __shared__ uint32_t W[kStageWords];
-  const SubTile T = tiles[blockIdx.x];
+  const SubTile T = tiles[bid];
   const DChunk& C = ch[T.chunk];
   if (st[T.chunk].err != ~0ull || hflag[T.chunk]) return;
   const uint32_t bidx = static_cast<uint32_t>((C.sub0 + T.first) / kSubPerBlock);
@@ -1128,11 +1128,11 @@ __global__ void __launch_bounds__(kSubPerBlock) k_huff_out(const DChunk* __restr
 
 // Exact sequential walk (huffman.hpp:274-290) for flagged chunks: reproduces
 // the reference's first error (exhaustion / invalid prefix / count).
-__global__ void k_dec_huff_seq(const DChunk* __restrict__ ch, DecState* __restrict__ st,
+__device__ __forceinline__ void k_dec_huff_seq_cta(uint32_t bid, const DChunk* __restrict__ ch, DecState* __restrict__ st,
                                const uint32_t* __restrict__ list, uint8_t* __restrict__ tabs,
                                const uint32_t* __restrict__ hflag) {
   if (threadIdx.x != 0) return;
-  const uint32_t c = list[blockIdx.x];
+  const uint32_t c = bid;
   const DChunk C = ch[c];
   DecState& S = st[c];
   if (S.err != ~0ull || !hflag[c]) return;
@@ -1177,8 +1177,7 @@ __global__ void k_dec_huff_seq(const DChunk* __restrict__ ch, DecState* __restri
 // ---------------------------------------------------------------------------
 // D9: fold the lowest failing chunk into the sticky record.
 // ---------------------------------------------------------------------------
-__global__ void k_dec_fold(const DecState* __restrict__ st, uint32_t n, DevError* err) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ __forceinline__ void dec_fold(const DecState* __restrict__ st, uint32_t n, DevError* err) {
   for (uint32_t c = 0; c < n; ++c) {
     const DecState& S = st[c];
     if (S.err == ~0ull) continue;
@@ -1196,6 +1195,120 @@ __global__ void k_dec_fold(const DecState* __restrict__ st, uint32_t n, DevError
                                         : EMBC_ERR_FORMAT;
     return;
   }
+}
+
+
+// ===========================================================================
+// Stage kernels: every decode call is k_dec_parse + four launches.  CTAs take
+// a role by blockIdx range; per-chunk follow-up work (the vlz segment-map
+// walk, the reference-chain resolution, the huffman block-map walk, the
+// failure fold) runs in the last CTA of its group to finish (an atomic ticket
+// after a __threadfence), so it needs no launch of its own.
+// ===========================================================================
+struct DecPlan {
+  uint32_t n_seg, n_htab, n_raw, n_sub, n_vt, nchunks;
+};
+
+struct DecArgs {
+  const DChunk* ch;
+  DecState* st;
+  const SegPair* segs;
+  const uint32_t* vlist;
+  const uint32_t* hlist;
+  const RawTile* raw;
+  const ElemTile* vtiles;
+  const SubTile* subt;
+  uint32_t* vflag;
+  uint32_t* hflag;
+  uint32_t* cnt;  // [3][nchunks] tickets + fold ticket
+  uint32_t* ustart;
+  uint8_t* ukind;
+  uint32_t* segu;
+  uint32_t* sege;
+  uint32_t* segr;
+  uint64_t* maps;
+  uint32_t* rtag;
+  uint32_t* rsrc;
+  uint32_t* rroot;
+  uint64_t* keys;
+  uint8_t* tabs;
+  uint32_t* qmaps;
+  uint32_t* gmaps;
+  uint32_t* bmaps;
+  uint32_t* bentry;
+  uint64_t* bbase;
+  DevError* err;
+  uint32_t* diag;  // [0]: chunks that needed the sequential walker in this call
+};
+
+constexpr uint32_t kStage2Smem = 45312;  // max(vlz lifting tables, huffman map scratch)
+
+__device__ __forceinline__ bool last_of(uint32_t* ticket, uint32_t total) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == total - 1;
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last != 0;
+}
+
+__global__ void __launch_bounds__(kBlock) k_dec_s1(DecPlan P, DecArgs a) {
+  uint32_t b = blockIdx.x;
+  if (b < P.n_seg) {
+    k_vlz_map_cta(b, a.ch, a.st, a.segs, a.ustart, a.ukind, a.segu, a.maps, a.vflag);
+    const uint32_t c = a.segs[b].chunk;
+    if (last_of(&a.cnt[c], a.ch[c].nseg) && threadIdx.x == 0)
+      vlz_chain_one(a.ch, a.st, c, a.maps, a.sege, a.segr, a.vflag);
+    return;
+  }
+  b -= P.n_seg;
+  if (b < P.n_htab) {
+    k_huff_tables_cta(b, a.ch, a.st, a.hlist, a.keys, a.tabs, a.hflag);
+    return;
+  }
+  b -= P.n_htab;
+  k_dec_raw_cta(b, a.ch, a.st, a.raw);
+}
+
+__global__ void __launch_bounds__(kBlock) k_dec_s2(DecPlan P, DecArgs a) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  uint32_t b = blockIdx.x;
+  if (b < P.n_seg) {
+    k_vlz_rows_cta(b, dsm, a.ch, a.st, a.segs, a.ustart, a.ukind, a.segu, a.sege, a.segr, a.rtag, a.rsrc,
+                   a.vflag);
+    const uint32_t c = a.segs[b].chunk;
+    if (last_of(&a.cnt[P.nchunks + c], a.ch[c].nseg))
+      k_vlz_roots_cta(c, dsm, a.ch, a.st, nullptr, a.vflag, a.rsrc, a.rtag, a.rroot);
+    return;
+  }
+  b -= P.n_seg;
+  k_huff_maps_cta(b, dsm, a.ch, a.st, a.subt, a.tabs, a.hflag, a.qmaps, a.gmaps, a.bmaps);
+  const uint32_t c = a.subt[b].chunk;
+  if (last_of(&a.cnt[P.nchunks + c], (a.ch[c].nsub + kSubPerBlock - 1) / kSubPerBlock))
+    k_huff_walk_cta(c, dsm, kStage2Smem / 4, a.ch, a.st, nullptr, a.tabs, a.hflag, a.bmaps, a.bentry, a.bbase);
+}
+
+__global__ void __launch_bounds__(kBlock) k_dec_s3(DecPlan P, DecArgs a) {
+  const uint32_t b = blockIdx.x;
+  if (b < P.n_vt) {
+    k_vlz_out_cta(b, a.ch, a.st, a.vtiles, a.vflag, a.ustart, a.segu, a.rroot);
+    return;
+  }
+  k_huff_out_cta(b - P.n_vt, a.ch, a.st, a.subt, a.tabs, a.hflag, a.qmaps, a.gmaps, a.bentry, a.bbase);
+}
+
+// Exact sequential walkers for chunks the parallel path flagged (they
+// reproduce the reference's first error and message), then the fold.
+__global__ void __launch_bounds__(32) k_dec_s4(DecPlan P, DecArgs a) {
+  const uint32_t c = blockIdx.x;
+  const uint8_t codec = a.ch[c].codec;
+  if (threadIdx.x == 0 && a.st[c].err == ~0ull &&
+      ((codec == EMBC_CODEC_VLZ && (a.ch[c].seq || a.vflag[c])) || (codec == EMBC_CODEC_HUFFMAN && a.hflag[c])))
+    atomicAdd(a.diag, 1u);
+  if (codec == EMBC_CODEC_VLZ) k_dec_vlz_seq_cta(c, a.ch, a.st, nullptr, a.vflag);
+  else if (codec == EMBC_CODEC_HUFFMAN) k_dec_huff_seq_cta(c, a.ch, a.st, nullptr, a.tabs, a.hflag);
+  if (last_of(&a.cnt[2 * P.nchunks], P.nchunks) && threadIdx.x == 0) dec_fold(a.st, P.nchunks, a.err);
 }
 
 }  // namespace embc_dev
@@ -1251,7 +1364,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
       for (uint64_t e = 0; e < C.N; e += per) raw_tiles.push_back(RawTile{c, 0, e, std::min(per, C.N - e)});
     } else if (r.codec == EMBC_CODEC_VLZ) {
       vlz_list.push_back(c);
-      C.seq = (r.dim == 0 || r.dim > kVlzMaxDim || C.N >= (1ull << 31)) ? 1 : 0;
+      C.seq = (r.dim == 0 || r.dim > kVlzMaxDim || C.N >= (1ull << 31) || (pay == 0 && r.count > 0)) ? 1 : 0;
       if (!C.seq) {
         C.nseg = static_cast<uint32_t>((pay + kSeg - 1) / kSeg);
         C.seg0 = seg_total;
@@ -1292,7 +1405,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   const size_t o_st2 = take(sizeof(SubTile) * (subtiles.size() + 1));
   const size_t o_vl = take(sizeof(uint32_t) * (vlz_list.size() + 1));
   const size_t o_hl = take(sizeof(uint32_t) * (huf_list.size() + 1));
-  const size_t o_flags = take(sizeof(uint32_t) * 2 * n);  // vflag | hflag, zeroed by the upload
+  const size_t o_flags = take(sizeof(uint32_t) * (5 * n + 1));  // vflag | hflag | tickets, zeroed by the upload
   const size_t host_bytes = off;
   const size_t o_st = take(sizeof(DecState) * n);
   const size_t o_ustart = take(sizeof(uint32_t) * (static_cast<size_t>(seg_total) * kSeg + 1));
@@ -1324,7 +1437,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   std::memcpy(hs + o_st2, subtiles.data(), sizeof(SubTile) * subtiles.size());
   std::memcpy(hs + o_vl, vlz_list.data(), sizeof(uint32_t) * vlz_list.size());
   std::memcpy(hs + o_hl, huf_list.data(), sizeof(uint32_t) * huf_list.size());
-  std::memset(hs + o_flags, 0, sizeof(uint32_t) * 2 * n);
+  std::memset(hs + o_flags, 0, sizeof(uint32_t) * (5 * n + 1));
   uint8_t* d = ctx->d_scratch;
   ce = cudaMemcpyAsync(d, hs, host_bytes, cudaMemcpyHostToDevice, stream);
   if (ce == cudaSuccess) ce = stage_commit(ctx, slot, stream);
@@ -1336,67 +1449,52 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   const uint32_t* d_vl = reinterpret_cast<const uint32_t*>(d + o_vl);
   const uint32_t* d_hl = reinterpret_cast<const uint32_t*>(d + o_hl);
   uint8_t* tabs = d + o_tabs;
+  DecArgs a{};
+  a.ch = d_ch;
+  a.st = d_st;
+  a.segs = reinterpret_cast<const SegPair*>(d + o_segs);
+  a.vlist = d_vl;
+  a.hlist = d_hl;
+  a.raw = reinterpret_cast<const RawTile*>(d + o_raw);
+  a.vtiles = reinterpret_cast<const ElemTile*>(d + o_vt);
+  a.subt = reinterpret_cast<const SubTile*>(d + o_st2);
+  a.vflag = vflag;
+  a.hflag = hflag;
+  a.cnt = vflag + 2 * n;
+  a.ustart = reinterpret_cast<uint32_t*>(d + o_ustart);
+  a.ukind = d + o_ukind;
+  a.segu = reinterpret_cast<uint32_t*>(d + o_segu);
+  a.sege = reinterpret_cast<uint32_t*>(d + o_sege);
+  a.segr = reinterpret_cast<uint32_t*>(d + o_segr);
+  a.maps = reinterpret_cast<uint64_t*>(d + o_maps);
+  a.rtag = reinterpret_cast<uint32_t*>(d + o_rtag);
+  a.rsrc = reinterpret_cast<uint32_t*>(d + o_rsrc);
+  a.rroot = reinterpret_cast<uint32_t*>(d + o_rroot);
+  a.keys = reinterpret_cast<uint64_t*>(d + o_keys);
+  a.tabs = tabs;
+  a.qmaps = reinterpret_cast<uint32_t*>(d + o_pmaps);
+  a.gmaps = reinterpret_cast<uint32_t*>(d + o_gmaps);
+  a.bmaps = reinterpret_cast<uint32_t*>(d + o_bmaps);
+  a.bentry = reinterpret_cast<uint32_t*>(d + o_bentry);
+  a.bbase = reinterpret_cast<uint64_t*>(d + o_bbase);
+  a.err = ctx->d_err;
+  a.diag = ctx->d_diag;
+  cudaMemsetAsync(ctx->d_diag, 0, sizeof(uint32_t), stream);
+  DecPlan P{};
+  P.n_seg = static_cast<uint32_t>(segs.size());
+  P.n_htab = static_cast<uint32_t>(huf_list.size());
+  P.n_raw = static_cast<uint32_t>(raw_tiles.size());
+  P.n_sub = static_cast<uint32_t>(subtiles.size());
+  P.n_vt = static_cast<uint32_t>(vlz_tiles.size());
+  P.nchunks = n;
   EMBC_TIMED(ctx, "k_dec_parse", stream, k_dec_parse<<<(n + 127) / 128, 128, 0, stream>>>(d_ch, d_st, n));
-  if (!raw_tiles.empty())
-    EMBC_TIMED(ctx, "k_dec_raw", stream,
-               k_dec_raw<<<static_cast<uint32_t>(raw_tiles.size()), kBlock, 0, stream>>>(
-                   d_ch, d_st, reinterpret_cast<const RawTile*>(d + o_raw)));
-  if (!vlz_list.empty()) {
-    uint32_t* ustart = reinterpret_cast<uint32_t*>(d + o_ustart);
-    uint8_t* ukind = d + o_ukind;
-    uint32_t* segu = reinterpret_cast<uint32_t*>(d + o_segu);
-    uint32_t* sege = reinterpret_cast<uint32_t*>(d + o_sege);
-    uint32_t* segr = reinterpret_cast<uint32_t*>(d + o_segr);
-    uint64_t* maps = reinterpret_cast<uint64_t*>(d + o_maps);
-    uint32_t* rtag = reinterpret_cast<uint32_t*>(d + o_rtag);
-    uint32_t* rsrc = reinterpret_cast<uint32_t*>(d + o_rsrc);
-    uint32_t* rroot = reinterpret_cast<uint32_t*>(d + o_rroot);
-    const SegPair* d_segs = reinterpret_cast<const SegPair*>(d + o_segs);
-    const uint32_t nv = static_cast<uint32_t>(vlz_list.size());
-    if (!segs.empty())
-      EMBC_TIMED(ctx, "k_vlz_map", stream,
-                 k_vlz_map<<<static_cast<uint32_t>(segs.size()), kBlock, 0, stream>>>(
-                     d_ch, d_st, d_segs, ustart, ukind, segu, maps, vflag));
-    EMBC_TIMED(ctx, "k_vlz_chain", stream,
-               k_vlz_chain<<<(nv + 63) / 64, 64, 0, stream>>>(d_ch, d_st, d_vl, nv, maps, sege, segr, vflag));
-    if (!segs.empty())
-      EMBC_TIMED(ctx, "k_vlz_rows", stream,
-                 k_vlz_rows<<<static_cast<uint32_t>(segs.size()), kBlock, 0, stream>>>(
-                     d_ch, d_st, d_segs, ustart, ukind, segu, sege, segr, rtag, rsrc, vflag));
-    EMBC_TIMED(ctx, "k_vlz_roots", stream,
-               k_vlz_roots<<<nv, 1024, 0, stream>>>(d_ch, d_st, d_vl, vflag, rsrc, rtag, rroot));
-    if (!vlz_tiles.empty())
-      EMBC_TIMED(ctx, "k_vlz_out", stream,
-                 k_vlz_out<<<static_cast<uint32_t>(vlz_tiles.size()), kBlock, 0, stream>>>(
-                     d_ch, d_st, reinterpret_cast<const ElemTile*>(d + o_vt), vflag, ustart, segu, rroot));
-    EMBC_TIMED(ctx, "k_dec_vlz_seq", stream,
-               k_dec_vlz_seq<<<nv, 32, 0, stream>>>(d_ch, d_st, d_vl, vflag));
-  }
-  if (!huf_list.empty()) {
-    const uint32_t nh = static_cast<uint32_t>(huf_list.size());
-    uint32_t* pmaps = reinterpret_cast<uint32_t*>(d + o_pmaps);
-    uint32_t* gmaps = reinterpret_cast<uint32_t*>(d + o_gmaps);
-    uint32_t* bmaps = reinterpret_cast<uint32_t*>(d + o_bmaps);
-    uint32_t* bentry = reinterpret_cast<uint32_t*>(d + o_bentry);
-    uint64_t* bbase = reinterpret_cast<uint64_t*>(d + o_bbase);
-    const SubTile* d_subt = reinterpret_cast<const SubTile*>(d + o_st2);
-    EMBC_TIMED(ctx, "k_huff_tables", stream,
-               k_huff_tables<<<nh, kBlock, 0, stream>>>(d_ch, d_st, d_hl,
-                                                       reinterpret_cast<uint64_t*>(d + o_keys), tabs, hflag));
-    if (!subtiles.empty()) {
-      EMBC_TIMED(ctx, "k_huff_maps", stream,
-                 k_huff_maps<<<static_cast<uint32_t>(subtiles.size()), kSubPerBlock, 0, stream>>>(
-                     d_ch, d_st, d_subt, tabs, hflag, pmaps, gmaps, bmaps));
-      EMBC_TIMED(ctx, "k_huff_walk", stream,
-                 k_huff_walk<<<nh, 128, sizeof(uint32_t) * 32 * max_blocks, stream>>>(
-                     d_ch, d_st, d_hl, tabs, hflag, bmaps, bentry, bbase));
-      EMBC_TIMED(ctx, "k_huff_out", stream,
-                 k_huff_out<<<static_cast<uint32_t>(subtiles.size()), kSubPerBlock, 0, stream>>>(
-                     d_ch, d_st, d_subt, tabs, hflag, pmaps, gmaps, bentry, bbase));
-    }
-    EMBC_TIMED(ctx, "k_dec_huff_seq", stream, k_dec_huff_seq<<<nh, 32, 0, stream>>>(d_ch, d_st, d_hl, tabs, hflag));
-  }
-  EMBC_TIMED(ctx, "k_dec_fold", stream, k_dec_fold<<<1, 32, 0, stream>>>(d_st, n, ctx->d_err));
+  if (P.n_seg + P.n_htab + P.n_raw)
+    EMBC_TIMED(ctx, "k_dec_s1", stream, k_dec_s1<<<P.n_seg + P.n_htab + P.n_raw, kBlock, 0, stream>>>(P, a));
+  if (P.n_seg + P.n_sub)
+    EMBC_TIMED(ctx, "k_dec_s2", stream, k_dec_s2<<<P.n_seg + P.n_sub, kBlock, kStage2Smem, stream>>>(P, a));
+  if (P.n_vt + P.n_sub)
+    EMBC_TIMED(ctx, "k_dec_s3", stream, k_dec_s3<<<P.n_vt + P.n_sub, kBlock, 0, stream>>>(P, a));
+  EMBC_TIMED(ctx, "k_dec_s4", stream, k_dec_s4<<<n, 32, 0, stream>>>(P, a));
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "decode launch");
   return EMBC_OK;

@@ -17,7 +17,8 @@ constexpr uint32_t kHeader = 30;      // CompressedChunk::kHeaderSize (container
 constexpr uint32_t kMetaSize = 25;    // ChunkMetadata::kWireSize (container.hpp:193)
 constexpr uint32_t kMaxWindow = 65536;  // VlzConfig::kMaxWindow (vlz.hpp:45)
 constexpr uint32_t kHistCap = 1u << 17;   // GPU Huffman alphabet span limit (EMBC_R_RANGE)
-constexpr uint32_t kSmemHist = 16384;     // span histogrammed in shared memory
+constexpr uint32_t kWin = 4096;           // K1 speculative histogram window, codes [-2048, 2048)
+constexpr uint32_t kWidePool = 4 * kHistCap;  // histogram entries for wider alphabets per call
 
 // ---------------------------------------------------------------------------
 // Device error record.  Each job keeps a 64-bit key (index << 6 | reason); the

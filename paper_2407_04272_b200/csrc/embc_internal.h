@@ -46,7 +46,9 @@ struct JobState {
   uint32_t nsym;           // huffman distinct symbols
   uint32_t flags;
   uint64_t aux;            // reason payload (e.g. huffman depth)
-  uint64_t hist_off;       // huffman: histogram / LUT region in the pool (k_huff_alloc)
+  uint64_t lut_off;        // huffman: LUT entry of code cmin
+  uint32_t wide;           // huffman: a code fell outside the speculative histogram window
+  uint32_t tiles_done;     // emit: tiles of this job finished (last one merges edge bytes)
 };
 
 enum : uint32_t { JF_ABORT = 1u };
@@ -91,6 +93,7 @@ struct embc_ctx {
   embc_error last{};
   // device memory
   embc_dev::DevError* d_err = nullptr;   // sticky error record (device)
+  uint32_t* d_diag = nullptr;            // diagnostics of the last call (device)
   embc_dev::DevError* h_err = nullptr;   // pinned mirror
   uint8_t* d_scratch = nullptr;
   size_t scratch_cap = 0;

@@ -58,8 +58,13 @@ __global__ void __launch_bounds__(kBlock) k_quant_stats(const DJob* __restrict__
                                                         const DTile* __restrict__ tiles,
                                                         JobState* __restrict__ st,
                                                         uint64_t* __restrict__ row_hash,
-                                                        uint32_t* __restrict__ row_lit) {
+                                                        uint32_t* __restrict__ row_lit,
+                                                        uint32_t* __restrict__ whist,
+                                                        uint32_t hist_smem_off) {
   extern __shared__ __align__(16) uint8_t smem[];
+  // huffman jobs: speculative histogram over the window [-kWin/2, kWin/2)
+  // (Codebook::build, huffman.hpp:122-128); K2 redoes it for wider alphabets
+  uint32_t* shist = reinterpret_cast<uint32_t*>(smem + hist_smem_off);
   __shared__ unsigned long long s_err;
   __shared__ int s_min, s_max;
   const DTile T = tiles[blockIdx.x];
@@ -74,7 +79,10 @@ __global__ void __launch_bounds__(kBlock) k_quant_stats(const DJob* __restrict__
     s_min = INT_MAX;
     s_max = INT_MIN;
   }
+  if (huf)
+    for (uint32_t b = threadIdx.x; b < kWin; b += blockDim.x) shist[b] = 0;
   __syncthreads();
+  bool lwide = false;
 
   const uint64_t e0 = static_cast<uint64_t>(T.row0) * dim;
   const uint32_t ne = T.rows * dim;
@@ -89,6 +97,11 @@ __global__ void __launch_bounds__(kBlock) k_quant_stats(const DJob* __restrict__
       if (reason) lerr = min(lerr, static_cast<unsigned long long>(err_key(e0 + l, reason)));
       lmin = min(lmin, c);
       lmax = max(lmax, c);
+      if (huf) {
+        const uint32_t b = static_cast<uint32_t>(c + static_cast<int32_t>(kWin / 2));
+        if (b < kWin) atomicAdd(&shist[b], 1u);
+        else lwide = true;
+      }
       if (vlz) {
         const uint32_t r = fdiv(l, J.fd);
         codes[r * stride + (l - r * dim)] = c;
@@ -100,6 +113,11 @@ __global__ void __launch_bounds__(kBlock) k_quant_stats(const DJob* __restrict__
       const int32_t c = __ldg(x + l);
       lmin = min(lmin, c);
       lmax = max(lmax, c);
+      if (huf) {
+        const uint32_t b = static_cast<uint32_t>(c + static_cast<int32_t>(kWin / 2));
+        if (b < kWin) atomicAdd(&shist[b], 1u);
+        else lwide = true;
+      }
       if (vlz) {
         const uint32_t r = fdiv(l, J.fd);
         codes[r * stride + (l - r * dim)] = c;
@@ -126,6 +144,18 @@ __global__ void __launch_bounds__(kBlock) k_quant_stats(const DJob* __restrict__
       atomicMax(&st[T.job].cmax, s_max);
     }
   }
+  if (huf) {
+    const bool wide = __syncthreads_or(lwide);
+    if (wide) {
+      if (threadIdx.x == 0) st[T.job].wide = 1;
+    } else {
+      uint32_t* gh = whist + static_cast<uint64_t>(J.hjob) * kWin;
+      for (uint32_t b = threadIdx.x; b < kWin; b += blockDim.x) {
+        const uint32_t v = shist[b];
+        if (v) atomicAdd(&gh[b], v);
+      }
+    }
+  }
   if (vlz) {
     // Row hash (any function works: equality is verified exactly in K3) and
     // literal token length 1 + sum varint_len(zigzag(c)) (vlz.hpp:115-118).
@@ -143,74 +173,6 @@ __global__ void __launch_bounds__(kBlock) k_quant_stats(const DJob* __restrict__
       row_hash[g] = h;
       row_lit[g] = lit;
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K1b: dense histogram over [cmin, cmax] (Codebook::build, huffman.hpp:122-128)
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_huff_hist(const DJob* __restrict__ jobs,
-                                                      const DTile* __restrict__ tiles,
-                                                      const uint32_t* __restrict__ tile_list,
-                                                      JobState* __restrict__ st,
-                                                      uint32_t* __restrict__ hist) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* sh = reinterpret_cast<uint32_t*>(smem);
-  const DTile T = tiles[tile_list[blockIdx.x]];
-  const DJob& J = jobs[T.job];
-  const JobState& S = st[T.job];
-  if (S.err != ~0ull) return;  // quantization failed, or no histogram room (K2 reports)
-  const int32_t cmin = S.cmin;
-  const uint64_t span = static_cast<uint64_t>(static_cast<int64_t>(S.cmax) - cmin + 1);
-  uint32_t* gh = hist + S.hist_off;
-  const uint64_t e0 = static_cast<uint64_t>(T.row0) * J.dim;
-  const uint32_t ne = T.rows * J.dim;
-  if (span <= kSmemHist) {
-    for (uint32_t b = threadIdx.x; b < span; b += blockDim.x) sh[b] = 0;
-    __syncthreads();
-    for (uint32_t l = threadIdx.x; l < ne; l += blockDim.x) {
-      uint32_t reason = 0;
-      const int32_t c = job_code(J, e0 + l, &reason);
-      atomicAdd(&sh[c - cmin], 1u);
-    }
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < span; b += blockDim.x) {
-      const uint32_t v = sh[b];
-      if (v) atomicAdd(&gh[b], v);
-    }
-  } else {
-    for (uint32_t l = threadIdx.x; l < ne; l += blockDim.x) {
-      uint32_t reason = 0;
-      const int32_t c = job_code(J, e0 + l, &reason);
-      atomicAdd(&gh[c - cmin], 1u);
-    }
-  }
-}
-
-// Histogram / LUT regions for the huffman jobs of this call, carved from the
-// context's zeroed pool in job order once the code ranges are known.  Empty
-// sequences and spans beyond kHistCap fail here (huffman.hpp:229; EMBC_R_RANGE).
-__global__ void k_huff_alloc(const DJob* __restrict__ jobs, const uint32_t* __restrict__ hjob_list,
-                             uint32_t nh, JobState* __restrict__ st, uint64_t pool) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  uint64_t off = 0;
-  for (uint32_t k = 0; k < nh; ++k) {
-    const uint32_t j = hjob_list[k];
-    JobState& S = st[j];
-    S.hist_off = 0;
-    if (S.err != ~0ull) continue;
-    if (jobs[j].N == 0) {  // huff_encode_codes on an empty sequence (huffman.hpp:229)
-      S.err = err_key(0, EMBC_R_HUF_EMPTY) | (1ull << 63);
-      continue;
-    }
-    const uint64_t span = static_cast<uint64_t>(static_cast<int64_t>(S.cmax) - S.cmin + 1);
-    if (span > kHistCap || off + span > pool) {
-      S.err = err_key(0, EMBC_R_RANGE) | (1ull << 63);
-      S.aux = span;
-      continue;
-    }
-    S.hist_off = off;
-    off += span;
   }
 }
 
@@ -250,27 +212,68 @@ constexpr uint32_t kSmemBook = 2048;  // symbols handled fully in shared memory
 __global__ void __launch_bounds__(kBookThreads) k_huff_book(
     const DJob* __restrict__ jobs, const uint32_t* __restrict__ hjob_list, JobState* __restrict__ st,
     uint32_t* __restrict__ hist, uint64_t* __restrict__ lut, uint8_t* __restrict__ books,
-    uint64_t book_stride, BookScratch gs, uint64_t gs_stride) {
+    uint64_t book_stride, BookScratch gs, uint64_t gs_stride, uint32_t nhuff,
+    unsigned long long* __restrict__ wide_ctr) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_tmp32[33];
   __shared__ unsigned long long s_tmp64[33];
   __shared__ uint32_t s_nsym;
   __shared__ unsigned long long s_cap;
+  __shared__ unsigned long long s_woff;
   const uint32_t jid = hjob_list[blockIdx.x];
   const DJob& J = jobs[jid];
   JobState& S = st[jid];
-  if (S.err != ~0ull) return;
+  const uint32_t hj = static_cast<uint32_t>(J.hjob);
+  uint32_t* narrow = hist + static_cast<uint64_t>(hj) * kWin;
+  if (S.err != ~0ull || J.N == 0) {
+    // quantization failed (or nothing to code): leave the window histogram clean
+    for (uint32_t b = threadIdx.x; b < kWin; b += blockDim.x) narrow[b] = 0;
+    if (J.N == 0 && S.err == ~0ull && threadIdx.x == 0)  // huffman.hpp:229
+      S.err = err_key(0, EMBC_R_HUF_EMPTY) | (1ull << 63);
+    return;
+  }
   const int32_t cmin = S.cmin;
   const uint64_t span = static_cast<uint64_t>(static_cast<int64_t>(S.cmax) - cmin + 1);
-  uint32_t* gh = hist + S.hist_off;
-  const uint32_t hj = static_cast<uint32_t>(J.hjob);
+  uint32_t* gh;
+  if (S.wide) {
+    // alphabet wider than the K1 window: histogram over [cmin, cmax] in the
+    // wide pool (huffman.hpp:122-128), EMBC_R_RANGE beyond kHistCap
+    for (uint32_t b = threadIdx.x; b < kWin; b += blockDim.x) narrow[b] = 0;
+    if (threadIdx.x == 0) {
+      s_woff = ~0ull;
+      if (span <= kHistCap) {
+        const unsigned long long o = atomicAdd(wide_ctr, static_cast<unsigned long long>(span));
+        if (o + span <= kWidePool) s_woff = o;
+      }
+    }
+    __syncthreads();
+    if (s_woff == ~0ull) {
+      if (threadIdx.x == 0) {
+        S.aux = span;
+        S.err = err_key(0, EMBC_R_RANGE) | (1ull << 63);
+      }
+      return;
+    }
+    gh = hist + static_cast<uint64_t>(nhuff) * kWin + s_woff;
+    for (uint64_t e = threadIdx.x; e < J.N; e += blockDim.x) {
+      uint32_t r = 0;
+      atomicAdd(&gh[job_code(J, e, &r) - cmin], 1u);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) S.lut_off = static_cast<uint64_t>(nhuff) * kWin + s_woff;
+  } else {
+    gh = narrow + (cmin + static_cast<int32_t>(kWin / 2));
+    if (threadIdx.x == 0) S.lut_off = static_cast<uint64_t>(hj) * kWin + (cmin + static_cast<int32_t>(kWin / 2));
+  }
+  __syncthreads();
 
   // 1. compact nonzero bins -> symbols in ascending order (sorted histogram, huffman.hpp:51)
   if (threadIdx.x == 0) s_nsym = 0;
   __syncthreads();
   // first pass: count
   uint32_t cnt = 0;
-  for (uint64_t b = threadIdx.x; b < span; b += blockDim.x) cnt += gh[b] != 0;
+  for (uint64_t b = threadIdx.x; b < span; b += blockDim.x) cnt += __ldcg(gh + b) != 0;
   const uint32_t nsym = block_sum<uint32_t>(cnt, s_tmp32);
 
   uint32_t p2 = 1;
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(kBookThreads) k_huff_book(
     uint64_t base = 0;
     for (uint64_t b0 = 0; b0 < span; b0 += blockDim.x) {
       const uint64_t b = b0 + threadIdx.x;
-      const uint32_t c = b < span ? gh[b] : 0;
+      const uint32_t c = b < span ? __ldcg(gh + b) : 0;
       uint32_t tot;
       const uint32_t pos = block_excl_scan<uint32_t>(c != 0, s_tmp32, &tot);
       if (c) key[base + pos] = (static_cast<uint64_t>(c) << 32) | b;
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(kBookThreads) k_huff_book(
   __syncthreads();
 
   uint8_t* book = books + hj * book_stride;
-  uint64_t* L = lut + S.hist_off;
+  uint64_t* L = lut + S.lut_off;
   // 2. leaves sorted by (count, symbol): stable_sort (huffman.hpp:74-77)
   if (nsym > 1) bitonic_sort(key, p2);
 
@@ -427,16 +430,13 @@ __device__ __forceinline__ bool warp_rows_equal(const DJob& J, uint32_t a, uint3
   return __all_sync(0xffffffffu, eq);
 }
 
-__global__ void __launch_bounds__(kBlock) k_sizes(const DJob* __restrict__ jobs,
-                                                  const DTile* __restrict__ tiles,
-                                                  const uint32_t* __restrict__ tile_list,
-                                                  const JobState* __restrict__ st,
-                                                  const uint64_t* __restrict__ row_hash,
-                                                  const uint32_t* __restrict__ row_lit,
-                                                  uint32_t* __restrict__ row_off,
-                                                  const uint64_t* __restrict__ lut,
-                                                  uint64_t* __restrict__ tile_sum) {
-  extern __shared__ __align__(16) uint8_t smem[];
+__device__ __forceinline__ void sizes_tile(const DJob* __restrict__ jobs, const DTile* __restrict__ tiles,
+                                           const uint32_t* __restrict__ tile_list,
+                                           const JobState* __restrict__ st,
+                                           const uint64_t* __restrict__ row_hash,
+                                           const uint32_t* __restrict__ row_lit, uint32_t* __restrict__ row_off,
+                                           const uint64_t* __restrict__ lut, uint64_t* __restrict__ tile_sum,
+                                           uint8_t* smem) {
   __shared__ unsigned long long s_tmp64[33];
   const uint32_t tid = tile_list[blockIdx.x];
   const DTile T = tiles[tid];
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(kBlock) k_sizes(const DJob* __restrict__ jobs,
     }
   } else {  // huffman: bits of every code in the tile
     const int32_t cmin = S.cmin;
-    const uint64_t* L = lut + S.hist_off;
+    const uint64_t* L = lut + S.lut_off;
     const uint64_t e0 = static_cast<uint64_t>(T.row0) * J.dim;
     const uint32_t ne = T.rows * J.dim;
     for (uint32_t l = threadIdx.x; l < ne; l += blockDim.x) {
@@ -559,11 +559,13 @@ struct LayoutArgs {
   uint64_t* d_total;
   uint32_t* call_flags;
   DevError* err;
+  int skip;  // match_stats: no layout
 };
 
-__global__ void __launch_bounds__(1024) k_layout(const DJob* __restrict__ jobs, JobState* st,
-                                                 const uint64_t* __restrict__ tile_sum,
-                                                 uint64_t* __restrict__ tile_off, LayoutArgs a) {
+__device__ void layout_body(const DJob* __restrict__ jobs, JobState* st,
+                            const uint64_t* __restrict__ tile_sum, uint64_t* __restrict__ tile_off,
+                            const LayoutArgs& a) {
+  if (a.skip) return;
   __shared__ unsigned long long s_tmp64[33];
   __shared__ unsigned long long s_first;
   if (threadIdx.x == 0) s_first = ~0ull;
@@ -674,6 +676,33 @@ __global__ void __launch_bounds__(1024) k_layout(const DJob* __restrict__ jobs, 
   }
 }
 
+// K3 kernel: vlz decisions / huffman bit counts per tile; the last CTA to
+// finish lays the call out (one launch instead of two).
+__global__ void __launch_bounds__(kBlock) k_sizes(const DJob* __restrict__ jobs,
+                                                  const DTile* __restrict__ tiles,
+                                                  const uint32_t* __restrict__ tile_list, uint32_t nlist,
+                                                  JobState* __restrict__ st,
+                                                  const uint64_t* __restrict__ row_hash,
+                                                  const uint32_t* __restrict__ row_lit,
+                                                  uint32_t* __restrict__ row_off,
+                                                  const uint64_t* __restrict__ lut,
+                                                  uint64_t* __restrict__ tile_sum,
+                                                  uint64_t* __restrict__ tile_off,
+                                                  uint32_t* __restrict__ done_ctr, LayoutArgs la) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_last;
+  if (blockIdx.x < nlist)
+    sizes_tile(jobs, tiles, tile_list, st, row_hash, row_lit, row_off, lut, tile_sum, smem);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    layout_body(jobs, st, tile_sum, tile_off, la);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K5: byte emission
 // ---------------------------------------------------------------------------
@@ -681,7 +710,7 @@ constexpr uint32_t kStageBytes = 48 * 1024;
 
 __global__ void __launch_bounds__(kBlock) k_emit(const DJob* __restrict__ jobs,
                                                  const DTile* __restrict__ tiles,
-                                                 const JobState* __restrict__ st,
+                                                 JobState* __restrict__ st,
                                                  const uint32_t* __restrict__ row_off,
                                                  const uint32_t* __restrict__ row_lit,
                                                  const uint64_t* __restrict__ tile_off,
@@ -698,7 +727,7 @@ __global__ void __launch_bounds__(kBlock) k_emit(const DJob* __restrict__ jobs,
   const uint32_t tid = blockIdx.x;
   const DTile T = tiles[tid];
   const DJob& J = jobs[T.job];
-  const JobState& S = st[T.job];
+  JobState& S = st[T.job];
   const uint32_t dim = J.dim;
   const uint64_t e0 = static_cast<uint64_t>(T.row0) * dim;
   const uint32_t ne = T.rows * dim;
@@ -799,7 +828,7 @@ __global__ void __launch_bounds__(kBlock) k_emit(const DJob* __restrict__ jobs,
     for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) words[w] = 0;
     __syncthreads();
     const int32_t cmin = S.cmin;
-    const uint64_t* L = lut + S.hist_off;
+    const uint64_t* L = lut + S.lut_off;
     const uint32_t per = (ne + blockDim.x - 1) / blockDim.x;
     const uint32_t l0 = threadIdx.x * per, l1 = min(l0 + per, ne);
     uint32_t nb = 0;
@@ -830,25 +859,21 @@ __global__ void __launch_bounds__(kBlock) k_emit(const DJob* __restrict__ jobs,
       edges[2 * tid + 1] = smem[nbytes_stage - 1];  // last byte (partial if endbit % 8)
     }
     copy_out_staged(dst, smem, nbytes);
+    // the job's last tile to finish merges the bytes shared by adjacent tiles
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&S.tiles_done, 1u) == J.ntiles - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (uint32_t k = 1 + threadIdx.x; k < J.ntiles; k += blockDim.x) {
+        const uint32_t t2 = J.tile0 + k;
+        const uint64_t b = __ldcg(tile_off + t2);
+        if (b & 7) stream[b >> 3] = __ldcg(edges + 2 * (t2 - 1) + 1) | __ldcg(edges + 2 * t2);
+      }
+    }
   }
-}
-
-// K6: bytes straddling two tiles of one job = OR of both partial bytes.
-__global__ void k_huff_edges(const DJob* __restrict__ jobs, const DTile* __restrict__ tiles,
-                             const JobState* __restrict__ st, const uint64_t* __restrict__ tile_off,
-                             const uint8_t* __restrict__ edges, uint8_t* __restrict__ out,
-                             uint32_t ntiles, const uint32_t* __restrict__ call_flags) {
-  if (*call_flags & JF_ABORT) return;
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= ntiles) return;
-  const DTile T = tiles[t];
-  const DJob& J = jobs[T.job];
-  if (J.codec != EMBC_CODEC_HUFFMAN || T.row0 == 0) return;
-  const uint64_t bit0 = tile_off[t];
-  if ((bit0 & 7) == 0) return;
-  const JobState& S = st[T.job];
-  uint8_t* stream = out + S.chunk_off + J.header + 12 + 5ull * S.nsym;
-  stream[bit0 >> 3] = edges[2 * (t - 1) + 1] | edges[2 * t];
 }
 
 __global__ void k_count_refs(const uint32_t* __restrict__ row_off, uint32_t n,
@@ -1011,7 +1036,7 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
     if (in.codec == EMBC_CODEC_HUFFMAN) {
       J.hjob = static_cast<int32_t>(nhuff++);
       J.hist_cap = std::min<uint64_t>(std::max<uint64_t>(J.N, 1), kHistCap);  // bound on distinct symbols
-      hist_entries += std::min<uint64_t>(kHistCap, std::max<uint64_t>(J.N, 1) * 4 + 1024);
+      hist_entries += kWin;
     }
     J.tile_rows = pick_tile_rows(in.dim, total_values);
     J.tile0 = static_cast<uint32_t>(tiles.size());
@@ -1058,7 +1083,7 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   const size_t o_tsum = cv.take<uint64_t>(ntiles + 1);
   const size_t o_toff = cv.take<uint64_t>(ntiles + 1);
   const size_t o_edges = cv.take<uint8_t>(2ull * ntiles + 2);
-  hist_entries = std::max<uint64_t>(hist_entries, kHistCap);
+  hist_entries += kWidePool;  // [nhuff windows | wide pool], LUT mirrors the layout
   const size_t o_lut = cv.take<uint64_t>(hist_entries + 1);
   const size_t o_books = cv.take<uint8_t>(book_stride * std::max<uint32_t>(nhuff, 1));
   size_t o_gkey = 0, o_gwgt = 0, o_gpar = 0;
@@ -1120,17 +1145,11 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
     for (uint32_t j = 0; j < njobs; ++j) m = std::max(m, jobs[j].tile_rows * (jobs[j].dim | 1u));
     return m;
   }();
+  const uint32_t hist_smem_off = static_cast<uint32_t>(align_up(sizeof(int32_t) * max_rows_stride, 16));
   if (ntiles) {
-    EMBC_TIMED(ctx, "k_quant_stats", stream, k_quant_stats<<<ntiles, kBlock, sizeof(int32_t) * max_rows_stride, stream>>>(d_jobs, d_tiles, d_st,
-                                                                               d_hash, d_lit));
-  }
-  if (!list_hjobs.empty()) {
-    EMBC_TIMED(ctx, "k_huff_alloc", stream, k_huff_alloc<<<1, 32, 0, stream>>>(d_jobs, reinterpret_cast<const uint32_t*>(d + o_l3),
-                                       static_cast<uint32_t>(list_hjobs.size()), d_st, hist_entries));
-  }
-  if (!list_huff_tiles.empty()) {
-    EMBC_TIMED(ctx, "k_huff_hist", stream, k_huff_hist<<<static_cast<uint32_t>(list_huff_tiles.size()), kBlock, sizeof(uint32_t) * kSmemHist, stream>>>(
-        d_jobs, d_tiles, reinterpret_cast<const uint32_t*>(d + o_l2), d_st, d_hist));
+    EMBC_TIMED(ctx, "k_quant_stats", stream,
+               k_quant_stats<<<ntiles, kBlock, hist_smem_off + (nhuff ? sizeof(uint32_t) * kWin : 0), stream>>>(
+                   d_jobs, d_tiles, d_st, d_hash, d_lit, d_hist, hist_smem_off));
   }
   if (!list_hjobs.empty()) {
     BookScratch gs{};
@@ -1140,20 +1159,10 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
       gs.parent = reinterpret_cast<int32_t*>(d + o_gpar);
     }
     const size_t sm = kSmemBook * (8 + 16 + 8);
-    EMBC_TIMED(ctx, "k_huff_book", stream, k_huff_book<<<static_cast<uint32_t>(list_hjobs.size()), kBookThreads, sm, stream>>>(
-        d_jobs, reinterpret_cast<const uint32_t*>(d + o_l3), d_st, d_hist, d_lut, d_books,
-        book_stride, gs, p2cap));
-  }
-  if (!list_nonraw.empty()) {
-    EMBC_TIMED(ctx, "k_sizes", stream, k_sizes<<<static_cast<uint32_t>(list_nonraw.size()), kBlock, sizeof(uint64_t) * kHashStage, stream>>>(
-        d_jobs, d_tiles, reinterpret_cast<const uint32_t*>(d + o_l1), d_st, d_hash, d_lit, d_off,
-        d_lut, d_tsum));
-  }
-  if (d_stats) {  // match_stats: count literal vs reference rows of job 0
-    k_count_refs<<<(static_cast<uint32_t>(total_rows) + 255) / 256, 256, 0, stream>>>(
-        d_off, static_cast<uint32_t>(total_rows), d_stats);
-    ce = cudaGetLastError();
-    return ce == cudaSuccess ? EMBC_OK : cuda_fail(ctx, ce, "match_stats launch");
+    EMBC_TIMED(ctx, "k_huff_book", stream,
+               k_huff_book<<<static_cast<uint32_t>(list_hjobs.size()), kBookThreads, sm, stream>>>(
+                   d_jobs, reinterpret_cast<const uint32_t*>(d + o_l3), d_st, d_hist, d_lut, d_books,
+                   book_stride, gs, p2cap, nhuff, reinterpret_cast<unsigned long long*>(d_flags + 2)));
   }
   LayoutArgs la{};
   la.njobs = njobs;
@@ -1166,15 +1175,25 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   la.d_total = d_total;
   la.call_flags = d_flags;
   la.err = ctx->d_err;
-  EMBC_TIMED(ctx, "k_layout", stream, k_layout<<<1, 1024, 0, stream>>>(d_jobs, d_st, d_tsum, d_toff, la));
+  la.skip = d_stats ? 1 : 0;
+  {
+    const uint32_t nl = static_cast<uint32_t>(list_nonraw.size());
+    EMBC_TIMED(ctx, "k_sizes", stream,
+               k_sizes<<<nl + 1, kBlock, sizeof(uint64_t) * kHashStage, stream>>>(
+                   d_jobs, d_tiles, reinterpret_cast<const uint32_t*>(d + o_l1), nl, d_st, d_hash, d_lit, d_off,
+                   d_lut, d_tsum, d_toff, d_flags + 1, la));
+  }
+  if (d_stats) {  // match_stats: count literal vs reference rows of job 0
+    k_count_refs<<<(static_cast<uint32_t>(total_rows) + 255) / 256, 256, 0, stream>>>(
+        d_off, static_cast<uint32_t>(total_rows), d_stats);
+    ce = cudaGetLastError();
+    return ce == cudaSuccess ? EMBC_OK : cuda_fail(ctx, ce, "match_stats launch");
+  }
   if (ntiles) {
-    EMBC_TIMED(ctx, "k_emit", stream, k_emit<<<ntiles, kBlock, kStageBytes + 36 * 1024, stream>>>(d_jobs, d_tiles, d_st, d_off, d_lit,
-                                                              d_toff, d_tsum, d_lut, d_books,
-                                                              book_stride, d_out, d_edges, d_flags));
-    if (nhuff) {
-      EMBC_TIMED(ctx, "k_huff_edges", stream, k_huff_edges<<<(ntiles + 255) / 256, 256, 0, stream>>>(d_jobs, d_tiles, d_st, d_toff, d_edges,
-                                                             d_out, ntiles, d_flags));
-    }
+    EMBC_TIMED(ctx, "k_emit", stream,
+               k_emit<<<ntiles, kBlock, kStageBytes + 36 * 1024, stream>>>(
+                   d_jobs, d_tiles, d_st, d_off, d_lit, d_toff, d_tsum, d_lut, d_books, book_stride, d_out,
+                   d_edges, d_flags));
   }
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "encode launch");
@@ -1185,14 +1204,11 @@ cudaError_t encode_set_attributes() {
   cudaError_t e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kStageBytes + 36 * 1024);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_huff_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           sizeof(uint32_t) * kSmemHist);
-  if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_huff_book, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kSmemBook * (8 + 16 + 8));
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_quant_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           sizeof(int32_t) * 16384 * 2);
+                           sizeof(int32_t) * 16384 * 2 + sizeof(uint32_t) * kWin);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_sizes, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               sizeof(uint64_t) * kHashStage);

@@ -120,6 +120,7 @@ def test_workload_digests(ctx, golden):
             b = K.encode_chunk(xd, w["eb"], codec, win)
             assert len(b) == c["len"] and sha(b) == c["sha"], (w["name"], key)
             d64 = K.decode_chunk(b, K.OUT_F64).cpu().numpy()
+            assert K.decode_fallbacks() == 0, (w["name"], key)  # parallel decoders handled it
             assert sha(d64.tobytes()) == c["dec_sha"], (w["name"], key)
             d32 = K.decode_chunk(b, K.OUT_F32).cpu().numpy()
             assert sha(d32.tobytes()) == c["dec32_sha"], (w["name"], key)
@@ -343,5 +344,19 @@ def test_large_tb_chunk_roundtrip(ctx):
     r2 = K.encode_chunks(jobs, K.LAYOUT_PACKED)
     assert torch.equal(r1.buffer, r2.buffer)
     outs = K.decode_packed(bytes(r1.buffer.cpu().numpy().tobytes()), K.OUT_F64)
+    assert K.decode_fallbacks() == 0
     for j, o in zip(jobs, outs):
         assert (o - j.batch.double()).abs().max().item() <= 0.03
+
+
+def test_long_huffman_codes_parallel_path(ctx, oracle):
+    """Terabyte tables whose Huffman codes exceed the 11-bit prefix LUT (max
+    length 16-17) decode on the parallel path, bit-exactly."""
+    for t, eb in ((12, 0.01), (23, 0.01), (7, 0.01)):
+        spec = W.TableSpec.preset(W.TERABYTE_TABLES, t, 64)
+        x = W.gen_table(spec)[W.lookup_indices(spec, 8192, W.lookup_stream(0, t, 0, 1))]
+        b = K.encode_chunk(dev(x), eb, K.CODEC_HUFFMAN)
+        assert b == oracle.encode_chunk(x.astype(np.float64), 64, eb, 2)
+        d = K.decode_chunk(b, K.OUT_F64).cpu().numpy()
+        assert K.decode_fallbacks() == 0, t
+        assert np.array_equal(d.view(np.uint64), oracle.decode_chunk(b).view(np.uint64))
