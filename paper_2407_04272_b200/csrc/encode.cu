@@ -1,17 +1,22 @@
 // encode.cu -- sm_100a compression pipeline: quantize -> (vlz dedup | huffman
-// | raw) -> chunk container -> packed send buffer, for a batch of jobs in one
-// launch sequence with no host synchronisation (graph-capturable).
+// | raw) -> chunk container -> packed send buffer, for a batch of jobs in TWO
+// launches with no host synchronisation (graph-capturable).
 //
 // Mirrors embc::encode_chunks + embc::pack (container.hpp:119-142, :242-256,
 // :304-311).  Kernels:
-//   K1 k_quant_stats  quantize every tile, first-failure record, per-row
-//                      hash + literal token length (vlz), code range (huffman)
-//   K1b k_huff_hist    dense code histogram over [cmin, cmax]   (huffman.hpp:122-128)
-//   K2 k_huff_book     two-queue Huffman lengths + canonical codes (huffman.hpp:49-120, :165-186)
-//   K3 k_sizes         vlz match decisions (vlz.hpp:86-103) + per-tile output sizes
-//   K4 k_layout        chunk offsets (scan, job order), headers, pack table, metadata
-//   K5 k_emit          raw / vlz token / huffman bitstream bytes
-//   K6 k_huff_edges    OR together the bitstream bytes shared by adjacent tiles
+//   E1 k_stats   one CTA per tile: 128-bit loads, quantize (quantizer.hpp:43-76),
+//                first-failure key, code range + warp-aggregated histogram
+//                (huffman jobs, Codebook::build huffman.hpp:122-128), per-row
+//                hash + literal token length (vlz jobs, vlz.hpp:115-118).  The
+//                last tile of a huffman job to finish builds its canonical
+//                codebook (huffman.hpp:49-120, :165-186) in the same launch.
+//   E2 k_emit    one CTA per tile, tiles taken in order from an atomic ticket:
+//                vlz match decisions (vlz.hpp:86-103) / huffman bit counts /
+//                raw sizes, then a decoupled look-back over tiles (offsets
+//                inside a chunk) and over jobs (chunk offsets in job order,
+//                container.hpp:245-250), then the bytes: tokens / MSB-first
+//                bitstream (bitstream.hpp:32-51) / u32le codes, chunk headers,
+//                pack table and 25-B metadata written by each job's last tile.
 #include <cuda_runtime.h>
 #include <limits.h>
 #include <stdint.h>
@@ -25,8 +30,40 @@
 
 namespace embc_dev {
 
+constexpr uint32_t kTileVals = 4096;     // values per tile (whole rows): 3 CTAs of E2 per SM
+constexpr uint32_t kMaxRowVals = 8192;   // a single row (dim) may exceed kTileVals up to this
+constexpr uint32_t kMaxTileRows = 1024;  // rows per tile (bounds the per-row smem arrays)
+constexpr uint32_t kHashStage = 2048;    // vlz: row hashes of [row0 - W, row0 + rows) staged in smem
+constexpr uint32_t kLutStage = 2048;     // huffman: codebook LUT entries staged in smem
+constexpr uint32_t kSmemBook = 1024;     // codebook symbols sorted fully in shared memory
+
+// E2 dynamic shared memory carve (bytes) for tiles of <= vals values / rows rows:
+//   [codes: padded, rows*(dim|1) or l + l/32][stage: output bytes][aux: hashes + dec/lit | LUT]
+__host__ __device__ constexpr uint32_t emit_codes_bytes(uint32_t vals, uint32_t rows) {
+  return ((vals + rows + 64) * 4 + 15) & ~15u;
+}
+__host__ __device__ constexpr uint32_t emit_stage_bytes(uint32_t vals, uint32_t rows) {
+  return (rows + 5 * vals + 128 + 15) & ~15u;
+}
+constexpr uint32_t kAuxBytes = kHashStage * 4 + kMaxTileRows * 20;  // hashes | dec, lits, cand, plist, miss
+constexpr uint32_t kEmitSmemMax = emit_codes_bytes(kMaxRowVals, kMaxTileRows) +
+                                  emit_stage_bytes(kMaxRowVals, kMaxTileRows) + kAuxBytes;
+// E1: codes staged for the generic (scalar) path + histogram window; the
+// codebook tail reuses the same bytes (>= kSmemBook * 32)
+__host__ __device__ constexpr uint32_t stats_codes_bytes(uint32_t vals, uint32_t rows) {
+  return (vals + rows) * 4 > 16384 ? ((vals + rows) * 4 + 15) & ~15u : 16384u;
+}
+constexpr uint32_t kStatsSmemMax = stats_codes_bytes(kMaxRowVals, kMaxTileRows) + kWin * 4;
+
+// look-back status words: flag in bits 63:62, value in 61:0
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+constexpr uint32_t kJobStride = 16;  // job status words one 128-B line apart (polled by many CTAs)
+
+// call-level flags (device): [0] abort bits, [1] E2 tile ticket, [2..3] wide-pool cursor (u64)
+enum : uint32_t { CF_ABORT = 0, CF_TICKET = 1, CF_WIDE = 2 };
+
 // ---------------------------------------------------------------------------
-// element access
+// element access (int32 code sources for the codec-stage entry points)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int32_t job_code(const DJob& J, uint64_t e, uint32_t* reason) {
   if (J.src_kind == EMBC_SRC_F32) {
@@ -36,151 +73,41 @@ __device__ __forceinline__ int32_t job_code(const DJob& J, uint64_t e, uint32_t*
   return __ldg(static_cast<const int32_t*>(J.src) + e);
 }
 
-__device__ __forceinline__ void atomic_min_u64(unsigned long long* p, unsigned long long v) {
-  if (v != ~0ull) atomicMin(p, v);
+// Row hash: a sum of per-element mixes, so partial sums combine in any order
+// (warp shuffles); equality is verified exactly (CodeRowEq, vlz.hpp:75-79),
+// so only the hit rate depends on the function.
+__device__ __forceinline__ uint32_t elem_mix(int32_t c, uint32_t col) {
+  uint32_t x = static_cast<uint32_t>(c) * 0x9E3779B1u ^ (col * 0x85EBCA77u + 0x165667B1u);
+  x ^= x >> 16;
+  x *= 0x7FEB352Du;
+  x ^= x >> 15;
+  x *= 0x846CA68Bu;
+  x ^= x >> 16;
+  return x;
 }
 
-// Block min-reduction of a failure key into the job state.
-__device__ __forceinline__ void publish_err(unsigned long long* dst, unsigned long long v,
-                                            unsigned long long* s_tmp) {
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    unsigned long long n = __shfl_xor_sync(0xffffffffu, v, o);
+    const unsigned long long n = __shfl_xor_sync(0xffffffffu, v, o);
     v = n < v ? n : v;
   }
-  if ((threadIdx.x & 31) == 0 && v != ~0ull) atomicMin(s_tmp, v);
+  return v;
 }
 
-// ---------------------------------------------------------------------------
-// K1: quantize + per-row statistics
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_quant_stats(const DJob* __restrict__ jobs,
-                                                        const DTile* __restrict__ tiles,
-                                                        JobState* __restrict__ st,
-                                                        uint64_t* __restrict__ row_hash,
-                                                        uint32_t* __restrict__ row_lit,
-                                                        uint32_t* __restrict__ whist,
-                                                        uint32_t hist_smem_off) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  // huffman jobs: speculative histogram over the window [-kWin/2, kWin/2)
-  // (Codebook::build, huffman.hpp:122-128); K2 redoes it for wider alphabets
-  uint32_t* shist = reinterpret_cast<uint32_t*>(smem + hist_smem_off);
-  __shared__ unsigned long long s_err;
-  __shared__ int s_min, s_max;
-  const DTile T = tiles[blockIdx.x];
-  const DJob& J = jobs[T.job];
-  const uint32_t dim = J.dim;
-  const uint32_t stride = dim | 1u;
-  const bool vlz = J.codec == EMBC_CODEC_VLZ;
-  const bool huf = J.codec == EMBC_CODEC_HUFFMAN;
-  int32_t* codes = reinterpret_cast<int32_t*>(smem);
-  if (threadIdx.x == 0) {
-    s_err = ~0ull;
-    s_min = INT_MAX;
-    s_max = INT_MIN;
-  }
-  if (huf)
-    for (uint32_t b = threadIdx.x; b < kWin; b += blockDim.x) shist[b] = 0;
-  __syncthreads();
-  bool lwide = false;
-
-  const uint64_t e0 = static_cast<uint64_t>(T.row0) * dim;
-  const uint32_t ne = T.rows * dim;
-  unsigned long long lerr = ~0ull;
-  int lmin = INT_MAX, lmax = INT_MIN;
-  if (J.src_kind == EMBC_SRC_F32) {
-    const float* x = static_cast<const float*>(J.src) + e0;
-    const QParams qp = J.qp;
-    for (uint32_t l = threadIdx.x; l < ne; l += blockDim.x) {
-      uint32_t reason = 0;
-      const int32_t c = quantize_f32(__ldg(x + l), qp, &reason);
-      if (reason) lerr = min(lerr, static_cast<unsigned long long>(err_key(e0 + l, reason)));
-      lmin = min(lmin, c);
-      lmax = max(lmax, c);
-      if (huf) {
-        const uint32_t b = static_cast<uint32_t>(c + static_cast<int32_t>(kWin / 2));
-        if (b < kWin) atomicAdd(&shist[b], 1u);
-        else lwide = true;
-      }
-      if (vlz) {
-        const uint32_t r = fdiv(l, J.fd);
-        codes[r * stride + (l - r * dim)] = c;
-      }
-    }
-  } else {
-    const int32_t* x = static_cast<const int32_t*>(J.src) + e0;
-    for (uint32_t l = threadIdx.x; l < ne; l += blockDim.x) {
-      const int32_t c = __ldg(x + l);
-      lmin = min(lmin, c);
-      lmax = max(lmax, c);
-      if (huf) {
-        const uint32_t b = static_cast<uint32_t>(c + static_cast<int32_t>(kWin / 2));
-        if (b < kWin) atomicAdd(&shist[b], 1u);
-        else lwide = true;
-      }
-      if (vlz) {
-        const uint32_t r = fdiv(l, J.fd);
-        codes[r * stride + (l - r * dim)] = c;
-      }
-    }
-  }
-  publish_err(&st[T.job].err, lerr, &s_err);
-  if (huf) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
-      lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-      atomicMin(&s_min, lmin);
-      atomicMax(&s_max, lmax);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (s_err != ~0ull) atomicMin(&st[T.job].err, s_err);
-    if (huf) {
-      atomicMin(&st[T.job].cmin, s_min);
-      atomicMax(&st[T.job].cmax, s_max);
-    }
-  }
-  if (huf) {
-    const bool wide = __syncthreads_or(lwide);
-    if (wide) {
-      if (threadIdx.x == 0) st[T.job].wide = 1;
-    } else {
-      uint32_t* gh = whist + static_cast<uint64_t>(J.hjob) * kWin;
-      for (uint32_t b = threadIdx.x; b < kWin; b += blockDim.x) {
-        const uint32_t v = shist[b];
-        if (v) atomicAdd(&gh[b], v);
-      }
-    }
-  }
-  if (vlz) {
-    // Row hash (any function works: equality is verified exactly in K3) and
-    // literal token length 1 + sum varint_len(zigzag(c)) (vlz.hpp:115-118).
-    for (uint32_t r = threadIdx.x; r < T.rows; r += blockDim.x) {
-      const int32_t* row = codes + r * stride;
-      uint64_t h = 0xCBF29CE484222325ull;
-      uint32_t lit = 1;
-      for (uint32_t j = 0; j < dim; ++j) {
-        const int32_t c = row[j];
-        lit += varint_len(zigzag(c));
-        h = (h ^ static_cast<uint32_t>(c)) * 0x100000001B3ull;
-      }
-      h ^= h >> 29;
-      const uint64_t g = J.row_base + T.row0 + r;
-      row_hash[g] = h;
-      row_lit[g] = lit;
-    }
-  }
+// warp-aggregated histogram increment: lanes with equal bins add once
+__device__ __forceinline__ void hist_add(uint32_t* shist, uint32_t bin) {
+  const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+  const uint32_t lane = threadIdx.x & 31;
+  if (bin != 0xFFFFFFFFu && (__ffs(peers) - 1) == static_cast<int>(lane)) atomicAdd(&shist[bin], __popc(peers));
 }
 
+__device__ __forceinline__ uint32_t ld_u32_cg(const void* p) { return __ldcg(static_cast<const unsigned int*>(p)); }
+
 // ---------------------------------------------------------------------------
-// K2: canonical Huffman codebook per job (one CTA).
+// Canonical Huffman codebook of one job (run by the job's last E1 tile).
 // ---------------------------------------------------------------------------
-// In-place ascending bitonic sort of n keys (n padded to a power of two with
-// ~0 sentinels by the caller); generic pointer: shared or global memory.
+// In-place ascending bitonic sort of p2 keys (shared or global memory).
 __device__ void bitonic_sort(uint64_t* key, uint32_t p2) {
   for (uint32_t k = 2; k <= p2; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
@@ -206,86 +133,91 @@ struct BookScratch {
   int32_t* parent;  // 2 * cap
 };
 
-constexpr uint32_t kBookThreads = 1024;
-constexpr uint32_t kSmemBook = 2048;  // symbols handled fully in shared memory
+struct BookArgs {
+  uint32_t* hist;       // [nhuff windows | wide pool]
+  uint64_t* lut;        // mirrors hist: (codeword << 8 | length) per code
+  uint8_t* books;       // serialized codebooks (write_codebook, huffman.hpp:202-209)
+  uint64_t book_stride;
+  BookScratch gs;       // global sort scratch for alphabets > kSmemBook
+  uint64_t gs_stride;
+  uint32_t nhuff;
+  uint32_t* flags;      // call flags
+};
 
-__global__ void __launch_bounds__(kBookThreads) k_huff_book(
-    const DJob* __restrict__ jobs, const uint32_t* __restrict__ hjob_list, JobState* __restrict__ st,
-    uint32_t* __restrict__ hist, uint64_t* __restrict__ lut, uint8_t* __restrict__ books,
-    uint64_t book_stride, BookScratch gs, uint64_t gs_stride, uint32_t nhuff,
-    unsigned long long* __restrict__ wide_ctr) {
-  extern __shared__ __align__(16) uint8_t smem[];
+__device__ void build_book(const DJob& J, JobState* Sp, const BookArgs& a, uint8_t* smem) {
   __shared__ uint32_t s_tmp32[33];
   __shared__ unsigned long long s_tmp64[33];
-  __shared__ uint32_t s_nsym;
   __shared__ unsigned long long s_cap;
   __shared__ unsigned long long s_woff;
-  const uint32_t jid = hjob_list[blockIdx.x];
-  const DJob& J = jobs[jid];
-  JobState& S = st[jid];
+  __shared__ int s_cmin, s_cmax, s_wide;
+  __shared__ unsigned long long s_err;
   const uint32_t hj = static_cast<uint32_t>(J.hjob);
-  uint32_t* narrow = hist + static_cast<uint64_t>(hj) * kWin;
-  if (S.err != ~0ull || J.N == 0) {
+  uint32_t* narrow = a.hist + static_cast<uint64_t>(hj) * kWin;
+  if (threadIdx.x == 0) {  // state written by other CTAs' atomics: read through L2
+    s_err = __ldcg(reinterpret_cast<const unsigned long long*>(&Sp->err));
+    s_cmin = static_cast<int>(ld_u32_cg(&Sp->cmin));
+    s_cmax = static_cast<int>(ld_u32_cg(&Sp->cmax));
+    s_wide = static_cast<int>(ld_u32_cg(&Sp->wide));
+  }
+  __syncthreads();
+  if (s_err != ~0ull || J.N == 0) {
     // quantization failed (or nothing to code): leave the window histogram clean
     for (uint32_t b = threadIdx.x; b < kWin; b += blockDim.x) narrow[b] = 0;
-    if (J.N == 0 && S.err == ~0ull && threadIdx.x == 0)  // huffman.hpp:229
-      S.err = err_key(0, EMBC_R_HUF_EMPTY) | (1ull << 63);
+    if (J.N == 0 && s_err == ~0ull && threadIdx.x == 0) {  // huffman.hpp:229
+      Sp->err = err_key(0, EMBC_R_HUF_EMPTY) | (1ull << 63);
+      atomicOr(&a.flags[CF_ABORT], JF_ABORT);
+    }
     return;
   }
-  const int32_t cmin = S.cmin;
-  const uint64_t span = static_cast<uint64_t>(static_cast<int64_t>(S.cmax) - cmin + 1);
+  const int32_t cmin = s_cmin;
+  const uint64_t span = static_cast<uint64_t>(static_cast<int64_t>(s_cmax) - cmin + 1);
   uint32_t* gh;
-  if (S.wide) {
-    // alphabet wider than the K1 window: histogram over [cmin, cmax] in the
+  uint64_t lut_off;
+  if (s_wide) {
+    // alphabet wider than the E1 window: histogram over [cmin, cmax] in the
     // wide pool (huffman.hpp:122-128), EMBC_R_RANGE beyond kHistCap
     for (uint32_t b = threadIdx.x; b < kWin; b += blockDim.x) narrow[b] = 0;
     if (threadIdx.x == 0) {
       s_woff = ~0ull;
       if (span <= kHistCap) {
-        const unsigned long long o = atomicAdd(wide_ctr, static_cast<unsigned long long>(span));
+        const unsigned long long o =
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.flags + CF_WIDE), static_cast<unsigned long long>(span));
         if (o + span <= kWidePool) s_woff = o;
       }
     }
     __syncthreads();
     if (s_woff == ~0ull) {
       if (threadIdx.x == 0) {
-        S.aux = span;
-        S.err = err_key(0, EMBC_R_RANGE) | (1ull << 63);
+        Sp->aux = span;
+        Sp->err = err_key(0, EMBC_R_RANGE) | (1ull << 63);
+        atomicOr(&a.flags[CF_ABORT], JF_ABORT);
       }
       return;
     }
-    gh = hist + static_cast<uint64_t>(nhuff) * kWin + s_woff;
+    gh = a.hist + static_cast<uint64_t>(a.nhuff) * kWin + s_woff;
     for (uint64_t e = threadIdx.x; e < J.N; e += blockDim.x) {
       uint32_t r = 0;
       atomicAdd(&gh[job_code(J, e, &r) - cmin], 1u);
     }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) S.lut_off = static_cast<uint64_t>(nhuff) * kWin + s_woff;
+    lut_off = static_cast<uint64_t>(a.nhuff) * kWin + s_woff;
   } else {
     gh = narrow + (cmin + static_cast<int32_t>(kWin / 2));
-    if (threadIdx.x == 0) S.lut_off = static_cast<uint64_t>(hj) * kWin + (cmin + static_cast<int32_t>(kWin / 2));
+    lut_off = static_cast<uint64_t>(hj) * kWin + (cmin + static_cast<int32_t>(kWin / 2));
   }
-  __syncthreads();
 
-  // 1. compact nonzero bins -> symbols in ascending order (sorted histogram, huffman.hpp:51)
-  if (threadIdx.x == 0) s_nsym = 0;
-  __syncthreads();
-  // first pass: count
+  // 1. nonzero bins -> symbols in ascending order (sorted histogram, huffman.hpp:51)
   uint32_t cnt = 0;
   for (uint64_t b = threadIdx.x; b < span; b += blockDim.x) cnt += __ldcg(gh + b) != 0;
   const uint32_t nsym = block_sum<uint32_t>(cnt, s_tmp32);
-
   uint32_t p2 = 1;
   while (p2 < nsym) p2 <<= 1;
   const bool in_smem = p2 <= kSmemBook;
-  uint64_t* key = in_smem ? reinterpret_cast<uint64_t*>(smem) : gs.key + hj * gs_stride;
-  uint64_t* wgt = in_smem ? key + kSmemBook : gs.wgt + hj * 2 * gs_stride;
-  int32_t* parent = in_smem ? reinterpret_cast<int32_t*>(wgt + 2 * kSmemBook)
-                            : gs.parent + hj * 2 * gs_stride;
-
-  // second pass: scatter (count << 32 | sym - cmin) keys in symbol order
-  {
+  uint64_t* key = in_smem ? reinterpret_cast<uint64_t*>(smem) : a.gs.key + hj * a.gs_stride;
+  uint64_t* wgt = in_smem ? key + kSmemBook : a.gs.wgt + hj * 2 * a.gs_stride;
+  int32_t* parent = in_smem ? reinterpret_cast<int32_t*>(wgt + 2 * kSmemBook) : a.gs.parent + hj * 2 * a.gs_stride;
+  {  // (count << 32 | sym - cmin) keys in symbol order
     uint64_t base = 0;
     for (uint64_t b0 = 0; b0 < span; b0 += blockDim.x) {
       const uint64_t b = b0 + threadIdx.x;
@@ -298,12 +230,10 @@ __global__ void __launch_bounds__(kBookThreads) k_huff_book(
   }
   for (uint32_t i = nsym + threadIdx.x; i < p2; i += blockDim.x) key[i] = ~0ull;
   __syncthreads();
-
-  uint8_t* book = books + hj * book_stride;
-  uint64_t* L = lut + S.lut_off;
+  uint8_t* book = a.books + hj * a.book_stride;
+  uint64_t* L = a.lut + lut_off;
   // 2. leaves sorted by (count, symbol): stable_sort (huffman.hpp:74-77)
   if (nsym > 1) bitonic_sort(key, p2);
-
   // 3. two-queue merge, leaf queue preferred on ties (huffman.hpp:91-109)
   if (nsym > 1 && threadIdx.x == 0) {
     const uint32_t n = nsym, total = 2 * n - 1;
@@ -312,7 +242,7 @@ __global__ void __launch_bounds__(kBookThreads) k_huff_book(
       parent[i] = -1;
     }
     uint32_t size = n, lh = 0, mh = n;
-    uint64_t wl = wgt[0];  // weight at the leaf head
+    uint64_t wl = wgt[0];
     while (size < total) {
       uint32_t ab[2];
 #pragma unroll
@@ -335,39 +265,34 @@ __global__ void __launch_bounds__(kBookThreads) k_huff_book(
   }
   if (threadIdx.x == 0) s_cap = ~0ull;
   __syncthreads();
-
-  // 4. code lengths = leaf depth; first leaf (sorted order) past 32 bits fails
-  //    with its depth (huffman.hpp:110-118)
+  // 4. code lengths = leaf depth; the first leaf (sorted order) past 32 bits
+  //    fails with its depth (huffman.hpp:110-118)
   for (uint32_t i = threadIdx.x; i < nsym; i += blockDim.x) {
     uint32_t depth = 0;
-    if (nsym == 1) {
-      depth = 1;
-    } else {
+    if (nsym == 1) depth = 1;
+    else
       for (int32_t p = parent[i]; p != -1; p = parent[p]) ++depth;
-    }
     if (depth > 32) atomicMin(&s_cap, (static_cast<unsigned long long>(i) << 32) | depth);
-    // canonical sort key: (length, symbol) (huffman.hpp:166-168)
-    const uint64_t sym = key[i] & 0xFFFFFFFFull;
+    const uint64_t sym = key[i] & 0xFFFFFFFFull;  // canonical key (length, symbol) (huffman.hpp:166-168)
     wgt[i] = (static_cast<uint64_t>(depth > 32 ? 63 : depth) << 32) | sym;
   }
   __syncthreads();
   if (s_cap != ~0ull) {
     if (threadIdx.x == 0) {
-      S.aux = s_cap & 0xFFFFFFFFull;
-      atomicMin(&S.err, err_key(s_cap >> 32, EMBC_R_HUF_LEN_CAP) | (1ull << 63));
+      Sp->aux = s_cap & 0xFFFFFFFFull;
+      atomicMin(reinterpret_cast<unsigned long long*>(&Sp->err), err_key(s_cap >> 32, EMBC_R_HUF_LEN_CAP) | (1ull << 63));
+      atomicOr(&a.flags[CF_ABORT], JF_ABORT);
     }
-    // leave the histogram clean for the next call
     for (uint64_t b = threadIdx.x; b < span; b += blockDim.x) gh[b] = 0;
     return;
   }
   // 5. canonical order (length asc, symbol asc)
-  uint64_t* ckey = wgt;  // reuse
+  uint64_t* ckey = wgt;
   for (uint32_t i = nsym + threadIdx.x; i < p2; i += blockDim.x) ckey[i] = ~0ull;
   __syncthreads();
   if (nsym > 1) bitonic_sort(ckey, p2);
-
-  // 6. canonical code values: code_i = sum_{j<i} 2^(len_i - len_j)  (the closed
-  //    form of finalize's shift-and-increment, huffman.hpp:170-181)
+  // 6. canonical codes: code_i = sum_{j<i} 2^(len_i - len_j), the closed form
+  //    of finalize's shift-and-increment (huffman.hpp:170-181)
   uint64_t bits_local = 0;
   {
     uint64_t carry = 0;
@@ -390,166 +315,239 @@ __global__ void __launch_bounds__(kBookThreads) k_huff_book(
         uint8_t* e = book + 12 + 5ull * i;
         st_be(e, static_cast<uint32_t>(sym), 4);
         e[4] = static_cast<uint8_t>(len);
-        bits_local += static_cast<uint64_t>(gh[symoff]) * len;
+        bits_local += static_cast<uint64_t>(__ldcg(gh + symoff)) * len;
       }
       carry += tot;
     }
   }
   const unsigned long long bits = block_sum<unsigned long long>(bits_local, s_tmp64);
-  // clean histogram for the next call
-  for (uint64_t b = threadIdx.x; b < span; b += blockDim.x) gh[b] = 0;
+  for (uint64_t b = threadIdx.x; b < span; b += blockDim.x) gh[b] = 0;  // clean for the next call
   if (threadIdx.x == 0) {
-    st_be(book, J.N, 8);   // u64be symbol_count (huffman.hpp:203)
+    st_be(book, J.N, 8);       // u64be symbol_count (huffman.hpp:203)
     st_be(book + 8, nsym, 4);  // u32be entry_count (huffman.hpp:204)
-    S.nsym = nsym;
-    S.bits = bits;
-    S.payload = 12 + 5ull * nsym + (bits + 7) / 8;
+    Sp->nsym = nsym;
+    Sp->bits = bits;
+    Sp->lut_off = lut_off;
+    Sp->payload = 12 + 5ull * nsym + (bits + 7) / 8;
   }
 }
 
 // ---------------------------------------------------------------------------
-// K3: vlz match decisions + per-tile output sizes
+// E1: quantize + per-tile statistics (+ codebook tail)
 // ---------------------------------------------------------------------------
-constexpr uint32_t kHashStage = 4096;
+struct StatsArgs {
+  const DJob* jobs;
+  const DTile* tiles;
+  JobState* st;
+  uint64_t* row_info;                 // vlz: (literal token bytes << 32) | row hash
+  unsigned long long* tile_status;    // zeroed here for E2
+  unsigned long long* job_status;
+  uint32_t* edge_slot;
+  BookArgs book;
+  uint32_t hist_off;  // dynamic smem offset of the histogram window
+};
 
-__device__ __forceinline__ uint64_t lut_entry(const uint64_t* L, int32_t c, int32_t cmin) {
-  return __ldg(L + (c - cmin));
-}
-
-// Exact row comparison (the reference's CodeRowEq, vlz.hpp:75-79): one warp
-// compares rows a and b of job J.
-__device__ __forceinline__ bool warp_rows_equal(const DJob& J, uint32_t a, uint32_t b) {
-  const uint32_t lane = threadIdx.x & 31;
-  bool eq = true;
-  for (uint32_t j = lane; j < J.dim; j += 32) {
-    uint32_t r = 0;
-    const int32_t ca = job_code(J, static_cast<uint64_t>(a) * J.dim + j, &r);
-    const int32_t cb = job_code(J, static_cast<uint64_t>(b) * J.dim + j, &r);
-    eq = eq && (ca == cb);
+__global__ void __launch_bounds__(kBlock) k_stats(StatsArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ unsigned long long s_err;
+  __shared__ int s_min, s_max, s_last;
+  const uint32_t tid = blockIdx.x;
+  const DTile T = a.tiles[tid];
+  const DJob& J = a.jobs[T.job];
+  // E2 scratch of this call starts clean
+  if (threadIdx.x == 0) {
+    a.tile_status[tid] = 0;
+    a.edge_slot[tid] = 0;
+    if (tid == J.tile0) a.job_status[T.job * kJobStride] = 0;
+    if (tid == 0) a.book.flags[CF_TICKET] = 0;
+    s_err = ~0ull;
+    s_min = INT_MAX;
+    s_max = INT_MIN;
   }
-  return __all_sync(0xffffffffu, eq);
-}
+  const uint32_t dim = J.dim;
+  const bool vlz = J.codec == EMBC_CODEC_VLZ;
+  const bool huf = J.codec == EMBC_CODEC_HUFFMAN;
+  uint32_t* shist = reinterpret_cast<uint32_t*>(smem + a.hist_off);
+  if (huf)
+    for (uint32_t b = threadIdx.x; b < kWin; b += blockDim.x) shist[b] = 0;
+  __syncthreads();
 
-__device__ __forceinline__ void sizes_tile(const DJob* __restrict__ jobs, const DTile* __restrict__ tiles,
-                                           const uint32_t* __restrict__ tile_list,
-                                           const JobState* __restrict__ st,
-                                           const uint64_t* __restrict__ row_hash,
-                                           const uint32_t* __restrict__ row_lit, uint32_t* __restrict__ row_off,
-                                           const uint64_t* __restrict__ lut, uint64_t* __restrict__ tile_sum,
-                                           uint8_t* smem) {
-  __shared__ unsigned long long s_tmp64[33];
-  const uint32_t tid = tile_list[blockIdx.x];
-  const DTile T = tiles[tid];
-  const DJob& J = jobs[T.job];
-  const JobState& S = st[T.job];
-  if (S.err != ~0ull) return;
-  uint64_t local = 0;
-  if (J.codec == EMBC_CODEC_VLZ) {
-    const uint32_t W = J.window;
-    const uint32_t lo = T.row0 > W ? T.row0 - W : 0;
-    const uint32_t nh = T.row0 + T.rows - lo;
-    const bool staged = nh <= kHashStage;
-    uint64_t* sh = reinterpret_cast<uint64_t*>(smem);
-    const uint64_t* gh = row_hash + J.row_base;
-    if (staged) {
-      for (uint32_t k = threadIdx.x; k < nh; k += blockDim.x) sh[k] = gh[lo + k];
-    }
-    __syncthreads();
-    for (uint32_t rb = 0; rb < T.rows; rb += blockDim.x) {
-      const uint32_t r = rb + threadIdx.x;
-      const bool active = r < T.rows;
-      const uint32_t i = T.row0 + r;
-      const uint64_t h = active ? (staged ? sh[i - lo] : gh[i]) : 0;
-      const uint32_t kmax = active ? min(W, i) : 0;
-      uint32_t k = 1;
-      uint32_t found = 0;  // offset of the verified match, 0 = literal
-      bool searching = active;
-      // advance to the next hash candidate
-      // nearest candidate first; four independent hash loads per step
-      auto next = [&]() {
-        while (k + 3 <= kmax) {
-          const uint32_t j = i - k;
-          uint64_t h0, h1, h2, h3;
-          if (staged) {
-            h0 = sh[j - lo];
-            h1 = sh[j - 1 - lo];
-            h2 = sh[j - 2 - lo];
-            h3 = sh[j - 3 - lo];
-          } else {
-            h0 = gh[j];
-            h1 = gh[j - 1];
-            h2 = gh[j - 2];
-            h3 = gh[j - 3];
-          }
-          if (h0 == h) return true;
-          if (h1 == h) { k += 1; return true; }
-          if (h2 == h) { k += 2; return true; }
-          if (h3 == h) { k += 3; return true; }
-          k += 4;
-        }
-        while (k <= kmax) {
-          const uint32_t j = i - k;
-          const uint64_t hj = staged ? sh[j - lo] : gh[j];
-          if (hj == h) return true;
-          ++k;
-        }
-        return false;
-      };
-      bool have = searching && next();
-      if (!have) searching = false;
-      // warp-cooperative exact verification of pending candidates
-      for (;;) {
-        const uint32_t pend = __ballot_sync(0xffffffffu, searching && have);
-        if (!pend) break;
-        uint32_t m = pend;
-        bool resolved_me = false, eq_me = false;
-        while (m) {
-          const int src = __ffs(m) - 1;
-          m &= m - 1;
-          const uint32_t ii = __shfl_sync(0xffffffffu, i, src);
-          const uint32_t jj = __shfl_sync(0xffffffffu, i - k, src);
-          const bool eq = warp_rows_equal(J, ii, jj);
-          if ((threadIdx.x & 31) == static_cast<uint32_t>(src)) {
-            resolved_me = true;
-            eq_me = eq;
+  const uint64_t e0 = static_cast<uint64_t>(T.row0) * dim;
+  const uint32_t ne = T.rows * dim;
+  unsigned long long lerr = ~0ull;
+  int lmin = INT_MAX, lmax = INT_MIN;
+  bool lwide = false;
+  const uint32_t qpr = dim >> 2;  // quads per row
+  const bool vec = (dim & 3) == 0 && (reinterpret_cast<uintptr_t>(J.src) & 15) == 0 &&
+                   (!vlz || (qpr <= 32 && (qpr & (qpr - 1)) == 0));
+  const uint64_t gbase = J.row_base + T.row0;
+  if (vec) {
+    // 128-bit loads, 4 quads in flight per thread; a row is qpr consecutive lanes
+    const uint32_t nq = ne >> 2;
+    const QParams qp = J.qp;
+    const bool f32 = J.src_kind == EMBC_SRC_F32;
+    const uint4* src4 = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(J.src) + e0);
+    for (uint32_t base = 0; base < nq; base += 4 * kBlock) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t q = base + u * kBlock + threadIdx.x;
+        if (q < nq) v[u] = __ldg(src4 + q);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t q = base + u * kBlock + threadIdx.x;
+        const bool ok = q < nq;
+        int32_t c[4] = {0, 0, 0, 0};
+        if (ok) {
+          const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (f32) {
+              uint32_t reason = 0;
+              c[k] = quantize_f32(__uint_as_float(w[k]), qp, &reason);
+              if (reason) lerr = min(lerr, static_cast<unsigned long long>(err_key(e0 + 4ull * q + k, reason)));
+            } else {
+              c[k] = static_cast<int32_t>(w[k]);
+            }
+            lmin = min(lmin, c[k]);
+            lmax = max(lmax, c[k]);
           }
         }
-        if (resolved_me) {
-          if (eq_me) {
-            found = k;
-            searching = false;
-          } else {
-            ++k;  // hash collision: keep looking further back
-            have = next();
-            if (!have) searching = false;
+        if (huf) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint32_t bin = 0xFFFFFFFFu;
+            if (ok) {
+              const uint32_t b = static_cast<uint32_t>(c[k] + static_cast<int32_t>(kWin / 2));
+              if (b < kWin) bin = b;
+              else lwide = true;
+            }
+            hist_add(shist, bin);
           }
+        }
+        if (vlz) {
+          const uint32_t col = (q & (qpr - 1)) * 4;
+          uint32_t h = 0, lit = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            h += elem_mix(c[k], col + k);
+            lit += varint_len(zigzag(c[k]));
+          }
+          for (uint32_t o = 1; o < qpr; o <<= 1) {
+            h += __shfl_xor_sync(0xffffffffu, h, o);
+            lit += __shfl_xor_sync(0xffffffffu, lit, o);
+          }
+          if (ok && (q & (qpr - 1)) == 0)
+            a.row_info[gbase + q / qpr] = (static_cast<uint64_t>(1 + lit) << 32) | h;
         }
       }
-      if (active) {
-        row_off[J.row_base + i] = found;
-        local += found ? 1u + varint_len(found) : row_lit[J.row_base + i];
+    }
+  } else {
+    // generic path: element loop, vlz codes staged at r * (dim|1) + col
+    int32_t* codes = reinterpret_cast<int32_t*>(smem);
+    const uint32_t stride = dim | 1u;
+    for (uint32_t l0 = 0; l0 < ne; l0 += kBlock) {
+      const uint32_t l = l0 + threadIdx.x;
+      const bool ok = l < ne;
+      int32_t c = 0;
+      if (ok) {
+        uint32_t reason = 0;
+        c = job_code(J, e0 + l, &reason);
+        if (reason) lerr = min(lerr, static_cast<unsigned long long>(err_key(e0 + l, reason)));
+        lmin = min(lmin, c);
+        lmax = max(lmax, c);
+      }
+      if (huf) {
+        uint32_t bin = 0xFFFFFFFFu;
+        if (ok) {
+          const uint32_t b = static_cast<uint32_t>(c + static_cast<int32_t>(kWin / 2));
+          if (b < kWin) bin = b;
+          else lwide = true;
+        }
+        hist_add(shist, bin);
+      }
+      if (vlz && ok) {
+        const uint32_t r = fdiv(l, J.fd);
+        codes[r * stride + (l - r * dim)] = c;
       }
     }
-  } else {  // huffman: bits of every code in the tile
-    const int32_t cmin = S.cmin;
-    const uint64_t* L = lut + S.lut_off;
-    const uint64_t e0 = static_cast<uint64_t>(T.row0) * J.dim;
-    const uint32_t ne = T.rows * J.dim;
-    for (uint32_t l = threadIdx.x; l < ne; l += blockDim.x) {
-      uint32_t r = 0;
-      const int32_t c = job_code(J, e0 + l, &r);
-      local += lut_entry(L, c, cmin) & 0xFF;
+    if (vlz) {
+      __syncthreads();
+      for (uint32_t r = threadIdx.x; r < T.rows; r += blockDim.x) {
+        const int32_t* row = codes + r * stride;
+        uint32_t h = 0, lit = 1;
+        for (uint32_t j = 0; j < dim; ++j) {
+          h += elem_mix(row[j], j);
+          lit += varint_len(zigzag(row[j]));
+        }
+        a.row_info[gbase + r] = (static_cast<uint64_t>(lit) << 32) | h;
+      }
     }
   }
-  const unsigned long long tot = block_sum<unsigned long long>(local, s_tmp64);
-  if (threadIdx.x == 0) tile_sum[tid] = tot;
+  // fold the tile's failure key and code range into the job state
+  JobState* Sp = &a.st[T.job];
+  lerr = warp_min_u64(lerr);
+  if ((threadIdx.x & 31) == 0 && lerr != ~0ull) atomicMin(&s_err, lerr);
+  if (huf) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+      lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&s_min, lmin);
+      atomicMax(&s_max, lmax);
+    }
+  }
+  const bool wide = __syncthreads_or(lwide);
+  if (threadIdx.x == 0) {
+    if (s_err != ~0ull) {
+      atomicMin(reinterpret_cast<unsigned long long*>(&Sp->err), s_err);
+      atomicOr(&a.book.flags[CF_ABORT], JF_ABORT);
+    }
+    if (huf && ne) {
+      atomicMin(&Sp->cmin, s_min);
+      atomicMax(&Sp->cmax, s_max);
+      if (wide) Sp->wide = 1;
+    }
+  }
+  if (huf && !wide && ne) {  // flush the occupied bins of the window
+    uint32_t* gh = a.book.hist + static_cast<uint64_t>(J.hjob) * kWin;
+    const uint32_t b0 = static_cast<uint32_t>(s_min + static_cast<int32_t>(kWin / 2));
+    const uint32_t b1 = static_cast<uint32_t>(s_max + static_cast<int32_t>(kWin / 2));
+    for (uint32_t b = b0 + threadIdx.x; b <= b1; b += blockDim.x) {
+      const uint32_t v = shist[b];
+      if (v) atomicAdd(&gh[b], v);
+    }
+  }
+  if (!huf) return;
+  // the job's last tile to finish builds the codebook
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&Sp->tiles_done, 1u) == J.ntiles - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  build_book(J, Sp, a.book, smem);
 }
 
 // ---------------------------------------------------------------------------
-// K4: layout, headers, pack table, metadata, failure folding (one CTA)
+// E2: sizes -> decoupled look-back -> bytes
 // ---------------------------------------------------------------------------
-struct LayoutArgs {
-  uint32_t njobs;
+struct EmitArgs {
+  const DJob* jobs;
+  const DTile* tiles;
+  JobState* st;
+  const uint64_t* row_info;
+  unsigned long long* tile_status;
+  unsigned long long* job_status;
+  uint32_t* edge_slot;
+  const uint64_t* lut;
+  const uint8_t* books;
+  uint64_t book_stride;
+  uint32_t* flags;
+  uint32_t njobs, ntiles;
   int layout;
   uint8_t* out;
   uint64_t cap;
@@ -557,103 +555,389 @@ struct LayoutArgs {
   uint64_t* d_lengths;
   uint8_t* d_meta;
   uint64_t* d_total;
-  uint32_t* call_flags;
   DevError* err;
-  int skip;  // match_stats: no layout
+  unsigned long long* d_stats;  // match_stats mode: (literals, references); no bytes
+  uint32_t stage_off, aux_off;  // dynamic smem carve
 };
 
-__device__ void layout_body(const DJob* __restrict__ jobs, JobState* st,
-                            const uint64_t* __restrict__ tile_sum, uint64_t* __restrict__ tile_off,
-                            const LayoutArgs& a) {
-  if (a.skip) return;
-  __shared__ unsigned long long s_tmp64[33];
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+// Warp-cooperative decoupled look-back: the exclusive prefix of element `i`
+// over status[first .. i-1], where status[first] always publishes an
+// inclusive value and `base` is the prefix before `first`.
+#ifdef EMBC_DEBUG
+__device__ unsigned long long g_dbg[8];
+__device__ unsigned long long g_ts[16384][6];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TS(k) do { if (threadIdx.x == 0 && tid < 16384) g_ts[tid][k] = gtime(); } while (0)
+#else
+#define TS(k) do {} while (0)
+#endif
+
+__device__ __forceinline__ uint64_t look_back(const unsigned long long* status, uint32_t first, uint32_t i,
+                                              uint64_t base, uint32_t stride = 1) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t acc = 0;
+  int64_t p = static_cast<int64_t>(i) - 1;
+  uint32_t delay = 32;
+  while (p >= static_cast<int64_t>(first)) {
+    const int64_t idx = p - lane;
+    unsigned long long s = kFlagInc;  // before `first`: inclusive 0 (never reached: first is inclusive)
+    if (idx >= static_cast<int64_t>(first)) s = ld_status(status + idx * stride);
+    const uint32_t inc = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+    const uint32_t zero = __ballot_sync(0xffffffffu, (s >> 62) == 0);
+    const int fi = inc ? __ffs(inc) - 1 : 32;
+    const uint32_t need = fi == 32 ? 0xffffffffu : ((2u << fi) - 1);
+    if (zero & need) {  // a predecessor has not published yet: back off, re-read
+#ifdef EMBC_DEBUG
+      if (lane == 0) atomicAdd(&g_dbg[stride == 1 ? 0 : 1], 1ull);
+#endif
+      __nanosleep(delay);
+      delay = min(delay * 2, 512u);
+      continue;
+    }
+    uint64_t v = (static_cast<int>(lane) <= fi) ? (s & kValMask) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    acc += v;
+    if (fi < 32) return acc;
+    p -= 32;
+  }
+  return acc + base;
+}
+
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+  __threadfence();
+  *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
+
+// fold the lowest failing job into the sticky record (layout order)
+__device__ void fold_failure(const EmitArgs& a) {
   __shared__ unsigned long long s_first;
   if (threadIdx.x == 0) s_first = ~0ull;
   __syncthreads();
-  // failure folding: lowest failing job, its first failure
-  for (uint32_t j = threadIdx.x; j < a.njobs; j += blockDim.x) {
-    if (st[j].err != ~0ull) atomicMin(&s_first, static_cast<unsigned long long>(j));
-  }
+  for (uint32_t j = threadIdx.x; j < a.njobs; j += blockDim.x)
+    if (a.st[j].err != ~0ull) atomicMin(&s_first, static_cast<unsigned long long>(j));
   __syncthreads();
-  const uint64_t base = a.layout == EMBC_LAYOUT_PACKED ? 4 + 16ull * a.njobs : 0;
-  // payload sizes + job-relative tile offsets
-  for (uint32_t j = threadIdx.x; j < a.njobs; j += blockDim.x) {
-    const DJob& J = jobs[j];
-    uint64_t P = 0;
-    if (J.codec == EMBC_CODEC_RAW) {
-      P = 4 * J.N;
-      uint64_t o = 0;
-      for (uint32_t t = 0; t < J.ntiles; ++t) {
-        tile_off[J.tile0 + t] = o;
-        o += 0;
+  if (threadIdx.x != 0) return;
+  if (a.d_total) *a.d_total = 0;
+  if (s_first == ~0ull || a.err->valid) return;
+  const uint32_t j = static_cast<uint32_t>(s_first);
+  const unsigned long long k = a.st[j].err & ~(1ull << 63);
+  a.err->valid = 1;
+  a.err->job = j;
+  a.err->reason = static_cast<int32_t>(k & 63);
+  a.err->index = k >> 6;
+  a.err->a = a.st[j].aux;
+  a.err->b = a.jobs[j].window;
+  a.err->eb = a.jobs[j].qp.eb;
+  a.err->status = (a.err->reason == EMBC_R_RANGE) ? EMBC_ERR_UNSUPPORTED : EMBC_ERR_VALUE;
+}
+
+// copy [a, b) of the staged bytes (stage[mis + k] <-> dst[k]) with 16-B stores
+__device__ __forceinline__ void copy_range(uint8_t* dst, const uint8_t* stage, uint32_t mis, uint64_t a, uint64_t b) {
+  if (b <= a) return;
+  const uint32_t m2 = (mis + static_cast<uint32_t>(a)) & 15u;
+  copy_out_staged(dst + a, stage + (mis + a - m2), b - a);
+}
+
+__global__ void __launch_bounds__(kBlock) k_emit(EmitArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_tmp32[33];
+  __shared__ unsigned long long s_tmp64[33];
+  __shared__ uint32_t s_t;
+  __shared__ unsigned long long s_pre, s_start;
+  if (threadIdx.x == 0) s_t = atomicAdd(&a.flags[CF_TICKET], 1u);
+  __syncthreads();
+  const uint32_t tid = s_t;  // tiles are processed in ticket order: look-back never waits on a later CTA
+  TS(0);
+  if (a.flags[CF_ABORT] & JF_ABORT) {
+    if (tid == 0 && !a.d_stats) fold_failure(a);
+    return;
+  }
+  const DTile T = a.tiles[tid];
+  const uint32_t jid = T.job;
+  const DJob& J = a.jobs[jid];
+  const JobState& S = a.st[jid];
+  const uint32_t dim = J.dim;
+  const uint64_t e0 = static_cast<uint64_t>(T.row0) * dim;
+  const uint32_t ne = T.rows * dim;
+  const bool first = tid == J.tile0, last = tid == J.tile0 + J.ntiles - 1;
+  int32_t* codes = reinterpret_cast<int32_t*>(smem);
+  uint8_t* stage = smem + a.stage_off;
+  uint8_t* aux = smem + a.aux_off;
+  const uint32_t codec = J.codec;
+  const uint32_t stride = codec == EMBC_CODEC_VLZ ? (dim | 1u) : 0;
+
+  // ---- 1. codes of the tile into shared memory (vlz: row stride dim|1;
+  //         huffman: l + l/32, conflict-free thread-contiguous reads)
+  if (codec != EMBC_CODEC_RAW && ne) {
+    const bool vec = (dim & 3) == 0 && (reinterpret_cast<uintptr_t>(J.src) & 15) == 0;
+    if (vec) {
+      const uint4* src4 = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(J.src) + e0);
+      const uint32_t nq = ne >> 2;
+      const bool f32 = J.src_kind == EMBC_SRC_F32;
+      for (uint32_t base = 0; base < nq; base += 4 * kBlock) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t q = base + u * kBlock + threadIdx.x;
+          if (q < nq) v[u] = __ldg(src4 + q);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t q = base + u * kBlock + threadIdx.x;
+          if (q >= nq) continue;
+          const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t l = 4 * q + k;
+            int32_t c;
+            if (f32) {
+              uint32_t r = 0;
+              c = quantize_f32(__uint_as_float(w[k]), J.qp, &r);
+            } else {
+              c = static_cast<int32_t>(w[k]);
+            }
+            uint32_t at;
+            if (stride) {
+              const uint32_t r = fdiv(l, J.fd);
+              at = r * stride + (l - r * dim);
+            } else {
+              at = l + (l >> 5);
+            }
+            codes[at] = c;
+          }
+        }
       }
     } else {
-      uint64_t o = 0;
-      for (uint32_t t = 0; t < J.ntiles; ++t) {
-        tile_off[J.tile0 + t] = o;
-        o += tile_sum[J.tile0 + t];
+      for (uint32_t l = threadIdx.x; l < ne; l += kBlock) {
+        uint32_t r = 0;
+        const int32_t c = job_code(J, e0 + l, &r);
+        uint32_t at;
+        if (stride) {
+          const uint32_t rr = fdiv(l, J.fd);
+          at = rr * stride + (l - rr * dim);
+        } else {
+          at = l + (l >> 5);
+        }
+        codes[at] = c;
       }
-      P = J.codec == EMBC_CODEC_VLZ ? o : st[j].payload;
-    }
-    if (J.N == 0 && J.codec != EMBC_CODEC_HUFFMAN) P = 0;
-    st[j].payload = P;
-  }
-  __syncthreads();
-  // chunk offsets: exclusive scan in job order (container.hpp:245-250)
-  uint64_t carry = base;
-  for (uint32_t j0 = 0; j0 < a.njobs; j0 += blockDim.x) {
-    const uint32_t j = j0 + threadIdx.x;
-    const uint64_t S = j < a.njobs ? jobs[j].header + st[j].payload : 0;
-    unsigned long long tot;
-    const unsigned long long pre = block_excl_scan<unsigned long long>(S, s_tmp64, &tot);
-    if (j < a.njobs) st[j].chunk_off = carry + pre;
-    carry += tot;
-  }
-  __syncthreads();
-  const uint64_t total = carry;
-  const bool failed = s_first != ~0ull;
-  const bool overflow = !failed && total > a.cap;
-  if (threadIdx.x == 0) {
-    *a.call_flags = (failed || overflow) ? JF_ABORT : 0;
-    if (a.d_total) *a.d_total = (failed || overflow) ? 0 : total;
-    if (failed && !a.err->valid) {
-      const uint32_t j = static_cast<uint32_t>(s_first);
-      const unsigned long long k = st[j].err & ~(1ull << 63);
-      a.err->valid = 1;
-      a.err->job = j;
-      a.err->reason = static_cast<int32_t>(k & 63);
-      a.err->index = k >> 6;
-      a.err->a = st[j].aux;
-      a.err->b = jobs[j].window;
-      a.err->eb = jobs[j].qp.eb;
-      const int r = a.err->reason;
-      a.err->status = (r == EMBC_R_RANGE) ? EMBC_ERR_UNSUPPORTED : EMBC_ERR_VALUE;
-    } else if (overflow && !a.err->valid) {
-      a.err->valid = 1;
-      a.err->job = 0;
-      a.err->reason = EMBC_R_CAPACITY;
-      a.err->index = 0;
-      a.err->a = total;
-      a.err->b = a.cap;
-      a.err->status = EMBC_ERR_CAPACITY;
     }
   }
-  if (failed || overflow) return;
-  if (a.layout == EMBC_LAYOUT_PACKED && threadIdx.x == 0) st_le(a.out, a.njobs, 4);
-  for (uint32_t j = threadIdx.x; j < a.njobs; j += blockDim.x) {
-    const DJob& J = jobs[j];
-    const uint64_t off = st[j].chunk_off;
-    const uint64_t len = J.header + st[j].payload;
-    if (a.d_offsets) a.d_offsets[j] = off;
-    if (a.d_lengths) a.d_lengths[j] = len;
-    if (a.layout == EMBC_LAYOUT_PACKED) {  // pack table (container.hpp:244-250)
-      st_le(a.out + 4 + 16ull * j, off, 8);
-      st_le(a.out + 12 + 16ull * j, len, 8);
+
+  __syncthreads();
+  TS(1);
+  // ---- 2. tile size in bits (payload only; the header / codebook bytes are
+  //         added at the job level)
+  uint64_t my_bits = 0;
+  uint32_t* dec = reinterpret_cast<uint32_t*>(aux + kHashStage * 4);  // vlz: match offset per row
+  uint32_t* lits = dec + kMaxTileRows;                                  // vlz: token bytes per row
+  uint32_t* cand = lits + kMaxTileRows;                                 // vlz: candidate offset under test
+  uint32_t* plist = cand + kMaxTileRows;                                // vlz: rows with a pending candidate
+  uint32_t* miss = plist + kMaxTileRows;                                // vlz: candidate disproved
+  uint32_t pos_thread = 0;                                              // huffman: this thread's first bit
+  const uint32_t per_h = (ne + kBlock - 1) / kBlock;
+  const uint64_t* L = a.lut + S.lut_off;
+  uint64_t* sl = reinterpret_cast<uint64_t*>(aux);
+  const int32_t cmin = S.cmin;
+  const uint32_t span = codec == EMBC_CODEC_HUFFMAN ? static_cast<uint32_t>(S.cmax - cmin + 1) : 0;
+  const bool lut_staged = span <= kLutStage;
+  if (codec == EMBC_CODEC_RAW) {
+    my_bits = 32ull * ne;
+  } else if (codec == EMBC_CODEC_VLZ) {
+    const uint32_t W = J.window;
+    const uint32_t lo = T.row0 > W ? T.row0 - W : 0;
+    const uint32_t nh = T.row0 + T.rows - lo;
+    const bool staged = nh <= kHashStage;
+    uint32_t* sh = reinterpret_cast<uint32_t*>(aux);
+    const uint64_t* ri = a.row_info + J.row_base;
+    if (staged)
+      for (uint32_t k = threadIdx.x; k < nh; k += kBlock) sh[k] = static_cast<uint32_t>(__ldg(ri + lo + k));
+    __syncthreads();
+    // nearest earlier row with an equal hash at offset >= k0, or 0
+    auto search = [&](uint32_t r, uint32_t k0) -> uint32_t {
+      const uint32_t i = T.row0 + r;
+      const uint32_t h = staged ? sh[i - lo] : static_cast<uint32_t>(__ldg(ri + i));
+      const uint32_t kmax = min(W, i);
+      uint32_t k = k0;
+      for (; k + 3 <= kmax; k += 4) {
+        const uint32_t j = i - k;
+        uint32_t h0, h1, h2, h3;
+        if (staged) {
+          h0 = sh[j - lo];
+          h1 = sh[j - 1 - lo];
+          h2 = sh[j - 2 - lo];
+          h3 = sh[j - 3 - lo];
+        } else {
+          h0 = static_cast<uint32_t>(__ldg(ri + j));
+          h1 = static_cast<uint32_t>(__ldg(ri + j - 1));
+          h2 = static_cast<uint32_t>(__ldg(ri + j - 2));
+          h3 = static_cast<uint32_t>(__ldg(ri + j - 3));
+        }
+        if (h0 == h) return k;
+        if (h1 == h) return k + 1;
+        if (h2 == h) return k + 2;
+        if (h3 == h) return k + 3;
+      }
+      for (; k <= kmax; ++k) {
+        const uint32_t j = i - k;
+        if ((staged ? sh[j - lo] : static_cast<uint32_t>(__ldg(ri + j))) == h) return k;
+      }
+      return 0;
+    };
+    // nearest identical row (vlz.hpp:86-103): hash candidates, nearest first,
+    // verified exactly for all rows of the tile at once (CodeRowEq, vlz.hpp:75-79)
+    for (uint32_t r = threadIdx.x; r < T.rows; r += kBlock) {
+      cand[r] = search(r, 1);
+      dec[r] = 0;
+    }
+    __syncthreads();
+    for (;;) {
+      uint32_t np = 0;  // compact the rows with a candidate under test
+      for (uint32_t r0 = 0; r0 < T.rows; r0 += kBlock) {
+        const uint32_t r = r0 + threadIdx.x;
+        const bool p = r < T.rows && cand[r] != 0;
+        uint32_t tot;
+        const uint32_t at = block_excl_scan<uint32_t>(p, s_tmp32, &tot);
+        if (p) {
+          plist[np + at] = r;
+          miss[np + at] = 0;
+        }
+        np += tot;
+      }
+      if (np == 0) break;
+      __syncthreads();
+      const uint32_t work = np * dim;
+      for (uint32_t e0w = 0; e0w < work; e0w += 4 * kBlock) {
+        int32_t cj[4], ci[4];
+        uint32_t pp[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // all loads first: four rows' elements in flight
+          const uint32_t e = e0w + u * kBlock + threadIdx.x;
+          pp[u] = 0xFFFFFFFFu;
+          if (e < work) {
+            const uint32_t pi = fdiv(e, J.fd);
+            const uint32_t col = e - pi * dim;
+            const uint32_t r = plist[pi];
+            const uint32_t i = T.row0 + r, j = i - cand[r];
+            pp[u] = pi;
+            ci[u] = codes[r * stride + col];
+            if (j >= T.row0) {
+              cj[u] = codes[(j - T.row0) * stride + col];
+            } else if (J.src_kind == EMBC_SRC_F32) {
+              cj[u] = __float_as_int(__ldg(static_cast<const float*>(J.src) + static_cast<uint64_t>(j) * dim + col));
+              pp[u] |= 0x80000000u;  // needs quantizing
+            } else {
+              cj[u] = __ldg(static_cast<const int32_t*>(J.src) + static_cast<uint64_t>(j) * dim + col);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (pp[u] == 0xFFFFFFFFu) continue;
+          int32_t c = cj[u];
+          if (pp[u] & 0x80000000u) {
+            uint32_t rr = 0;
+            c = quantize_f32(__int_as_float(c), J.qp, &rr);
+          }
+          if (c != ci[u]) miss[pp[u] & 0x7FFFFFFFu] = 1;
+        }
+      }
+      __syncthreads();
+      for (uint32_t q = threadIdx.x; q < np; q += kBlock) {
+        const uint32_t r = plist[q];
+        if (!miss[q]) {
+          dec[r] = cand[r];
+          cand[r] = 0;
+        } else {  // hash collision: keep looking further back
+          cand[r] = search(r, cand[r] + 1);
+        }
+      }
+      __syncthreads();
+    }
+    uint64_t local = 0, nref = 0;
+    for (uint32_t r = threadIdx.x; r < T.rows; r += kBlock) {
+      const uint32_t found = dec[r];
+      const uint32_t sz = found ? 1u + varint_len(found) : static_cast<uint32_t>(__ldg(ri + T.row0 + r) >> 32);
+      lits[r] = sz;
+      local += sz;
+      nref += found != 0;
+    }
+    if (a.d_stats) {  // match_stats (vlz.hpp:162-168)
+      nref = block_sum<unsigned long long>(nref, s_tmp64);
+      if (threadIdx.x == 0) {
+        atomicAdd(&a.d_stats[0], static_cast<unsigned long long>(T.rows) - nref);
+        atomicAdd(&a.d_stats[1], nref);
+      }
+      return;
+    }
+    my_bits = 8ull * block_sum<unsigned long long>(local, s_tmp64);
+  } else {  // huffman
+    if (lut_staged)
+      for (uint32_t k = threadIdx.x; k < span; k += kBlock) sl[k] = __ldg(L + k);
+    __syncthreads();
+    const uint32_t l0 = threadIdx.x * per_h, l1 = min(l0 + per_h, ne);
+    uint32_t nb = 0;
+    for (uint32_t l = l0; l < l1; ++l) {
+      const uint32_t s = static_cast<uint32_t>(codes[l + (l >> 5)] - cmin);
+      nb += static_cast<uint32_t>((lut_staged ? sl[s] : __ldg(L + s)) & 0xFF);
+    }
+    uint32_t tot;
+    pos_thread = block_excl_scan<uint32_t>(nb, s_tmp32, &tot);
+    my_bits = tot;
+  }
+
+  TS(2);
+  // ---- 3. offsets: look-back over the job's tiles (bits), then over jobs (bytes)
+  const uint64_t hdr = J.header;
+  const uint64_t book_bytes = codec == EMBC_CODEC_HUFFMAN ? 12 + 5ull * S.nsym : 0;
+  if (threadIdx.x < 32) {
+    uint64_t pre = 0;
+    if (first) {
+      if (threadIdx.x == 0) st_status(a.tile_status + tid, kFlagInc | my_bits);
+    } else {
+      if (threadIdx.x == 0) st_status(a.tile_status + tid, kFlagAgg | my_bits);
+      pre = look_back(a.tile_status, J.tile0, tid, 0);
+      if (threadIdx.x == 0) st_status(a.tile_status + tid, kFlagInc | (pre + my_bits));
+    }
+    TS(3);
+    const uint64_t job_bytes = hdr + book_bytes + (pre + my_bits + 7) / 8;
+    const uint64_t base = a.layout == EMBC_LAYOUT_PACKED ? 4 + 16ull * a.njobs : 0;
+    if (last && jid > 0 && threadIdx.x == 0) st_status(a.job_status + jid * kJobStride, kFlagAgg | job_bytes);
+    const uint64_t start = jid == 0 ? base : look_back(a.job_status, 0, jid, 0, kJobStride);
+    if (last && threadIdx.x == 0) st_status(a.job_status + jid * kJobStride, kFlagInc | (start + job_bytes));
+    TS(4);
+    if (threadIdx.x == 0) {
+      s_pre = pre;
+      s_start = start;
+    }
+  }
+  __syncthreads();
+  const uint64_t pre = s_pre, start = s_start;
+  const uint64_t pay_end = start + hdr + book_bytes + (pre + my_bits + 7) / 8;  // end of this job's bytes so far
+  uint8_t* pay = a.out + start + hdr;
+
+  // ---- 4. job-level records by the job's last tile (header, pack table, metadata)
+  if (last && threadIdx.x == 0) {
+    const uint64_t P = book_bytes + (pre + my_bits + 7) / 8;
+    const uint64_t len = hdr + P;
+    if (a.d_offsets) a.d_offsets[jid] = start;
+    if (a.d_lengths) a.d_lengths[jid] = len;
+    if (a.layout == EMBC_LAYOUT_PACKED && 20 + 16ull * jid <= a.cap) {  // pack table (container.hpp:244-250)
+      st_le(a.out + 4 + 16ull * jid, start, 8);
+      st_le(a.out + 12 + 16ull * jid, len, 8);
     }
     uint64_t ebits;
     memcpy(&ebits, &J.qp.eb, 8);
-    if (J.header) {  // serialize_chunk header (container.hpp:74-85)
-      uint8_t* h = a.out + off;
+    if (hdr && start + kHeader <= a.cap) {  // serialize_chunk header (container.hpp:74-85)
+      uint8_t* h = a.out + start;
       h[0] = 'E';
       h[1] = 'M';
       h[2] = 'B';
@@ -663,229 +947,203 @@ __device__ void layout_body(const DJob* __restrict__ jobs, JobState* st,
       st_le(h + 6, ebits, 8);
       st_le(h + 14, J.dim, 4);
       st_le(h + 18, J.n, 4);
-      st_le(h + 22, st[j].payload, 8);
+      st_le(h + 22, P, 8);
     }
     if (a.d_meta) {  // serialize_metadata(metadata_for(chunk)) (container.hpp:196-209)
-      uint8_t* m = a.d_meta + static_cast<uint64_t>(kMetaSize) * j;
-      st_le(m, kHeader + st[j].payload, 8);
+      uint8_t* m = a.d_meta + static_cast<uint64_t>(kMetaSize) * jid;
+      st_le(m, kHeader + P, 8);
       m[8] = J.codec;
       st_le(m + 9, ebits, 8);
       st_le(m + 17, J.dim, 4);
       st_le(m + 21, J.n, 4);
     }
+    if (tid == a.ntiles - 1) {  // the call's last byte
+      const uint64_t total = start + len;
+      if (total > a.cap) {
+        if (a.d_total) *a.d_total = 0;
+        if (!a.err->valid) {
+          a.err->valid = 1;
+          a.err->job = 0;
+          a.err->reason = EMBC_R_CAPACITY;
+          a.err->index = 0;
+          a.err->a = total;
+          a.err->b = a.cap;
+          a.err->status = EMBC_ERR_CAPACITY;
+        }
+      } else if (a.d_total) {
+        *a.d_total = total;
+      }
+    }
   }
-}
-
-// K3 kernel: vlz decisions / huffman bit counts per tile; the last CTA to
-// finish lays the call out (one launch instead of two).
-__global__ void __launch_bounds__(kBlock) k_sizes(const DJob* __restrict__ jobs,
-                                                  const DTile* __restrict__ tiles,
-                                                  const uint32_t* __restrict__ tile_list, uint32_t nlist,
-                                                  JobState* __restrict__ st,
-                                                  const uint64_t* __restrict__ row_hash,
-                                                  const uint32_t* __restrict__ row_lit,
-                                                  uint32_t* __restrict__ row_off,
-                                                  const uint64_t* __restrict__ lut,
-                                                  uint64_t* __restrict__ tile_sum,
-                                                  uint64_t* __restrict__ tile_off,
-                                                  uint32_t* __restrict__ done_ctr, LayoutArgs la) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ int s_last;
-  if (blockIdx.x < nlist)
-    sizes_tile(jobs, tiles, tile_list, st, row_hash, row_lit, row_off, lut, tile_sum, smem);
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    layout_body(jobs, st, tile_sum, tile_off, la);
+  if (tid == 0 && threadIdx.x == 0 && a.layout == EMBC_LAYOUT_PACKED && a.cap >= 4) st_le(a.out, a.njobs, 4);
+#ifdef EMBC_DEBUG
+  if (threadIdx.x == 0 && atomicAdd(&g_dbg[2], 1ull) == a.ntiles - 1 && (g_dbg[2] = 0, a.ntiles > 1000) &&
+      atomicAdd(&g_dbg[3], 1ull) % 8 == 7) {
+    printf("k_emit: tiles %u tile-spins %llu job-spins %llu\n", a.ntiles, g_dbg[0], g_dbg[1]);
+    g_dbg[0] = g_dbg[1] = 0;
+    unsigned long long t0 = ~0ull;
+    for (uint32_t t = 0; t < a.ntiles; ++t) t0 = min(t0, g_ts[t][0]);
+    for (uint32_t j = 0; j < a.njobs; ++j) {
+      unsigned long long mn[5] = {~0ull, ~0ull, ~0ull, ~0ull, ~0ull}, mx[5] = {0, 0, 0, 0, 0};
+      for (uint32_t t = a.jobs[j].tile0; t < a.jobs[j].tile0 + a.jobs[j].ntiles; ++t)
+        for (int k = 0; k < 5; ++k) { mn[k] = min(mn[k], g_ts[t][k] - t0); mx[k] = max(mx[k], g_ts[t][k] - t0); }
+      printf("job %2u codec %u start [%6llu %6llu] loaded [%6llu %6llu] sized [%6llu %6llu] tilelb [%6llu %6llu] joblb [%6llu %6llu] ns\n",
+             j, a.jobs[j].codec, mn[0], mx[0], mn[1], mx[1], mn[2], mx[2], mn[3], mx[3], mn[4], mx[4]);
+    }
   }
-}
+#endif
+  const bool fits = pay_end <= a.cap;
 
-// ---------------------------------------------------------------------------
-// K5: byte emission
-// ---------------------------------------------------------------------------
-constexpr uint32_t kStageBytes = 48 * 1024;
-
-__global__ void __launch_bounds__(kBlock) k_emit(const DJob* __restrict__ jobs,
-                                                 const DTile* __restrict__ tiles,
-                                                 JobState* __restrict__ st,
-                                                 const uint32_t* __restrict__ row_off,
-                                                 const uint32_t* __restrict__ row_lit,
-                                                 const uint64_t* __restrict__ tile_off,
-                                                 const uint64_t* __restrict__ tile_sum,
-                                                 const uint64_t* __restrict__ lut,
-                                                 const uint8_t* __restrict__ books,
-                                                 uint64_t book_stride, uint8_t* __restrict__ out,
-                                                 uint8_t* __restrict__ edges,
-                                                 const uint32_t* __restrict__ call_flags) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_tmp32[33];
-  __shared__ unsigned long long s_tmp64[33];
-  if (*call_flags & JF_ABORT) return;
-  const uint32_t tid = blockIdx.x;
-  const DTile T = tiles[tid];
-  const DJob& J = jobs[T.job];
-  JobState& S = st[T.job];
-  const uint32_t dim = J.dim;
-  const uint64_t e0 = static_cast<uint64_t>(T.row0) * dim;
-  const uint32_t ne = T.rows * dim;
-  uint8_t* pay = out + S.chunk_off + J.header;
-
-  if (J.codec == EMBC_CODEC_RAW) {  // u32le codes (container.hpp:128-133)
+  // ---- 5. bytes
+  if (codec == EMBC_CODEC_RAW) {  // u32le codes (container.hpp:128-133)
+    if (!fits || !ne) return;
     uint8_t* dst = pay + 4 * e0;
-    const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uint64_t>(dst) & 15);
-    for (uint32_t l = threadIdx.x; l < ne; l += blockDim.x) {
+    const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 15);
+    const bool vec = (dim & 3) == 0 && (reinterpret_cast<uintptr_t>(J.src) & 15) == 0 && J.src_kind == EMBC_SRC_F32;
+    if (vec && mis == 0) {  // aligned: quantize straight into 16-B stores
+      const uint4* src4 = reinterpret_cast<const uint4*>(static_cast<const float*>(J.src) + e0);
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      for (uint32_t q = threadIdx.x; q < ne / 4; q += kBlock) {
+        const uint4 v = __ldg(src4 + q);
+        uint32_t r = 0;
+        uint4 o;
+        o.x = static_cast<uint32_t>(quantize_f32(__uint_as_float(v.x), J.qp, &r));
+        o.y = static_cast<uint32_t>(quantize_f32(__uint_as_float(v.y), J.qp, &r));
+        o.z = static_cast<uint32_t>(quantize_f32(__uint_as_float(v.z), J.qp, &r));
+        o.w = static_cast<uint32_t>(quantize_f32(__uint_as_float(v.w), J.qp, &r));
+        d4[q] = o;
+      }
+      return;
+    }
+    for (uint32_t l = threadIdx.x; l < ne; l += kBlock) {
       uint32_t r = 0;
       const uint32_t c = static_cast<uint32_t>(job_code(J, e0 + l, &r));
-      uint8_t* s = smem + mis + 4 * l;
+      uint8_t* s = stage + mis + 4 * l;
       s[0] = static_cast<uint8_t>(c);
       s[1] = static_cast<uint8_t>(c >> 8);
       s[2] = static_cast<uint8_t>(c >> 16);
       s[3] = static_cast<uint8_t>(c >> 24);
     }
     __syncthreads();
-    copy_out_staged(dst, smem, 4ull * ne);
+    copy_out_staged(dst, stage, 4ull * ne);
     return;
   }
 
-  if (J.codec == EMBC_CODEC_VLZ) {  // token stream (vlz.hpp:111-125)
-    uint8_t* dst = pay + tile_off[tid];
-    const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uint64_t>(dst) & 15);
-    uint32_t* roff = reinterpret_cast<uint32_t*>(smem + kStageBytes);  // per-row byte offset
-    // token sizes, thread-contiguous rows
-    const uint32_t per = (T.rows + blockDim.x - 1) / blockDim.x;
-    const uint32_t r0 = threadIdx.x * per;
+  if (codec == EMBC_CODEC_VLZ) {  // token stream (vlz.hpp:111-125)
+    if (!fits) return;
+    uint8_t* dst = pay + pre / 8;
+    const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 15);
+    uint32_t* roff = lits;  // token sizes -> byte offsets inside the tile (in place)
+    const uint32_t per = (T.rows + kBlock - 1) / kBlock;
+    const uint32_t r0 = threadIdx.x * per, r1 = min(r0 + per, T.rows);
     uint32_t sum = 0;
-    for (uint32_t r = r0; r < min(r0 + per, T.rows); ++r) {
-      const uint64_t g = J.row_base + T.row0 + r;
-      const uint32_t o = row_off[g];
-      sum += o ? 1 + varint_len(o) : row_lit[g];
-    }
+    for (uint32_t r = r0; r < r1; ++r) sum += lits[r];
+    __syncthreads();
     uint32_t tot;
-    uint32_t pre = block_excl_scan<uint32_t>(sum, s_tmp32, &tot);
-    for (uint32_t r = r0; r < min(r0 + per, T.rows); ++r) {
-      const uint64_t g = J.row_base + T.row0 + r;
-      const uint32_t o = row_off[g];
-      roff[r] = pre;
+    uint32_t p = block_excl_scan<uint32_t>(sum, s_tmp32, &tot);
+    for (uint32_t r = r0; r < r1; ++r) {
+      const uint32_t sz = roff[r];
+      roff[r] = p;
+      const uint32_t o = dec[r];
       if (o) {  // reference token: 0x01, varint(offset)
-        uint8_t* p = smem + mis + pre;
-        *p++ = 0x01;
-        put_varint(p, o);
-        pre += 1 + varint_len(o);
-      } else {
-        pre += row_lit[g];
+        uint8_t* q = stage + mis + p;
+        *q++ = 0x01;
+        put_varint(q, o);
       }
+      p += sz;
     }
     __syncthreads();
     // literal tokens: 0x00 then dim zigzag varints, one warp per row
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    for (uint32_t r = warp; r < T.rows; r += nwarps) {
-      const uint64_t g = J.row_base + T.row0 + r;
-      if (row_off[g]) continue;
-      uint8_t* p = smem + mis + roff[r];
-      if (lane == 0) p[0] = 0x00;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t r = warp; r < T.rows; r += kBlock / 32) {
+      if (dec[r]) continue;
+      uint8_t* q = stage + mis + roff[r];
+      if (lane == 0) q[0] = 0x00;
       uint32_t carry = 1;
+      const int32_t* row = codes + r * stride;
       for (uint32_t j0 = 0; j0 < dim; j0 += 32) {
         const uint32_t j = j0 + lane;
         uint32_t z = 0, len = 0;
         if (j < dim) {
-          uint32_t rr = 0;
-          z = zigzag(job_code(J, (e0 + static_cast<uint64_t>(r) * dim) + j, &rr));
+          z = zigzag(row[j]);
           len = varint_len(z);
         }
         const uint32_t inc = warp_incl_scan<uint32_t>(len);
-        if (j < dim) put_varint(p + carry + inc - len, z);
+        if (j < dim) put_varint(q + carry + inc - len, z);
         carry += __shfl_sync(0xffffffffu, inc, 31);
       }
     }
     __syncthreads();
-    copy_out_staged(dst, smem, tot);
+    copy_out_staged(dst, stage, tot);
     return;
   }
 
-  // huffman bitstream: MSB-first (bitstream.hpp:32-51)
-  {
-    const uint64_t bit0 = tile_off[tid];  // bit offset of this tile in the bitstream
-    uint8_t* stream = pay + 12 + 5ull * S.nsym;
-    uint8_t* dst = stream + (bit0 >> 3);
-    const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uint64_t>(dst) & 15);
-    const uint32_t b0 = static_cast<uint32_t>(bit0 & 7);
-    // tile 0 of the job also writes the serialized codebook (huffman.hpp:202-209)
-    if (T.row0 == 0) {
-      const uint8_t* bk = books + static_cast<uint64_t>(J.hjob) * book_stride;
-      const uint64_t blen = 12 + 5ull * S.nsym;
-      for (uint64_t k = threadIdx.x; k < blen; k += blockDim.x) pay[k] = bk[k];
-    }
-    int32_t* codes = reinterpret_cast<int32_t*>(smem + kStageBytes);  // padded: l + l/32
-    for (uint32_t l = threadIdx.x; l < ne; l += blockDim.x) {
-      uint32_t r = 0;
-      codes[l + (l >> 5)] = job_code(J, e0 + l, &r);
-    }
-    uint32_t* words = reinterpret_cast<uint32_t*>(smem);
-    const uint32_t nwords = static_cast<uint32_t>((8 * mis + b0 + tile_sum[tid]) >> 5) + 2;
-    for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) words[w] = 0;
-    __syncthreads();
-    const int32_t cmin = S.cmin;
-    const uint64_t* L = lut + S.lut_off;
-    const uint32_t per = (ne + blockDim.x - 1) / blockDim.x;
-    const uint32_t l0 = threadIdx.x * per, l1 = min(l0 + per, ne);
-    uint32_t nb = 0;
-    for (uint32_t l = l0; l < l1; ++l) nb += lut_entry(L, codes[l + (l >> 5)], cmin) & 0xFF;
-    uint32_t tot;
-    uint32_t pos = block_excl_scan<uint32_t>(nb, s_tmp32, &tot) + 8 * mis + b0;
+  // huffman bitstream, MSB-first (bitstream.hpp:32-51)
+  uint8_t* bstream = pay + book_bytes;
+  if (first && fits) {  // the serialized codebook (huffman.hpp:202-209)
+    const uint8_t* bk = a.books + static_cast<uint64_t>(J.hjob) * a.book_stride;
+    for (uint64_t k = threadIdx.x; k < book_bytes; k += kBlock) pay[k] = bk[k];
+  }
+  uint8_t* dst = bstream + (pre >> 3);
+  const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 15);
+  const uint32_t b0 = static_cast<uint32_t>(pre & 7);
+  uint32_t* words = reinterpret_cast<uint32_t*>(stage);
+  const uint32_t lead = 8 * mis + b0;
+  const uint32_t endbit = lead + static_cast<uint32_t>(my_bits);
+  const uint32_t nwords = (endbit + 31) / 32;
+  for (uint32_t w = threadIdx.x; w < nwords + 1; w += kBlock) words[w] = 0;
+  __syncthreads();
+  {  // this thread's codes, assembled in a register and stored word by word
+    const uint32_t l0 = threadIdx.x * per_h, l1 = min(l0 + per_h, ne);
+    uint32_t p = lead + pos_thread;
+    uint32_t wi = p >> 5, used = p & 31;
+    uint64_t buf = 0;
+    bool shared_word = true;  // the first word may be shared with the previous thread
     for (uint32_t l = l0; l < l1; ++l) {
-      const uint64_t e = lut_entry(L, codes[l + (l >> 5)], cmin);
+      const uint32_t s = static_cast<uint32_t>(codes[l + (l >> 5)] - cmin);
+      const uint64_t e = lut_staged ? sl[s] : __ldg(L + s);
       const uint32_t len = static_cast<uint32_t>(e & 0xFF);
-      const uint64_t cw = e >> 8;
-      const uint32_t off = pos & 31;
-      const uint64_t v = cw << (64 - off - len);
-      atomicOr(&words[pos >> 5], static_cast<uint32_t>(v >> 32));
-      const uint32_t lo = static_cast<uint32_t>(v);
-      if (lo) atomicOr(&words[(pos >> 5) + 1], lo);
-      pos += len;
-    }
-    __syncthreads();
-    const uint32_t endbit = 8 * mis + b0 + tot;
-    const uint32_t nbytes_stage = (endbit + 7) / 8;  // stage bytes incl. the leading `mis`
-    for (uint32_t w = threadIdx.x; w < (nbytes_stage + 3) / 4; w += blockDim.x)
-      words[w] = __byte_perm(words[w], 0, 0x0123);
-    __syncthreads();
-    const uint32_t nbytes = nbytes_stage - mis;
-    // boundary bytes shared with the neighbouring tiles are merged by K6
-    if (threadIdx.x == 0) {
-      edges[2 * tid] = smem[mis];                  // first byte (partial if b0 != 0)
-      edges[2 * tid + 1] = smem[nbytes_stage - 1];  // last byte (partial if endbit % 8)
-    }
-    copy_out_staged(dst, smem, nbytes);
-    // the job's last tile to finish merges the bytes shared by adjacent tiles
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(&S.tiles_done, 1u) == J.ntiles - 1;
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      for (uint32_t k = 1 + threadIdx.x; k < J.ntiles; k += blockDim.x) {
-        const uint32_t t2 = J.tile0 + k;
-        const uint64_t b = __ldcg(tile_off + t2);
-        if (b & 7) stream[b >> 3] = __ldcg(edges + 2 * (t2 - 1) + 1) | __ldcg(edges + 2 * t2);
+      buf |= (e >> 8) << (64 - used - len);
+      used += len;
+      if (used >= 32) {
+        const uint32_t w = static_cast<uint32_t>(buf >> 32);
+        if (shared_word) atomicOr(&words[wi], w);
+        else words[wi] = w;
+        shared_word = false;
+        buf <<= 32;
+        used -= 32;
+        ++wi;
       }
     }
+    if (used) atomicOr(&words[wi], static_cast<uint32_t>(buf >> 32));  // may be shared with the next thread
   }
-}
-
-__global__ void k_count_refs(const uint32_t* __restrict__ row_off, uint32_t n,
-                             unsigned long long* __restrict__ cnt) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool ref = i < n && row_off[i] != 0;
-  const bool lit = i < n && row_off[i] == 0;
-  const uint32_t nr = __popc(__ballot_sync(0xffffffffu, ref));
-  const uint32_t nl = __popc(__ballot_sync(0xffffffffu, lit));
-  if ((threadIdx.x & 31) == 0) {
-    if (nl) atomicAdd(&cnt[0], nl);
-    if (nr) atomicAdd(&cnt[1], nr);
+  __syncthreads();
+  const uint32_t nbytes_stage = (endbit + 7) / 8;
+  for (uint32_t w = threadIdx.x; w < (nbytes_stage + 3) / 4; w += kBlock) words[w] = __byte_perm(words[w], 0, 0x0123);
+  __syncthreads();
+  const uint32_t nbytes = nbytes_stage - mis;  // output bytes touched by this tile
+  const bool head_shared = b0 != 0;
+  const bool tail_shared = !last && (endbit & 7) != 0;
+  if (fits) copy_range(dst, stage, mis, head_shared ? 1 : 0, nbytes - (tail_shared ? 1 : 0));
+  // bytes shared with the neighbouring tiles: the second of the two to arrive
+  // writes the OR of both halves and re-arms the slot (kept zero between calls)
+  if (threadIdx.x == 0) {
+    if (head_shared) {
+      const uint32_t mine = stage[mis];
+      const uint32_t old = atomicOr(&a.edge_slot[tid], 0x100u | mine);
+      if (old & 0x200u) {
+        if (fits) dst[0] = static_cast<uint8_t>((old | mine) & 0xFF);
+        a.edge_slot[tid] = 0;
+      }
+    }
+    if (tail_shared) {
+      const uint32_t mine = stage[nbytes_stage - 1];
+      const uint32_t old = atomicOr(&a.edge_slot[tid + 1], 0x200u | mine);
+      if (old & 0x100u) {
+        if (fits) dst[nbytes - 1] = static_cast<uint8_t>((old | mine) & 0xFF);
+        a.edge_slot[tid + 1] = 0;
+      }
+    }
   }
 }
 
@@ -912,14 +1170,13 @@ struct Carve {
 };
 
 static uint32_t pick_tile_rows(uint32_t dim, uint64_t total_values) {
-  // target ~2 tiles per SM on a 148-SM part, 1K..8K values per tile
+  // ~2 tiles per SM on a 148-SM part, 1K..4K values per tile, <= 1024 rows
   uint64_t target = total_values / 296;
-  target = std::max<uint64_t>(1024, std::min<uint64_t>(8192, target));
-  uint32_t rows = static_cast<uint32_t>(std::max<uint64_t>(1, target / std::max<uint32_t>(dim, 1)));
-  rows = std::min<uint32_t>(rows, 1024);
-  while (rows > 1 && static_cast<uint64_t>(rows) * dim > 8192) --rows;
-  if (static_cast<uint64_t>(rows) * dim < 8) rows = std::min<uint32_t>(1024, (8 + dim - 1) / dim);
-  return rows;
+  target = std::max<uint64_t>(1024, std::min<uint64_t>(kTileVals, target));
+  uint64_t rows = std::max<uint64_t>(1, target / std::max<uint32_t>(dim, 1));
+  rows = std::min<uint64_t>(rows, kMaxTileRows);
+  while (rows > 1 && rows * dim > kTileVals) --rows;
+  return static_cast<uint32_t>(rows);
 }
 
 uint64_t encode_bound(const embc_job* jobs, uint32_t njobs, int layout) {
@@ -947,7 +1204,7 @@ embc_status encode(embc_ctx* ctx, const embc_job* hj, uint32_t njobs, int layout
                      stream, nullptr);
 }
 
-// match_stats (vlz.hpp:162-168): the K1/K3 dedup decisions of one job, counted.
+// match_stats (vlz.hpp:162-168): the E1/E2 dedup decisions of one job, counted.
 embc_status match_stats(embc_ctx* ctx, const int32_t* d_codes, uint32_t dim, uint32_t n,
                         uint32_t window, uint64_t* h_lit, uint64_t* h_ref, cudaStream_t stream) {
   if (window < 1 || window > kMaxWindow)  // VlzConfig::validate (vlz.hpp:39-43)
@@ -992,12 +1249,14 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   //      reference as well: ErrorBound ctor at container.hpp:308, check_shape)
   ctx->job_eb.assign(njobs, 0.0);
   ctx->job_window.assign(njobs, 0);
+  if (njobs == 0) return EMBC_OK;
   std::vector<DJob> jobs(njobs);
   std::vector<DTile> tiles;
   uint64_t total_values = 0, total_rows = 0;
   for (uint32_t j = 0; j < njobs; ++j) total_values += static_cast<uint64_t>(hj[j].dim) * hj[j].n;
   uint32_t nhuff = 0;
   uint64_t hist_entries = 0;
+  bool host_abort = false;
   for (uint32_t j = 0; j < njobs; ++j) {
     const embc_job& in = hj[j];
     ctx->job_eb[j] = in.eb;
@@ -1009,7 +1268,7 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
       return set_error(ctx, EMBC_ERR_ARGUMENT, 0, j, 0, 0, 0, "invalid job descriptor");
     if (in.dim == 0)
       return set_error(ctx, EMBC_ERR_VALUE, EMBC_R_DIM0, j, 0, 0, 0, "embedding batch dim must be >= 1");
-    if (in.dim > 8192)
+    if (in.dim > kMaxRowVals)
       return set_error(ctx, EMBC_ERR_UNSUPPORTED, 0, j, 0, 0, 0, "dim > 8192 is outside the GPU tile envelope");
     DJob& J = jobs[j];
     J.src = in.src;
@@ -1038,6 +1297,7 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
       J.hist_cap = std::min<uint64_t>(std::max<uint64_t>(J.N, 1), kHistCap);  // bound on distinct symbols
       hist_entries += kWin;
     }
+    if (in.codec == EMBC_CODEC_VLZ && !J.window_ok) host_abort = true;
     J.tile_rows = pick_tile_rows(in.dim, total_values);
     J.tile0 = static_cast<uint32_t>(tiles.size());
     for (uint32_t r = 0; r < in.n; r += J.tile_rows) {
@@ -1047,21 +1307,18 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
       t.rows = std::min<uint32_t>(J.tile_rows, in.n - r);
       tiles.push_back(t);
     }
+    if (in.n == 0) tiles.push_back(DTile{j, 0, 0, 0});  // every job publishes through one tile
     J.ntiles = static_cast<uint32_t>(tiles.size()) - J.tile0;
   }
   const uint32_t ntiles = static_cast<uint32_t>(tiles.size());
-  std::vector<uint32_t> list_nonraw, list_huff_tiles, list_hjobs;
-  for (uint32_t t = 0; t < ntiles; ++t) {
-    const uint8_t c = jobs[tiles[t].job].codec;
-    if (c != EMBC_CODEC_RAW) list_nonraw.push_back(t);
-    if (c == EMBC_CODEC_HUFFMAN) list_huff_tiles.push_back(t);
+  uint32_t vals_max = 1, rows_max = 1;
+  for (const DTile& t : tiles) {
+    vals_max = std::max(vals_max, t.rows * jobs[t.job].dim);
+    rows_max = std::max(rows_max, t.rows);
   }
   uint64_t book_cap = 1;
   for (uint32_t j = 0; j < njobs; ++j)
-    if (jobs[j].codec == EMBC_CODEC_HUFFMAN) {
-      list_hjobs.push_back(j);
-      book_cap = std::max<uint64_t>(book_cap, jobs[j].hist_cap);
-    }
+    if (jobs[j].codec == EMBC_CODEC_HUFFMAN) book_cap = std::max<uint64_t>(book_cap, jobs[j].hist_cap);
   uint64_t p2cap = 1;
   while (p2cap < book_cap) p2cap <<= 1;
   const uint64_t book_stride = align_up(12 + 5 * book_cap, 16);
@@ -1072,17 +1329,12 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   const size_t o_jobs = cv.take<DJob>(njobs);
   const size_t o_tiles = cv.take<DTile>(ntiles);
   const size_t o_st = cv.take<JobState>(njobs);
-  const size_t o_l1 = cv.take<uint32_t>(list_nonraw.size() + 1);
-  const size_t o_l2 = cv.take<uint32_t>(list_huff_tiles.size() + 1);
-  const size_t o_l3 = cv.take<uint32_t>(list_hjobs.size() + 1);
-  const size_t o_flags = cv.take<uint32_t>(4);
+  const size_t o_flags = cv.take<uint32_t>(8);
   const size_t host_bytes = cv.off;  // everything above is uploaded from the host
-  const size_t o_hash = cv.take<uint64_t>(total_rows + 1);
-  const size_t o_lit = cv.take<uint32_t>(total_rows + 1);
-  const size_t o_off = cv.take<uint32_t>(total_rows + 1);
-  const size_t o_tsum = cv.take<uint64_t>(ntiles + 1);
-  const size_t o_toff = cv.take<uint64_t>(ntiles + 1);
-  const size_t o_edges = cv.take<uint8_t>(2ull * ntiles + 2);
+  const size_t o_info = cv.take<uint64_t>(total_rows + 1);
+  const size_t o_tstat = cv.take<unsigned long long>(ntiles + 1);
+  const size_t o_jstat = cv.take<unsigned long long>(kJobStride * (njobs + 1), 128);
+  const size_t o_slot = cv.take<uint32_t>(ntiles + 1);
   hist_entries += kWidePool;  // [nhuff windows | wide pool], LUT mirrors the layout
   const size_t o_lut = cv.take<uint64_t>(hist_entries + 1);
   const size_t o_books = cv.take<uint8_t>(book_stride * std::max<uint32_t>(nhuff, 1));
@@ -1115,103 +1367,74 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
       s.err = err_key(0, EMBC_R_BAD_WINDOW) | (1ull << 63);
     std::memcpy(hs + o_st + sizeof(JobState) * j, &s, sizeof(JobState));
   }
-  std::memcpy(hs + o_l1, list_nonraw.data(), sizeof(uint32_t) * list_nonraw.size());
-  std::memcpy(hs + o_l2, list_huff_tiles.data(), sizeof(uint32_t) * list_huff_tiles.size());
-  std::memcpy(hs + o_l3, list_hjobs.data(), sizeof(uint32_t) * list_hjobs.size());
-  std::memset(hs + o_flags, 0, 16);
+  uint32_t flags0[8] = {host_abort ? JF_ABORT : 0u, 0, 0, 0, 0, 0, 0, 0};
+  std::memcpy(hs + o_flags, flags0, sizeof(flags0));
   uint8_t* d = ctx->d_scratch;
   ce = cudaMemcpyAsync(d, hs, host_bytes, cudaMemcpyHostToDevice, stream);
   if (ce == cudaSuccess) ce = stage_commit(ctx, slot, stream);
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "descriptor upload");
 
-  const DJob* d_jobs = reinterpret_cast<const DJob*>(d + o_jobs);
-  const DTile* d_tiles = reinterpret_cast<const DTile*>(d + o_tiles);
-  JobState* d_st = reinterpret_cast<JobState*>(d + o_st);
-  uint32_t* d_flags = reinterpret_cast<uint32_t*>(d + o_flags);
-  uint64_t* d_hash = reinterpret_cast<uint64_t*>(d + o_hash);
-  uint32_t* d_lit = reinterpret_cast<uint32_t*>(d + o_lit);
-  uint32_t* d_off = reinterpret_cast<uint32_t*>(d + o_off);
-  uint64_t* d_tsum = reinterpret_cast<uint64_t*>(d + o_tsum);
-  uint64_t* d_toff = reinterpret_cast<uint64_t*>(d + o_toff);
-  uint8_t* d_edges = d + o_edges;
-  uint64_t* d_lut = reinterpret_cast<uint64_t*>(d + o_lut);
-  uint8_t* d_books = d + o_books;
-  uint32_t* d_hist = reinterpret_cast<uint32_t*>(ctx->d_hist);
+  StatsArgs sa{};
+  sa.jobs = reinterpret_cast<const DJob*>(d + o_jobs);
+  sa.tiles = reinterpret_cast<const DTile*>(d + o_tiles);
+  sa.st = reinterpret_cast<JobState*>(d + o_st);
+  sa.row_info = reinterpret_cast<uint64_t*>(d + o_info);
+  sa.tile_status = reinterpret_cast<unsigned long long*>(d + o_tstat);
+  sa.job_status = reinterpret_cast<unsigned long long*>(d + o_jstat);
+  sa.edge_slot = reinterpret_cast<uint32_t*>(d + o_slot);
+  sa.book.hist = reinterpret_cast<uint32_t*>(ctx->d_hist);
+  sa.book.lut = reinterpret_cast<uint64_t*>(d + o_lut);
+  sa.book.books = d + o_books;
+  sa.book.book_stride = book_stride;
+  if (big_books) {
+    sa.book.gs.key = reinterpret_cast<uint64_t*>(d + o_gkey);
+    sa.book.gs.wgt = reinterpret_cast<uint64_t*>(d + o_gwgt);
+    sa.book.gs.parent = reinterpret_cast<int32_t*>(d + o_gpar);
+  }
+  sa.book.gs_stride = p2cap;
+  sa.book.nhuff = nhuff;
+  sa.book.flags = reinterpret_cast<uint32_t*>(d + o_flags);
+  sa.hist_off = stats_codes_bytes(vals_max, rows_max);
+  const uint32_t stats_smem = sa.hist_off + (nhuff ? kWin * 4 : 0);
 
-  // The staged job state makes a raw-only call with a bad window impossible;
-  // the stage-2 key above is folded like any other device failure.
-  const uint32_t max_rows_stride = [&] {
-    uint32_t m = 0;
-    for (uint32_t j = 0; j < njobs; ++j) m = std::max(m, jobs[j].tile_rows * (jobs[j].dim | 1u));
-    return m;
-  }();
-  const uint32_t hist_smem_off = static_cast<uint32_t>(align_up(sizeof(int32_t) * max_rows_stride, 16));
-  if (ntiles) {
-    EMBC_TIMED(ctx, "k_quant_stats", stream,
-               k_quant_stats<<<ntiles, kBlock, hist_smem_off + (nhuff ? sizeof(uint32_t) * kWin : 0), stream>>>(
-                   d_jobs, d_tiles, d_st, d_hash, d_lit, d_hist, hist_smem_off));
-  }
-  if (!list_hjobs.empty()) {
-    BookScratch gs{};
-    if (big_books) {
-      gs.key = reinterpret_cast<uint64_t*>(d + o_gkey);
-      gs.wgt = reinterpret_cast<uint64_t*>(d + o_gwgt);
-      gs.parent = reinterpret_cast<int32_t*>(d + o_gpar);
-    }
-    const size_t sm = kSmemBook * (8 + 16 + 8);
-    EMBC_TIMED(ctx, "k_huff_book", stream,
-               k_huff_book<<<static_cast<uint32_t>(list_hjobs.size()), kBookThreads, sm, stream>>>(
-                   d_jobs, reinterpret_cast<const uint32_t*>(d + o_l3), d_st, d_hist, d_lut, d_books,
-                   book_stride, gs, p2cap, nhuff, reinterpret_cast<unsigned long long*>(d_flags + 2)));
-  }
-  LayoutArgs la{};
-  la.njobs = njobs;
-  la.layout = layout;
-  la.out = d_out;
-  la.cap = cap;
-  la.d_offsets = d_offsets;
-  la.d_lengths = d_lengths;
-  la.d_meta = d_meta;
-  la.d_total = d_total;
-  la.call_flags = d_flags;
-  la.err = ctx->d_err;
-  la.skip = d_stats ? 1 : 0;
-  {
-    const uint32_t nl = static_cast<uint32_t>(list_nonraw.size());
-    EMBC_TIMED(ctx, "k_sizes", stream,
-               k_sizes<<<nl + 1, kBlock, sizeof(uint64_t) * kHashStage, stream>>>(
-                   d_jobs, d_tiles, reinterpret_cast<const uint32_t*>(d + o_l1), nl, d_st, d_hash, d_lit, d_off,
-                   d_lut, d_tsum, d_toff, d_flags + 1, la));
-  }
-  if (d_stats) {  // match_stats: count literal vs reference rows of job 0
-    k_count_refs<<<(static_cast<uint32_t>(total_rows) + 255) / 256, 256, 0, stream>>>(
-        d_off, static_cast<uint32_t>(total_rows), d_stats);
-    ce = cudaGetLastError();
-    return ce == cudaSuccess ? EMBC_OK : cuda_fail(ctx, ce, "match_stats launch");
-  }
-  if (ntiles) {
-    EMBC_TIMED(ctx, "k_emit", stream,
-               k_emit<<<ntiles, kBlock, kStageBytes + 36 * 1024, stream>>>(
-                   d_jobs, d_tiles, d_st, d_off, d_lit, d_toff, d_tsum, d_lut, d_books, book_stride, d_out,
-                   d_edges, d_flags));
-  }
+  EMBC_TIMED(ctx, "k_stats", stream, k_stats<<<ntiles, kBlock, stats_smem, stream>>>(sa));
+
+  EmitArgs ea{};
+  ea.jobs = sa.jobs;
+  ea.tiles = sa.tiles;
+  ea.st = sa.st;
+  ea.row_info = sa.row_info;
+  ea.tile_status = sa.tile_status;
+  ea.job_status = sa.job_status;
+  ea.edge_slot = sa.edge_slot;
+  ea.lut = sa.book.lut;
+  ea.books = sa.book.books;
+  ea.book_stride = book_stride;
+  ea.flags = sa.book.flags;
+  ea.njobs = njobs;
+  ea.ntiles = ntiles;
+  ea.layout = layout;
+  ea.out = d_out;
+  ea.cap = cap;
+  ea.d_offsets = d_offsets;
+  ea.d_lengths = d_lengths;
+  ea.d_meta = d_meta;
+  ea.d_total = d_total;
+  ea.err = ctx->d_err;
+  ea.d_stats = d_stats;
+  ea.stage_off = emit_codes_bytes(vals_max, rows_max);
+  ea.aux_off = ea.stage_off + emit_stage_bytes(vals_max, rows_max);
+  const uint32_t emit_smem = ea.aux_off + kAuxBytes;
+  EMBC_TIMED(ctx, "k_emit", stream, k_emit<<<ntiles, kBlock, emit_smem, stream>>>(ea));
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "encode launch");
   return EMBC_OK;
 }
 
 cudaError_t encode_set_attributes() {
-  cudaError_t e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kStageBytes + 36 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmemMax);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_huff_book, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kSmemBook * (8 + 16 + 8));
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_quant_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           sizeof(int32_t) * 16384 * 2 + sizeof(uint32_t) * kWin);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_sizes, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              sizeof(uint64_t) * kHashStage);
+  return cudaFuncSetAttribute(k_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, kStatsSmemMax);
 }
 
 }  // namespace embc_host
