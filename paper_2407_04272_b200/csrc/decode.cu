@@ -1,9 +1,33 @@
-// decode.cu -- sm_100a decompression: chunk parse/validation, raw / vlz /
-// huffman decoding and dequantization straight into the consumer tensor.
+// decode.cu -- sm_100a decompression in two launches: chunk parse/validation,
+// raw / vlz / huffman decoding and dequantization straight into the consumer
+// tensor.
 //
 // Mirrors embc::parse_chunk + embc::decode_chunk (container.hpp:89-115,
 // :146-181), vlz_decode (vlz.hpp:129-158), huff_decode (huffman.hpp:254-291),
 // dequantize (quantizer.hpp:95-102).
+//
+//   D1 k_dec_main   CTAs take work from an atomic ticket, in this order:
+//     chunk CTAs    parse + validate every header (container.hpp:89-115); for
+//                   huffman chunks also validate the codebook exactly as
+//                   read_codebook + from_lengths + finalize and build the
+//                   decode tables, then raise the chunk's ready flag.
+//     vlz segments  2 KiB of tokens each: unit table, binary-lifting tables of
+//                   the token chain, the segment's entry->exit map, a
+//                   decoupled look-back over earlier segments for the true
+//                   entry, then every token of the segment: literal rows
+//                   decoded straight into the output, reference offsets
+//                   validated (vlz.hpp:141-145).  The chunk's last segment to
+//                   finish resolves reference chains to their root rows.
+//     huffman blocks 8192 bits each: per 64-bit subsequence and entry offset
+//                   the exit offset + symbol count (self-synchronising chains
+//                   merged by codeword-start bitmaps), group/block maps, a
+//                   decoupled look-back for the block's true entry, then the
+//                   symbols, staged in shared memory and stored coalesced.
+//     raw tiles     u32le -> values.
+//   D2 k_dec_fin    reference rows copied from their roots; chunks the
+//                   parallel path flagged are re-walked by the exact
+//                   sequential decoders (the reference's first error and
+//                   message); the lowest failing chunk is folded.
 //
 // Every malformed-input check of the reference is reproduced, in the
 // reference's order, so the first failure (and its message) is identical.
@@ -17,6 +41,21 @@
 #include "embc_internal.h"
 
 namespace embc_dev {
+
+#ifdef EMBC_DEBUG
+__device__ unsigned long long g_dts[16384][12];  // role, t1..t11 (t7 = end)
+__device__ unsigned long long g_dcalls;
+__device__ __forceinline__ unsigned long long dtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define DTS(slot, k) do { if (threadIdx.x == 0 && (slot) < 16384) g_dts[slot][k] = dtime(); } while (0)
+#define DROLE(slot, r) do { if (threadIdx.x == 0 && (slot) < 16384) { g_dts[slot][0] = (r); for (int q = 2; q < 12; ++q) g_dts[slot][q] = 0; } } while (0)
+#else
+#define DTS(slot, k) do {} while (0)
+#define DROLE(slot, r) do {} while (0)
+#endif
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
@@ -50,14 +89,12 @@ __device__ __forceinline__ void copy_value(const DChunk& C, uint64_t dst, uint64
 }
 
 // ---------------------------------------------------------------------------
-// D0: header parse (container.hpp:89-115) + metadata agreement
+// Header parse (container.hpp:89-115) + metadata agreement
 // (commsim.hpp:371-376) + ErrorBound (container.hpp:147, batch.hpp:33-37)
-// + raw size (container.hpp:152-155).  One thread per chunk.
+// + raw size (container.hpp:152-155).  Deterministic: every CTA of a chunk
+// computes the same state; the chunk CTA stores it.
 // ---------------------------------------------------------------------------
-__global__ void k_dec_parse(const DChunk* __restrict__ ch, DecState* __restrict__ st, uint32_t n) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  const DChunk C = ch[c];
+__device__ DecState parse_chunk(const DChunk& C) {
   DecState S;
   S.err = ~0ull;
   S.a = S.b = 0;
@@ -120,11 +157,11 @@ __global__ void k_dec_parse(const DChunk* __restrict__ ch, DecState* __restrict_
   if (S.err == ~0ull && !(isfinite(S.eb) && S.eb > 0.0)) dec_fail(S, 0, EMBC_R_BAD_EB, 0, 0);
   if (S.err == ~0ull && C.codec == EMBC_CODEC_RAW && S.pay_len != 4 * C.N)
     dec_fail(S, 0, EMBC_R_RAW_SIZE, S.pay_len, C.N);
-  st[c] = S;
+  return S;
 }
 
 // ---------------------------------------------------------------------------
-// D1: raw payload (container.hpp:151-160): u32le codes -> values
+// raw payload (container.hpp:151-160): u32le codes -> values
 // ---------------------------------------------------------------------------
 struct RawTile {
   uint32_t chunk;
@@ -132,12 +169,7 @@ struct RawTile {
   uint64_t e0, ne;
 };
 
-__device__ __forceinline__ void k_dec_raw_cta(uint32_t bid, const DChunk* __restrict__ ch,
-                                                    const DecState* __restrict__ st,
-                                                    const RawTile* __restrict__ tiles) {
-  const RawTile T = tiles[bid];
-  const DChunk& C = ch[T.chunk];
-  const DecState& S = st[T.chunk];
+__device__ __forceinline__ void raw_tile(const DChunk& C, const DecState& S, const RawTile& T) {
   if (S.err != ~0ull) return;
   const uint8_t* p = C.in + S.pay_off;
   const double w = 2.0 * S.eb;
@@ -216,334 +248,6 @@ __device__ __forceinline__ void k_dec_vlz_seq_cta(uint32_t bid, const DChunk* __
   if (pos != L) dec_fail(S, 0, EMBC_R_VLZ_TRAILING, L - pos, n);
 }
 // ===========================================================================
-// VLZ parallel decode (vlz.hpp:129-158 without its sequential dependency).
-//
-// A valid token stream is a sequence of "units": maximal byte runs ending in a
-// byte with bit 7 clear.  Tags are one-byte units (0x00 / 0x01); every varint
-// is one unit.  The token chain over units is next(u) = u + (tag ? 2 : dim+1),
-// so token boundaries are recovered in parallel without side-band offsets:
-//   V1 k_vlz_map    per 2 KiB byte segment: unit table, then pointer jumping
-//                   gives, for each possible entry offset e in [0, dim], the
-//                   exit offset into the next segment and the tokens crossed.
-//   V2 k_vlz_chain  per chunk: walk the segment maps -> true entry + first row
-//                   of every segment; checks the token count and the end.
-//   V3 k_vlz_rows   per segment: binary lifting enumerates the chain's tags ->
-//                   per row: tag unit, reference source row (offset validated).
-//   V4 k_vlz_roots  per chunk: pointer jumping resolves reference chains to the
-//                   root literal row.
-//   V5 k_vlz_out    per element: varint of the root literal -> zigzag ->
-//                   dequantize -> output tensor.
-// Any anomaly flags the chunk; k_dec_vlz_seq then re-walks it sequentially to
-// report the reference's exact error.
-// ===========================================================================
-constexpr uint32_t kSeg = 2048;        // bytes (>= units) per segment
-constexpr uint32_t kVlzMaxDim = 1023;  // larger dims use the sequential walker
-constexpr int kLift = 11;              // 2^11 > kSeg / 2 chain steps
-constexpr uint16_t kInv = 0xFFFF;
-
-struct SegPair {
-  uint32_t chunk, seg;
-};
-
-// unit kinds: 0 = tag 0x00, 1 = tag 0x01, 2 = not a valid tag
-__device__ __forceinline__ void k_vlz_map_cta(uint32_t bid, const DChunk* __restrict__ ch,
-                                                    const DecState* __restrict__ st,
-                                                    const SegPair* __restrict__ segs,
-                                                    uint32_t* __restrict__ ustart,
-                                                    uint8_t* __restrict__ ukind,
-                                                    uint32_t* __restrict__ seg_units,
-                                                    uint64_t* __restrict__ maps,
-                                                    uint32_t* __restrict__ vflag) {
-  __shared__ uint16_t J[kSeg], Cn[kSeg];
-  __shared__ uint32_t uend[kSeg];
-  __shared__ uint32_t s_tmp32[33];
-  __shared__ int s_bad;
-  const SegPair sp = segs[bid];
-  const DChunk& C = ch[sp.chunk];
-  if (st[sp.chunk].err != ~0ull || C.seq) return;
-  const DecState& S = st[sp.chunk];
-  const uint8_t* p = C.in + S.pay_off;
-  const uint64_t L = S.pay_len;
-  const uint32_t b0 = sp.seg * kSeg;
-  const uint32_t nb = static_cast<uint32_t>(umin64(kSeg, L > b0 ? L - b0 : 0));
-  const uint32_t D = C.dim;
-  if (threadIdx.x == 0) s_bad = 0;
-  // terminal bytes, 8 consecutive bytes per thread
-  const uint32_t i0 = threadIdx.x * 8;
-  uint32_t mask = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t i = i0 + k;
-    if (i < nb && !(p[b0 + i] & 0x80)) mask |= 1u << k;
-  }
-  uint32_t U;
-  uint32_t k0 = block_excl_scan<uint32_t>(__popc(mask), s_tmp32, &U);
-  {
-    uint32_t m = mask, k = k0;
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      uend[k++] = b0 + i0 + b;
-    }
-  }
-  __syncthreads();
-  const uint64_t ubase = static_cast<uint64_t>(C.seg0 + sp.seg) * kSeg;
-  for (uint32_t k = threadIdx.x; k < U; k += blockDim.x) {
-    uint32_t start;
-    if (k > 0) {
-      start = uend[k - 1] + 1;
-    } else {  // the first unit may begin in the previous segment
-      start = b0;
-      while (start > 0 && (p[start - 1] & 0x80) && b0 - start <= 10) --start;
-    }
-    const uint32_t len = uend[k] - start + 1;
-    if (len > 10) s_bad = 1;  // neither a tag nor a <= 10-byte varint (bytes.hpp:139-147)
-    const uint8_t v = p[start];
-    const uint8_t kind = (len == 1 && v <= 1) ? v : 2;
-    ustart[ubase + k] = start;
-    ukind[ubase + k] = kind;
-    J[k] = kind == 2 ? kInv : static_cast<uint16_t>(k + (kind == 0 ? D + 1 : 2));
-    Cn[k] = 1;
-  }
-  // a trailing partial unit can never be consumed by a valid parse
-  if (threadIdx.x == 0 && b0 + nb == L && nb > 0 && (p[L - 1] & 0x80)) s_bad = 1;
-  if (threadIdx.x == 0) seg_units[C.seg0 + sp.seg] = U;
-  __syncthreads();
-  // pointer jumping: J[k] -> first chain unit outside the segment (or kInv),
-  // Cn[k] -> tags visited from k
-  for (int r = 0; r < kLift; ++r) {
-    uint16_t nj[kSeg / kBlock], nc[kSeg / kBlock];
-#pragma unroll
-    for (uint32_t q = 0; q < kSeg / kBlock; ++q) {
-      const uint32_t k = threadIdx.x + q * kBlock;
-      nj[q] = 0;
-      nc[q] = 0;
-      if (k < U) {
-        const uint16_t j = J[k];
-        nj[q] = j;
-        nc[q] = Cn[k];
-        if (j < U) {
-          nj[q] = J[j];
-          nc[q] = Cn[k] + Cn[j];
-        }
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (uint32_t q = 0; q < kSeg / kBlock; ++q) {
-      const uint32_t k = threadIdx.x + q * kBlock;
-      if (k < U) {
-        J[k] = nj[q];
-        Cn[k] = nc[q];
-      }
-    }
-    __syncthreads();
-  }
-  uint64_t* m = maps + C.map_base + static_cast<uint64_t>(sp.seg) * (D + 1);
-  for (uint32_t e = threadIdx.x; e <= D; e += blockDim.x) {
-    uint32_t exit_off, cnt;
-    if (e < U) {
-      const uint16_t j = J[e];
-      exit_off = j == kInv ? 0xFFFFFFFFu : j - U;
-      cnt = Cn[e];
-    } else {
-      exit_off = e - U;
-      cnt = 0;
-    }
-    m[e] = (static_cast<uint64_t>(cnt) << 32) | exit_off;
-  }
-  if (threadIdx.x == 0 && s_bad) vflag[sp.chunk] = 1;
-}
-
-__device__ __forceinline__ void vlz_chain_one(const DChunk* __restrict__ ch, const DecState* __restrict__ st,
-                                              uint32_t c, const uint64_t* __restrict__ maps,
-                                              uint32_t* __restrict__ seg_entry, uint32_t* __restrict__ seg_row0,
-                                              uint32_t* __restrict__ vflag) {
-  const DChunk& C = ch[c];
-  if (st[c].err != ~0ull || C.seq || vflag[c]) return;
-  const uint32_t D = C.dim;
-  uint32_t e = 0, row = 0;
-  bool bad = false;
-  for (uint32_t s = 0; s < C.nseg; ++s) {
-    seg_entry[C.seg0 + s] = e;
-    seg_row0[C.seg0 + s] = row;
-    const uint64_t m = maps[C.map_base + static_cast<uint64_t>(s) * (D + 1) + e];
-    const uint32_t exit_off = static_cast<uint32_t>(m);
-    if (exit_off == 0xFFFFFFFFu) {
-      bad = true;
-      break;
-    }
-    row += static_cast<uint32_t>(m >> 32);
-    e = exit_off;
-    if (row > C.count) {
-      bad = true;
-      break;
-    }
-  }
-  if (bad || row != C.count || e != 0) vflag[c] = 1;
-}
-
-__device__ __forceinline__ uint32_t unit_advance(const uint32_t* __restrict__ seg_units, uint32_t seg0,
-                                                 uint32_t nseg, uint32_t addr, uint32_t k, bool* ok) {
-  uint32_t s = addr / kSeg, l = addr % kSeg;
-  while (s < nseg) {
-    const uint32_t U = seg_units[seg0 + s];
-    if (l + k < U) return s * kSeg + l + k;
-    k -= U - l;
-    l = 0;
-    ++s;
-  }
-  *ok = false;
-  return 0;
-}
-
-// varint at unit start (bytes.hpp:139-147 semantics: bits past 64 dropped)
-__device__ __forceinline__ uint64_t unit_varint(const uint8_t* p, uint32_t start) {
-  uint64_t v = 0;
-#pragma unroll 1
-  for (int shift = 0; shift < 70; shift += 7) {
-    const uint8_t b = p[start++];
-    if (shift < 64) v |= static_cast<uint64_t>(b & 0x7F) << shift;
-    if (!(b & 0x80)) break;
-  }
-  return v;
-}
-
-__device__ __forceinline__ void k_vlz_rows_cta(uint32_t bid, uint8_t* dsm, const DChunk* __restrict__ ch,
-                                                     const DecState* __restrict__ st,
-                                                     const SegPair* __restrict__ segs,
-                                                     const uint32_t* __restrict__ ustart,
-                                                     const uint8_t* __restrict__ ukind,
-                                                     const uint32_t* __restrict__ seg_units,
-                                                     const uint32_t* __restrict__ seg_entry,
-                                                     const uint32_t* __restrict__ seg_row0,
-                                                     uint32_t* __restrict__ row_tag,
-                                                     uint32_t* __restrict__ row_src,
-                                                     uint32_t* __restrict__ vflag) {
-  uint16_t (*Jt)[kSeg] = reinterpret_cast<uint16_t (*)[kSeg]>(dsm);
-  const SegPair sp = segs[bid];
-  const DChunk& C = ch[sp.chunk];
-  if (st[sp.chunk].err != ~0ull || C.seq || vflag[sp.chunk]) return;
-  const DecState& S = st[sp.chunk];
-  const uint8_t* p = C.in + S.pay_off;
-  const uint32_t D = C.dim;
-  const uint32_t g = C.seg0 + sp.seg;
-  const uint32_t U = seg_units[g];
-  const uint32_t e = seg_entry[g];
-  const uint32_t row0 = seg_row0[g];
-  const uint32_t rowN = sp.seg + 1 < C.nseg ? seg_row0[g + 1] : C.count;
-  const uint32_t T = rowN - row0;
-  if (T == 0) return;
-  const uint64_t ubase = static_cast<uint64_t>(g) * kSeg;
-  for (uint32_t k = threadIdx.x; k < U; k += blockDim.x) {
-    const uint8_t kind = ukind[ubase + k];
-    Jt[0][k] = kind == 2 ? kInv : static_cast<uint16_t>(umin32(k + (kind == 0 ? D + 1 : 2), kInv - 1));
-  }
-  __syncthreads();
-  for (int r = 1; r < kLift; ++r) {
-    for (uint32_t k = threadIdx.x; k < U; k += blockDim.x) {
-      const uint16_t j = Jt[r - 1][k];
-      Jt[r][k] = j < U ? Jt[r - 1][j] : j;
-    }
-    __syncthreads();
-  }
-  const uint64_t rb = C.row_base;
-  bool bad = false;
-  for (uint32_t t = threadIdx.x; t < T; t += blockDim.x) {
-    uint32_t pos = e;
-    for (int r = 0; r < kLift && pos < U; ++r)
-      if ((t >> r) & 1) pos = Jt[r][pos];
-    if (pos >= U) {
-      bad = true;
-      continue;
-    }
-    const uint32_t row = row0 + t;
-    const uint32_t addr = sp.seg * kSeg + pos;
-    row_tag[rb + row] = addr;
-    if (ukind[ubase + pos] == 1) {  // reference token: validate (vlz.hpp:141-145)
-      bool ok = true;
-      const uint32_t ga = unit_advance(seg_units, C.seg0, C.nseg, addr, 1, &ok);
-      uint64_t off = 0;
-      if (ok) off = unit_varint(p, ustart[static_cast<uint64_t>(C.seg0) * kSeg + ga]);
-      if (!ok || off < 1 || off > row || off > kMaxWindow) {
-        bad = true;
-        row_src[rb + row] = row;
-      } else {
-        row_src[rb + row] = row - static_cast<uint32_t>(off);
-      }
-    } else {
-      row_src[rb + row] = row;
-    }
-  }
-  if (bad) vflag[sp.chunk] = 1;
-}
-
-constexpr uint32_t kRootSmem = 11264;  // rows resolved in shared memory (45 KiB of the stage-2 buffer)
-
-__device__ __forceinline__ void k_vlz_roots_cta(uint32_t bid, uint8_t* dsm, const DChunk* __restrict__ ch,
-                                                    const DecState* __restrict__ st,
-                                                    const uint32_t* __restrict__ list,
-                                                    const uint32_t* __restrict__ vflag,
-                                                    uint32_t* __restrict__ row_src,
-                                                    uint32_t* __restrict__ row_tag,
-                                                    uint32_t* __restrict__ row_root) {
-  uint32_t* sh = reinterpret_cast<uint32_t*>(dsm);
-  const uint32_t c = bid;
-  const DChunk& C = ch[c];
-  if (st[c].err != ~0ull || C.seq || vflag[c]) return;
-  const uint32_t n = C.count;
-  uint32_t* src = row_src + C.row_base;
-  uint32_t* a = n <= kRootSmem ? sh : src;
-  if (n <= kRootSmem)
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) sh[i] = src[i];
-  __syncthreads();
-  for (;;) {  // pointer jumping to the root literal (every source is an earlier row)
-    bool changed = false;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint32_t s = a[i];
-      const uint32_t ss = a[s];
-      if (ss != s) {
-        a[i] = ss;
-        changed = true;
-      }
-    }
-    if (!__syncthreads_or(changed)) break;
-  }
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
-    row_root[C.row_base + i] = row_tag[C.row_base + a[i]];
-}
-
-struct ElemTile {
-  uint32_t chunk, pad;
-  uint64_t e0, ne;
-};
-
-__device__ __forceinline__ void k_vlz_out_cta(uint32_t bid, const DChunk* __restrict__ ch,
-                                                    const DecState* __restrict__ st,
-                                                    const ElemTile* __restrict__ tiles,
-                                                    const uint32_t* __restrict__ vflag,
-                                                    const uint32_t* __restrict__ ustart,
-                                                    const uint32_t* __restrict__ seg_units,
-                                                    const uint32_t* __restrict__ row_root) {
-  const ElemTile T = tiles[bid];
-  const DChunk& C = ch[T.chunk];
-  if (st[T.chunk].err != ~0ull || C.seq || vflag[T.chunk]) return;
-  const DecState& S = st[T.chunk];
-  const uint8_t* p = C.in + S.pay_off;
-  const double w = 2.0 * S.eb;
-  const uint32_t D = C.dim;
-  const uint32_t* us = ustart + static_cast<uint64_t>(C.seg0) * kSeg;
-  for (uint64_t e = T.e0 + threadIdx.x; e < T.e0 + T.ne; e += blockDim.x) {
-    const uint32_t row = fdiv(static_cast<uint32_t>(e), C.fd);
-    const uint32_t col = static_cast<uint32_t>(e) - row * D;
-    bool ok = true;
-    const uint32_t ga = unit_advance(seg_units, C.seg0, C.nseg, row_root[C.row_base + row], 1 + col, &ok);
-    const uint64_t v = unit_varint(p, us[ga]);
-    store_value(C, e, unzigzag(static_cast<uint32_t>(v)), w);
-  }
-}
-
-// ===========================================================================
 // Huffman: codebook tables (read_codebook + from_lengths + finalize,
 // huffman.hpp:132-148, :165-186, :213-222), then a self-synchronising
 // parallel decode of the MSB-first bitstream (huffman.hpp:254-291):
@@ -615,17 +319,13 @@ __device__ __forceinline__ uint64_t value_bits(int32_t code, double w, int kind)
   return static_cast<uint32_t>(code);
 }
 
-__device__ __forceinline__ void k_huff_tables_cta(uint32_t bid, const DChunk* __restrict__ ch,
-                                                        DecState* __restrict__ st,
-                                                        const uint32_t* __restrict__ list,
-                                                        uint64_t* __restrict__ keys,
-                                                        uint8_t* __restrict__ tabs,
-                                                        uint32_t* __restrict__ hflag) {
+__device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState* __restrict__ st,
+                            uint64_t* __restrict__ keys, uint8_t* __restrict__ tabs,
+                            uint32_t* __restrict__ hflag, uint64_t* skey, uint32_t skey_cap) {
   __shared__ unsigned long long s_tmp64[33];
   __shared__ unsigned long long s_bad;
   __shared__ int s_stop;
   __shared__ HTab tb;
-  const uint32_t c = list[bid];
   const DChunk C = ch[c];
   DecState& S = st[c];
   if (S.err != ~0ull) return;
@@ -688,6 +388,7 @@ __device__ __forceinline__ void k_huff_tables_cta(uint32_t bid, const DChunk* __
   // canonical order (length, symbol): key = len << 32 | (symbol ^ 0x80000000)
   uint32_t p2 = 1;
   while (p2 < nent) p2 <<= 1;
+  if (p2 <= skey_cap) key = skey;  // small codebooks sort in shared memory
   for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) {
     if (i < nent) {
       const uint32_t s = static_cast<uint32_t>(ld_be(p + 12 + 5ull * i, 4));
@@ -697,7 +398,9 @@ __device__ __forceinline__ void k_huff_tables_cta(uint32_t bid, const DChunk* __
     }
   }
   __syncthreads();
+  DTS(blockIdx.x, 2);
   bitonic_sort_u64(key, p2);
+  DTS(blockIdx.x, 3);
   for (uint32_t i = threadIdx.x; i < nent; i += blockDim.x)
     hv.syms[i] = static_cast<int32_t>(static_cast<uint32_t>(key[i]) ^ 0x80000000u);
   if (threadIdx.x < 33) {
@@ -732,6 +435,7 @@ __device__ __forceinline__ void k_huff_tables_cta(uint32_t bid, const DChunk* __
     carry += tot;
   }
   __syncthreads();
+  DTS(blockIdx.x, 4);
   // left-aligned code starts, ascending in canonical order -> prefix LUT
   for (uint32_t i = threadIdx.x; i < nent; i += blockDim.x) {
     const uint32_t len = static_cast<uint32_t>(key[i] >> 32);
@@ -764,11 +468,13 @@ __device__ __forceinline__ void k_huff_tables_cta(uint32_t bid, const DChunk* __
     hv.lut[s] = ent;
   }
   __syncthreads();  // the code starts in key[] are read above; reused below
+  DTS(blockIdx.x, 5);
   // duplicate symbols (huffman.hpp:183-185) across all lengths
   for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x)
     key[i] = i < nent ? (static_cast<uint64_t>(static_cast<uint32_t>(hv.syms[i]) ^ 0x80000000u) << 32) | i : ~0ull;
   __syncthreads();
   bitonic_sort_u64(key, p2);
+  DTS(blockIdx.x, 6);
   bool dup = false;
   for (uint32_t i = 1 + threadIdx.x; i < nent; i += blockDim.x) dup |= (key[i] >> 32) == (key[i - 1] >> 32);
   dup = __syncthreads_or(dup);
@@ -825,48 +531,6 @@ __device__ __forceinline__ int decode_one(const uint32_t* lut, const HTab& t, ui
   return -1;
 }
 
-enum : uint32_t { HF_INVALID = 1, HF_ENDED = 2, HF_DEAD = 4 };
-
-// Decode from `pos` until crossing `end` (or the stream end / an invalid code).
-__device__ __forceinline__ void decode_run(const uint8_t* s, uint64_t nbytes, uint64_t nbits,
-                                           const uint32_t* lut, const HTab& t, uint64_t pos, uint64_t end,
-                                           uint64_t* x, uint32_t* cnt, uint32_t* flags) {
-  uint32_t c = 0, f = 0;
-  while (pos < end) {
-    if (pos >= nbits) {
-      f |= HF_ENDED;
-      break;
-    }
-    uint32_t len = 0;
-    const int ent = decode_one(lut, t, peek32(s, nbytes, pos), &len);
-    if (ent < 0) {
-      f |= HF_INVALID;
-      break;
-    }
-    if (pos + len > nbits) {
-      f |= HF_ENDED;
-      break;
-    }
-    pos += len;
-    ++c;
-  }
-  *x = pos;
-  *cnt = c;
-  *flags = f;
-}
-
-struct SubTile {
-  uint32_t chunk;
-  uint32_t first;  // first subsequence of this CTA (multiple of kSubPerBlock)
-};
-
-constexpr uint32_t kSubPerBlock = 256;                   // subsequences per CTA / block map
-constexpr uint32_t kGroup = 32;                          // subsequences per group map
-constexpr uint32_t kBlockBits = kSubBits * kSubPerBlock;  // bits staged per CTA
-constexpr uint32_t kStageWords = kBlockBits / 32 + 4;    // + look-ahead past the block
-constexpr int kClasses = 4;                              // distinct chains tracked per subsequence
-constexpr uint32_t kMapsSmem = 0;
-
 // Packed map entry: entry/exit bit offset (5 bits) | termination kind (2 bits)
 // | symbol count (25 bits).  Termination: 0 live, 1 invalid prefix, 2 stream end.
 __device__ __forceinline__ uint32_t pk(uint32_t off, uint32_t term, uint32_t cnt) {
@@ -877,9 +541,9 @@ __device__ __forceinline__ uint32_t pk_term(uint32_t v) { return (v >> 5) & 3; }
 __device__ __forceinline__ uint32_t pk_cnt(uint32_t v) { return v >> 7; }
 
 // Stage the CTA's slice of the bitstream as big-endian 32-bit words.
-__device__ __forceinline__ void stage_bits(uint32_t* W, const uint8_t* s, uint64_t nbytes, uint64_t bit0) {
+__device__ __forceinline__ void stage_bits(uint32_t* W, uint32_t nwords, const uint8_t* s, uint64_t nbytes, uint64_t bit0) {
   const uint64_t b0 = bit0 >> 3;  // bit0 is a multiple of 32
-  for (uint32_t w = threadIdx.x; w < kStageWords; w += blockDim.x) {
+  for (uint32_t w = threadIdx.x; w < nwords; w += blockDim.x) {
     const uint64_t b = b0 + 4ull * w;
     uint32_t v = 0;
     if (b + 4 <= nbytes) {
@@ -901,231 +565,6 @@ __device__ __forceinline__ uint32_t speek(const uint32_t* W, uint32_t p) {
 __device__ __forceinline__ uint32_t popc_below(uint64_t bm, uint32_t p) {
   return static_cast<uint32_t>(__popcll(bm & ((1ull << p) - 1ull)));
 }
-
-// H1: for subsequence i (bits [iK, iK+K)) and each possible entry offset
-// r < max_len: F_i(r) = (exit offset past (i+1)K, symbols, termination).
-// Chains are decoded one after another; the codeword starts of up to
-// kClasses distinct chains are kept as bitmaps in registers, and a chain that
-// lands on a start of a known chain has merged with it: its result follows by
-// a popcount.  (Self-synchronising codes merge within a few codewords;
-// fixed-length codes need one decode per residue class.)  Groups of 32
-// subsequences are then composed per entry offset (lane r), and the group maps
-// per block.
-__device__ __forceinline__ void k_huff_maps_cta(uint32_t bid, uint8_t* dsm, const DChunk* __restrict__ ch,
-                                                             const DecState* __restrict__ st,
-                                                             const SubTile* __restrict__ tiles,
-                                                             uint8_t* __restrict__ tabs,
-                                                             const uint32_t* __restrict__ hflag,
-                                                             uint32_t* __restrict__ qmaps,
-                                                             uint32_t* __restrict__ gmaps,
-                                                             uint32_t* __restrict__ bmaps) {
-  __shared__ HTab t;
-  uint32_t* lut = reinterpret_cast<uint32_t*>(dsm);
-  uint32_t* W = lut + (1 << kL0);
-  uint32_t (*Fm)[33] = reinterpret_cast<uint32_t (*)[33]>(W + kStageWords);
-  uint32_t (*G)[32] = reinterpret_cast<uint32_t (*)[32]>(&Fm[kSubPerBlock][0]);
-  const SubTile T = tiles[bid];
-  const DChunk& C = ch[T.chunk];
-  if (st[T.chunk].err != ~0ull || hflag[T.chunk]) return;
-  HView hv = hview(tabs, C);
-  for (uint32_t i = threadIdx.x; i < (1u << kL0); i += blockDim.x) lut[i] = hv.lut[i];
-  if (threadIdx.x == 0) t = *hv.tab;
-  __syncthreads();
-  const uint64_t bit0 = static_cast<uint64_t>(T.first) * kSubBits;
-  stage_bits(W, C.in + st[T.chunk].pay_off + t.bit_off, t.nbits / 8, bit0);
-  __syncthreads();
-  const uint32_t R = t.max_len;
-  const uint32_t sub = T.first + threadIdx.x;
-  const uint64_t nbits = t.nbits;
-  {
-    static_assert(kSubBits == 64, "chain bitmaps are one 64-bit word");
-    uint64_t cbm[kClasses];
-    uint32_t cres[kClasses];
-    int ncls = 0;
-    const uint32_t base = threadIdx.x * kSubBits;  // relative bit of this subsequence
-    for (uint32_t r = 0; r < 32; ++r) {
-      uint32_t out = pk(0, 2, 0);
-      if (r < R && sub < C.nsub) {
-        int merged = -1;
-        uint32_t mpos = 0, cnt = 0;
-        uint64_t mine = 0;
-        uint32_t p = r;
-        for (;;) {
-          if (p >= kSubBits) {
-            out = pk(p - kSubBits, 0, cnt);
-            break;
-          }
-#pragma unroll
-          for (int c = 0; c < kClasses; ++c)
-            if (merged < 0 && c < ncls && ((cbm[c] >> p) & 1)) merged = c;
-          if (merged >= 0) {
-            mpos = p;
-            break;
-          }
-          mine |= 1ull << p;
-          const uint64_t pos = bit0 + base + p;
-          if (pos >= nbits) {
-            out = pk(0, 2, cnt);
-            break;
-          }
-          uint32_t len = 0;
-          if (decode_one(lut, t, speek(W, base + p), &len) < 0) {
-            out = pk(0, 1, cnt);
-            break;
-          }
-          if (pos + len > nbits) {
-            out = pk(0, 2, cnt);
-            break;
-          }
-          p += len;
-          ++cnt;
-        }
-        if (merged >= 0) {
-#pragma unroll
-          for (int c = 0; c < kClasses; ++c) {
-            if (c == merged) {
-              const uint32_t o = cres[c];
-              out = pk(pk_off(o), pk_term(o), cnt + pk_cnt(o) - popc_below(cbm[c], mpos));
-            }
-          }
-        } else if (ncls < kClasses) {
-#pragma unroll
-          for (int c = 0; c < kClasses; ++c) {
-            if (c == ncls) {
-              cbm[c] = mine;
-              cres[c] = out;
-            }
-          }
-          ++ncls;
-        }
-      }
-      Fm[threadIdx.x][r] = out;
-    }
-  }
-  __syncthreads();
-  // group prefix maps: warp g, lane r follows entry offset r through its 32 subsequences
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t nloc = min(kSubPerBlock, C.nsub - T.first);
-  {
-    uint32_t e = lane, term = 0, cnt = 0;
-    for (uint32_t j = 0; j < kGroup; ++j) {
-      const uint32_t i = warp * kGroup + j;
-      if (i < nloc) qmaps[(C.sub0 + T.first + i) * 32 + lane] = pk(e, term, cnt);
-      if (!term && i < nloc) {
-        const uint32_t f = Fm[i][e];
-        term = pk_term(f);
-        cnt += pk_cnt(f);
-        e = pk_off(f);
-      }
-    }
-    G[warp][lane] = pk(e, term, cnt);
-  }
-  __syncthreads();
-  if (warp == 0) {  // block prefix over groups
-    uint32_t e = lane, term = 0, cnt = 0;
-    const uint32_t gb = static_cast<uint32_t>((C.sub0 + T.first) / kGroup);
-    for (uint32_t g = 0; g < kSubPerBlock / kGroup; ++g) {
-      gmaps[(gb + g) * 32 + lane] = pk(e, term, cnt);
-      if (!term) {
-        const uint32_t f = G[g][e];
-        term = pk_term(f);
-        cnt += pk_cnt(f);
-        e = pk_off(f);
-      }
-    }
-    bmaps[((C.sub0 + T.first) / kSubPerBlock) * 32 + lane] = pk(e, term, cnt);
-  }
-}
-
-// H2: per chunk, walk the block maps from entry offset 0: true entry offset and
-// output base of every block; then check that N symbols exist before the chain
-// terminates (huffman.hpp:274-288: exhaustion / invalid prefix).
-__device__ __forceinline__ void k_huff_walk_cta(uint32_t bid, uint8_t* dsm, uint32_t dsm_words, const DChunk* __restrict__ ch, const DecState* __restrict__ st,
-                            const uint32_t* __restrict__ list, uint8_t* __restrict__ tabs,
-                            uint32_t* __restrict__ hflag, const uint32_t* __restrict__ bmaps,
-                            uint32_t* __restrict__ bentry, uint64_t* __restrict__ bbase) {
-  uint32_t* sm = reinterpret_cast<uint32_t*>(dsm);
-  const uint32_t c = bid;
-  const DChunk& C = ch[c];
-  if (st[c].err != ~0ull || hflag[c]) return;
-  const uint32_t nb = (C.nsub + kSubPerBlock - 1) / kSubPerBlock;
-  const uint32_t b0 = static_cast<uint32_t>(C.sub0 / kSubPerBlock);
-  const bool in_smem = nb * 32 <= dsm_words;
-  if (in_smem)
-    for (uint32_t k = threadIdx.x; k < nb * 32; k += blockDim.x) sm[k] = bmaps[b0 * 32 + k];
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  HView hv = hview(tabs, C);
-  const uint64_t N = hv.tab->nsym;
-  uint32_t e = 0, term = 0;
-  uint64_t acc = 0;
-  for (uint32_t b = 0; b < nb; ++b) {
-    bentry[b0 + b] = term ? 0xFFFFFFFFu : e;
-    bbase[b0 + b] = acc;
-    if (term) continue;
-    const uint32_t m = in_smem ? sm[b * 32 + e] : bmaps[(b0 + b) * 32 + e];
-    acc += pk_cnt(m);
-    term = pk_term(m);
-    e = pk_off(m);
-  }
-  // every path terminates at the stream end (term 2) unless an invalid prefix
-  // comes first; either way fewer than N decodable symbols is an error
-  if (acc < N) hflag[c] = 1;
-}
-
-// H3: decode every subsequence from its true start and write the values.
-__device__ __forceinline__ void k_huff_out_cta(uint32_t bid, const DChunk* __restrict__ ch,
-                                                           const DecState* __restrict__ st,
-                                                           const SubTile* __restrict__ tiles,
-                                                           uint8_t* __restrict__ tabs,
-                                                           const uint32_t* __restrict__ hflag,
-                                                           const uint32_t* __restrict__ qmaps,
-                                                           const uint32_t* __restrict__ gmaps,
-                                                           const uint32_t* __restrict__ bentry,
-                                                           const uint64_t* __restrict__ bbase) {
-  __shared__ uint32_t lut[1 << kL0];
-  __shared__ HTab t;
-  __shared__ uint32_t W[kStageWords];
-  const SubTile T = tiles[bid];
-  const DChunk& C = ch[T.chunk];
-  if (st[T.chunk].err != ~0ull || hflag[T.chunk]) return;
-  const uint32_t bidx = static_cast<uint32_t>((C.sub0 + T.first) / kSubPerBlock);
-  const uint32_t be = bentry[bidx];
-  if (be == 0xFFFFFFFFu) return;
-  HView hv = hview(tabs, C);
-  for (uint32_t i = threadIdx.x; i < (1u << kL0); i += blockDim.x) lut[i] = hv.lut[i];
-  if (threadIdx.x == 0) t = *hv.tab;
-  __syncthreads();
-  const uint64_t bit0 = static_cast<uint64_t>(T.first) * kSubBits;
-  stage_bits(W, C.in + st[T.chunk].pay_off + t.bit_off, t.nbits / 8, bit0);
-  __syncthreads();
-  const uint32_t sub = T.first + threadIdx.x;
-  if (sub >= C.nsub) return;
-  const uint32_t gidx = static_cast<uint32_t>((C.sub0 + sub) / kGroup);
-  const uint32_t gm = gmaps[gidx * 32 + be];
-  if (pk_term(gm)) return;
-  const uint32_t qm = qmaps[(C.sub0 + sub) * 32 + pk_off(gm)];
-  if (pk_term(qm)) return;
-  const uint64_t base = bbase[bidx] + pk_cnt(gm) + pk_cnt(qm);
-  if (base >= t.nsym) return;
-  const uint32_t rel0 = threadIdx.x * kSubBits;
-  uint32_t p = rel0 + pk_off(qm);
-  const uint32_t end = rel0 + kSubBits;
-  const uint64_t stop = t.nsym - base;
-  const uint64_t nbits = t.nbits;
-  const int kind = C.out_kind;
-  for (uint64_t k = 0; k < stop && p < end && bit0 + p < nbits; ++k) {
-    uint32_t len = 0;
-    const int ent = decode_one(lut, t, speek(W, p), &len);
-    if (ent < 0 || bit0 + p + len > nbits) break;
-    p += len;
-    const uint64_t v = hv.vals[ent];
-    const uint64_t i = base + k;
-    if (kind == EMBC_OUT_F64) static_cast<uint64_t*>(C.out)[i] = v;
-    else static_cast<uint32_t*>(C.out)[i] = static_cast<uint32_t>(v);
-  }
-}
-
 // Exact sequential walk (huffman.hpp:274-290) for flagged chunks: reproduces
 // the reference's first error (exhaustion / invalid prefix / count).
 __device__ __forceinline__ void k_dec_huff_seq_cta(uint32_t bid, const DChunk* __restrict__ ch, DecState* __restrict__ st,
@@ -1199,125 +638,914 @@ __device__ __forceinline__ void dec_fold(const DecState* __restrict__ st, uint32
 
 
 // ===========================================================================
-// Stage kernels: every decode call is k_dec_parse + four launches.  CTAs take
-// a role by blockIdx range; per-chunk follow-up work (the vlz segment-map
-// walk, the reference-chain resolution, the huffman block-map walk, the
-// failure fold) runs in the last CTA of its group to finish (an atomic ticket
-// after a __threadfence), so it needs no launch of its own.
+// look-back status words (flag in bits 63:62; 1 = aggregate map published,
+// 2 = inclusive state published)
 // ===========================================================================
-struct DecPlan {
-  uint32_t n_seg, n_htab, n_raw, n_sub, n_vt, nchunks;
+constexpr unsigned long long kStAgg = 1ull << 62, kStInc = 2ull << 62;
+
+__device__ __forceinline__ unsigned long long ld_vol(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ void st_vol(unsigned long long* p, unsigned long long v) {
+  __threadfence();
+  *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
+
+// Warp 0: index of the nearest predecessor in [first, i) with an inclusive
+// state (every element between it and i has at least published its map).
+// Returns that index and its status word.
+__device__ __forceinline__ uint32_t find_inclusive(const unsigned long long* status, uint32_t first, uint32_t i,
+                                                   unsigned long long* word) {
+  const uint32_t lane = threadIdx.x & 31;
+  int64_t p = static_cast<int64_t>(i) - 1;
+  uint32_t delay = 32;
+  for (;;) {
+    const int64_t idx = p - lane;
+    unsigned long long s = kStInc;
+    if (idx >= static_cast<int64_t>(first)) s = ld_vol(status + idx);
+    const uint32_t inc = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+    const uint32_t zero = __ballot_sync(0xffffffffu, (s >> 62) == 0);
+    const int fi = inc ? __ffs(inc) - 1 : 32;
+    const uint32_t need = fi == 32 ? 0xffffffffu : ((2u << fi) - 1);
+    if (zero & need) {  // a predecessor has not published yet: back off, re-read
+      __nanosleep(delay);
+      delay = min(delay * 2, 256u);
+      continue;
+    }
+    if (fi < 32) {
+      *word = __shfl_sync(0xffffffffu, s, fi);
+      return static_cast<uint32_t>(p - fi);
+    }
+    p -= 32;
+  }
+}
+
+// ===========================================================================
+// VLZ (vlz.hpp:129-158) without its sequential dependency.
+//
+// A valid token stream is a sequence of "units": maximal byte runs ending in a
+// byte with bit 7 clear.  Tags are one-byte units (0x00 / 0x01) and every
+// varint is one unit, so the token chain over units is
+// next(u) = u + (tag 0x00 ? dim + 1 : 2).  Each 2 KiB segment builds binary
+// lifting tables of that chain, derives its entry -> (exit, tokens) map for
+// the dim + 1 possible entry offsets, and learns its true entry from the
+// segments before it (decoupled look-back).  Any anomaly flags the chunk;
+// the exact sequential walker then reproduces the reference's error.
+// ===========================================================================
+constexpr uint32_t kSeg = 1024;         // payload bytes per segment
+constexpr uint32_t kVlzMaxDim = 1023;   // larger dims use the sequential walker
+constexpr int kLift = 10;               // 2^10 > kSeg / 2 tokens per segment
+constexpr uint16_t kInv = 0xFFFF;
+constexpr uint32_t kSegBack = 16;       // bytes staged before the segment (first unit's start)
+// VLZ segment smem for chunks of dim <= dmax: staged bytes (the segment plus
+// one literal token past it) | unit ends | lifting tables | literal queue
+__host__ __device__ constexpr uint32_t vlz_unit_cap(uint32_t dmax) { return kSeg + dmax + 2; }
+__host__ __device__ constexpr uint32_t vlz_bytes_cap(uint32_t dmax) {
+  return (kSegBack + kSeg + 10 * (dmax + 1) + 32 + 15) & ~15u;
+}
+__host__ __device__ constexpr uint32_t vlz_smem(uint32_t dmax) {
+  return vlz_bytes_cap(dmax) + ((vlz_unit_cap(dmax) * 2 + 15) & ~15u) + kLift * kSeg * 2 + 8 * (kSeg / 2);
+}
+constexpr uint32_t kVlzSmem = vlz_smem(kVlzMaxDim);
+constexpr uint32_t kRootBlock = 1024;   // rows resolved per pass of the root tail
+
+struct SegPair {
+  uint32_t chunk, seg;
 };
+
+// inclusive vlz state: flag | dead (61) | entry unit offset (42:32) | rows (31:0)
+__device__ __forceinline__ unsigned long long vlz_state(bool dead, uint32_t e, uint32_t rows) {
+  return (dead ? (1ull << 61) : 0) | (static_cast<unsigned long long>(e & 0x7FF) << 32) | rows;
+}
 
 struct DecArgs {
   const DChunk* ch;
   DecState* st;
   const SegPair* segs;
-  const uint32_t* vlist;
-  const uint32_t* hlist;
+  const uint32_t* hblk_chunk;  // huffman block -> chunk
   const RawTile* raw;
-  const ElemTile* vtiles;
-  const SubTile* subt;
+  const uint32_t* ctile;       // D2 copy tiles: (chunk << 0) in [0], row0 in [1], rows in [2] (triplets)
   uint32_t* vflag;
   uint32_t* hflag;
-  uint32_t* cnt;  // [3][nchunks] tickets + fold ticket
-  uint32_t* ustart;
-  uint8_t* ukind;
-  uint32_t* segu;
-  uint32_t* sege;
-  uint32_t* segr;
-  uint64_t* maps;
-  uint32_t* rtag;
-  uint32_t* rsrc;
-  uint32_t* rroot;
+  uint32_t* ready;
+  uint32_t* cnt;               // per-chunk tail tickets
+  uint32_t* tickets;           // [0] D1 ticket, [1] D2 fold ticket
+  unsigned long long* seg_status;
+  unsigned long long* blk_status;
+  uint32_t* maps;              // vlz: per segment (dim + 1) entry maps
+  uint32_t* bmaps;             // huffman: per block 32 entry maps
+  uint32_t* row_src;
   uint64_t* keys;
   uint8_t* tabs;
-  uint32_t* qmaps;
-  uint32_t* gmaps;
-  uint32_t* bmaps;
-  uint32_t* bentry;
-  uint64_t* bbase;
   DevError* err;
-  uint32_t* diag;  // [0]: chunks that needed the sequential walker in this call
+  uint32_t* diag;
+  uint32_t nchunks, nseg, nhblk, nraw, nctile;
+  uint32_t vlz_dmax;    // largest vlz dim of the call (sizes the segment smem carve)
+  uint32_t smem_bytes;  // dynamic shared memory of k_dec_main
 };
 
-constexpr uint32_t kStage2Smem = 45312;  // max(vlz lifting tables, huffman map scratch)
+__device__ __forceinline__ uint64_t stage_varint(const uint8_t* B, uint32_t start, uint32_t end) {
+  uint64_t v = 0;
+  int shift = 0;
+  for (uint32_t k = start; k <= end; ++k, shift += 7)
+    if (shift < 64) v |= static_cast<uint64_t>(B[k] & 0x7F) << shift;
+  return v;
+}
 
-__device__ __forceinline__ bool last_of(uint32_t* ticket, uint32_t total) {
+__device__ void vlz_roots(const DecArgs& a, uint32_t c, uint8_t* smem);
+
+__device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
+  __shared__ uint32_t s_tmp32[33];
+  __shared__ uint32_t s_bad, s_nlit, s_first_start;
+  __shared__ unsigned long long s_in;
   __shared__ int s_last;
+  const SegPair sp = a.segs[gseg];
+  const uint32_t c = sp.chunk;
+  const DChunk& C = a.ch[c];
+  const DecState S = parse_chunk(C);
+  DROLE(blockIdx.x, 1);
+  const uint32_t D = C.dim;
+  const uint32_t kUnitCap = vlz_unit_cap(a.vlz_dmax);
+  uint8_t* B = smem;                                                          // staged bytes (set below)
+  uint16_t* uend = reinterpret_cast<uint16_t*>(smem + vlz_bytes_cap(a.vlz_dmax));  // unit terminal byte
+  uint16_t(*J)[kSeg] = reinterpret_cast<uint16_t(*)[kSeg]>(reinterpret_cast<uint8_t*>(uend) + ((kUnitCap * 2 + 15) & ~15u));
+  uint32_t* lit = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(J) + kLift * kSeg * 2);  // literal tokens (<= kSeg/2)
+  if (S.err != ~0ull) return;  // every CTA of the chunk sees it: nobody waits on this segment
+  const uint8_t* p = C.in + S.pay_off;
+  const uint64_t L = S.pay_len;
+  const uint32_t b0 = sp.seg * kSeg;
+  const uint32_t nb = static_cast<uint32_t>(umin64(kSeg, L - b0));
+  const uint32_t sb = b0 >= kSegBack ? b0 - kSegBack : 0;
+  const uint32_t la = static_cast<uint32_t>(umin64(L - (b0 + nb), 10ull * (D + 1) + 10));
+  const uint32_t ns = b0 + nb + la - sb;
+  {  // 16-B loads of the aligned blocks covering [sb, sb + ns); B points at byte sb
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(p + sb);
+    const uint4* gv = reinterpret_cast<const uint4*>(g0 & ~uintptr_t(15));
+    const uint32_t lead = static_cast<uint32_t>(g0 & 15);
+    const uint32_t nv = (lead + ns + 15) / 16;
+    uint4* sv = reinterpret_cast<uint4*>(smem);
+    for (uint32_t k0 = 0; k0 < nv; k0 += 4 * blockDim.x) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t k = k0 + u * blockDim.x + threadIdx.x;
+        if (k < nv) v[u] = __ldg(gv + k);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t k = k0 + u * blockDim.x + threadIdx.x;
+        if (k < nv) sv[k] = v[u];
+      }
+    }
+    B = smem + lead;
+  }
+  if (threadIdx.x == 0) {
+    s_bad = 0;
+    s_nlit = 0;
+  }
+  __syncthreads();
+  DTS(blockIdx.x, 2);
+  // unit table: terminal bytes at payload offsets [b0, b0 + nb + la)
+  uint32_t nu = 0, U = 0;
+  for (uint32_t r0 = b0; r0 < b0 + nb + la && nu < kUnitCap; r0 += 8 * blockDim.x) {
+    const uint32_t x0 = r0 + threadIdx.x * 8;
+    uint32_t mask = 0, nseg_here = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (x0 + k < b0 + nb + la && !(B[x0 + k - sb] & 0x80)) {
+        mask |= 1u << k;
+        nseg_here += x0 + k < b0 + nb;
+      }
+    uint32_t tot;
+    uint32_t k0 = nu + block_excl_scan<uint32_t>(__popc(mask), s_tmp32, &tot);
+    if (r0 == b0) U = block_sum<uint32_t>(nseg_here, s_tmp32);  // the segment lies in the first round
+    uint32_t m = mask;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      if (k0 < kUnitCap) uend[k0] = static_cast<uint16_t>(x0 + b - sb);
+      ++k0;
+    }
+    nu += tot;
+  }
+  nu = min(nu, kUnitCap);
+  if (threadIdx.x == 0) {  // the first unit may begin in the previous segment
+    uint32_t start = b0;
+    while (start > 0 && (p[start - 1] & 0x80) && b0 - start <= 10) --start;
+    s_first_start = start - sb;
+    // a trailing partial unit can never be consumed by a valid parse
+    if (b0 + nb == L && nb > 0 && (B[L - 1 - sb] & 0x80)) s_bad = 1;
+  }
+  __syncthreads();
+  DTS(blockIdx.x, 3);
+  auto ustart = [&](uint32_t k) -> uint32_t { return k ? uend[k - 1] + 1u : s_first_start; };
+  // unit kinds -> level-0 jumps; units longer than 10 bytes are never valid (bytes.hpp:139-147)
+  for (uint32_t k = threadIdx.x; k < U; k += blockDim.x) {
+    const uint32_t st0 = ustart(k), e = uend[k];
+    const uint32_t len = e - st0 + 1;
+    if (len > 10) s_bad = 1;
+    const uint8_t v = B[st0];
+    const uint32_t kind = (len == 1 && v <= 1) ? v : 2;
+    J[0][k] = kind == 2 ? kInv : static_cast<uint16_t>(k + (kind == 0 ? D + 1 : 2));
+  }
+  __syncthreads();
+  int nlev = kLift;  // levels past the point where every jump has left the segment are copies
+  for (int r = 1; r < kLift; ++r) {
+    bool live = false;
+    for (uint32_t k = threadIdx.x; k < U; k += blockDim.x) {
+      const uint16_t j = J[r - 1][k];
+      const uint16_t v = (j == kInv || j >= U) ? j : J[r - 1][j];
+      J[r][k] = v;
+      live |= v != kInv && v < U;
+    }
+    if (!__syncthreads_or(live)) {
+      nlev = r + 1;
+      break;
+    }
+  }
+  DTS(blockIdx.x, 4);
+  // entry -> (exit offset into the next segment, tokens) for entries 0..D
+  uint32_t* mymap = a.maps + C.map_base + static_cast<uint64_t>(sp.seg) * (D + 1);
+  for (uint32_t e = threadIdx.x; e <= D; e += blockDim.x) {
+    uint32_t m;
+    if (e >= U) {
+      m = e - U;  // no token starts in this segment
+    } else {
+      uint32_t pos = e, n = 0;
+      for (int r = nlev - 1; r >= 0; --r) {
+        const uint16_t j = J[r][pos];
+        if (j != kInv && j < U) {
+          pos = j;
+          n += 1u << r;
+        }
+      }
+      const uint16_t x = J[0][pos];
+      m = x == kInv ? 0xFFFFFFFFu : (((n + 1) << 16) | (x - U));
+    }
+    mymap[e] = m;
+  }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == total - 1;
+  DTS(blockIdx.x, 5);
+  unsigned long long* status = a.seg_status;
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0 && sp.seg > 0) st_vol(status + gseg, kStAgg);
+    unsigned long long in;
+    if (sp.seg == 0) {
+      in = vlz_state(false, 0, 0);
+    } else {
+      unsigned long long w;
+      const uint32_t q = find_inclusive(status, C.seg0, gseg, &w);
+      bool dead = (w >> 61) & 1;
+      uint32_t e = static_cast<uint32_t>(w >> 32) & 0x7FF, rows = static_cast<uint32_t>(w);
+      // apply the maps published after it: batches loaded in parallel into
+      // shared memory (the literal queue is free until the tokens), applied in order
+      const uint32_t cap = max(1u, kSeg / (D + 1));  // lit holds kSeg u32
+      for (uint32_t m0 = q + 1; m0 < gseg && !dead; m0 += cap) {
+        const uint32_t nm = min(cap, gseg - m0);
+        const uint32_t* src = a.maps + C.map_base + static_cast<uint64_t>(m0 - C.seg0) * (D + 1);
+        for (uint32_t k = threadIdx.x; k < nm * (D + 1); k += 32) lit[k] = __ldcg(src + k);
+        __syncwarp();
+        for (uint32_t m = 0; m < nm && !dead; ++m) {
+          const uint32_t v = lit[m * (D + 1) + e];
+          if (v == 0xFFFFFFFFu) dead = true;
+          else {
+            rows += v >> 16;
+            e = v & 0xFFFF;
+          }
+        }
+        __syncwarp();
+      }
+      in = vlz_state(dead, e, rows);
+    }
+    if (threadIdx.x == 0) {
+      bool dead = (in >> 61) & 1;
+      const uint32_t e = static_cast<uint32_t>(in >> 32) & 0x7FF, rows = static_cast<uint32_t>(in);
+      uint32_t eo = 0, ro = rows;
+      if (!dead) {
+        const uint32_t v = mymap[e];
+        if (v == 0xFFFFFFFFu) dead = true;
+        else {
+          eo = v & 0xFFFF;
+          ro = rows + (v >> 16);
+          if (ro > C.count) dead = true;  // more tokens than vectors: trailing bytes
+        }
+      }
+      st_vol(status + gseg, kStInc | vlz_state(dead, eo, ro));
+      s_in = in;
+    }
+  }
   __syncthreads();
-  if (s_last) __threadfence();
-  return s_last != 0;
+  DTS(blockIdx.x, 6);
+  const unsigned long long in = s_in;
+  const bool dead_in = (in >> 61) & 1;
+  const uint32_t e_in = static_cast<uint32_t>(in >> 32) & 0x7FF, row0 = static_cast<uint32_t>(in);
+  bool bad = s_bad || dead_in;
+  const uint32_t T = (!bad && e_in < U) ? (mymap[e_in] == 0xFFFFFFFFu ? 0 : mymap[e_in] >> 16) : 0;
+  if (!bad && e_in < U && mymap[e_in] == 0xFFFFFFFFu) bad = true;
+  if (!bad && row0 + T > C.count) bad = true;
+  // every token of the segment: reference offsets validated (vlz.hpp:141-145),
+  // literal tokens queued for the warp decoder
+  const double w = 2.0 * S.eb;
+  uint32_t* row_src = a.row_src + C.row_base;
+  if (!bad) {
+    for (uint32_t t = threadIdx.x; t < T; t += blockDim.x) {
+      uint32_t u = e_in;
+      for (int r = 0; r < nlev; ++r)
+        if ((t >> r) & 1) u = J[r][u];
+      const uint32_t row = row0 + t;
+      const uint8_t tag = B[uend[u]];
+      if (tag == 0x01) {
+        if (u + 1 >= nu) {
+          s_bad = 1;
+          continue;
+        }
+        const uint32_t s1 = ustart(u + 1), e1 = uend[u + 1];
+        if (e1 - s1 + 1 > 10) {
+          s_bad = 1;
+          continue;
+        }
+        const uint64_t off = stage_varint(B, s1, e1);
+        if (off < 1 || off > row || off > kMaxWindow) {
+          s_bad = 1;
+          continue;
+        }
+        row_src[row] = row - static_cast<uint32_t>(off);
+      } else {
+        row_src[row] = row;
+        const uint32_t k = atomicAdd(&s_nlit, 1u);
+        lit[2 * k] = row;
+        lit[2 * k + 1] = u;
+      }
+    }
+  }
+  __syncthreads();
+  DTS(blockIdx.x, 8);
+  if (!bad) {  // literal rows: 0x00 then dim zigzag varints, one warp per row
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t nl = s_nlit;
+    for (uint32_t q = warp; q < nl; q += nw) {
+      const uint32_t row = lit[2 * q], u = lit[2 * q + 1];
+      for (uint32_t j = lane; j < D; j += 32) {
+        const uint32_t k = u + 1 + j;
+        if (k >= nu) {
+          s_bad = 1;
+          break;
+        }
+        const uint32_t s1 = ustart(k), e1 = uend[k];
+        if (e1 - s1 + 1 > 10) {
+          s_bad = 1;
+          break;
+        }
+        store_value(C, static_cast<uint64_t>(row) * D + j, unzigzag(static_cast<uint32_t>(stage_varint(B, s1, e1))), w);
+      }
+    }
+  }
+  __syncthreads();
+  DTS(blockIdx.x, 9);
+  if (threadIdx.x == 0 && (bad || s_bad)) atomicOr(&a.vflag[c], 1u);
+  // the chunk's last segment to finish checks the end state and resolves roots
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.cnt[c], 1u) == C.nseg - 1;
+  __syncthreads();
+  DTS(blockIdx.x, 10);
+  if (!s_last) return;
+  __threadfence();
+  vlz_roots(a, c, smem);
+  DTS(blockIdx.x, 11);
 }
 
-__global__ void __launch_bounds__(kBlock) k_dec_s1(DecPlan P, DecArgs a) {
+// Reference chains -> root rows, in row blocks of kRootBlock: every source of
+// a row is an earlier row, so sources before the block are already final and
+// sources inside it resolve by pointer jumping.
+__device__ void vlz_roots(const DecArgs& a, uint32_t c, uint8_t* smem) {
+  __shared__ int s_ok;
+  const DChunk& C = a.ch[c];
+  if (threadIdx.x == 0) {
+    const unsigned long long w = ld_vol(a.seg_status + C.seg0 + C.nseg - 1);
+    const bool dead = (w >> 61) & 1;
+    const uint32_t e = static_cast<uint32_t>(w >> 32) & 0x7FF, rows = static_cast<uint32_t>(w);
+    s_ok = !dead && rows == C.count && e == 0 && !*reinterpret_cast<volatile uint32_t*>(&a.vflag[c]);
+    if (!s_ok) a.vflag[c] = 1;
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  uint32_t* src = a.row_src + C.row_base;
+  const bool in_smem = C.count <= a.smem_bytes / 4;
+  uint32_t* A = in_smem ? reinterpret_cast<uint32_t*>(smem) : src;  // whole chunk in smem when it fits
+  if (in_smem) {
+    for (uint32_t k0 = 0; k0 < C.count; k0 += 8 * blockDim.x) {
+      uint32_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t k = k0 + u * blockDim.x + threadIdx.x;
+        if (k < C.count) v[u] = __ldcg(src + k);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t k = k0 + u * blockDim.x + threadIdx.x;
+        if (k < C.count) A[k] = v[u];
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t b0 = 0; b0 < C.count; b0 += kRootBlock) {
+    const uint32_t n = min(kRootBlock, C.count - b0);
+    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {  // sources before the block hold their root
+      const uint32_t s = in_smem ? A[b0 + k] : __ldcg(A + b0 + k);
+      if (s < b0) A[b0 + k] = in_smem ? A[s] : __ldcg(A + s);
+    }
+    if (!in_smem) __threadfence();
+    __syncthreads();
+    for (;;) {  // pointer jumping inside the block
+      bool changed = false;
+      for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const uint32_t v = in_smem ? A[b0 + k] : __ldcg(A + b0 + k);
+        if (v >= b0 && v != b0 + k) {
+          const uint32_t vv = in_smem ? A[v] : __ldcg(A + v);
+          if (vv != v) {
+            A[b0 + k] = vv;
+            changed = true;
+          }
+        }
+      }
+      if (!in_smem) __threadfence();
+      if (!__syncthreads_or(changed)) break;
+    }
+  }
+  if (in_smem)
+    for (uint32_t k = threadIdx.x; k < C.count; k += blockDim.x) src[k] = A[k];
+}
+
+// ===========================================================================
+// Huffman blocks: 128 subsequences of 64 bits.
+// ===========================================================================
+constexpr uint32_t kHSub = 128;                        // subsequences per block
+constexpr uint32_t kHBits = kSubBits * kHSub;          // 8192 bits
+constexpr uint32_t kHPre = 2;                          // words staged before the block (warm-up)
+constexpr uint32_t kHWords = kHPre + kHBits / 32 + 4;  // + look-ahead past the block
+constexpr uint32_t kHOut = kHBits;                     // at most one symbol per bit
+// smem: LUT | staged words | per-subsequence chain summaries | group states, later the symbols (u16)
+constexpr uint32_t kHGsBytes = kHSub * 33 * 4;
+constexpr uint32_t kHOutBytes = kHOut * 2;
+constexpr uint32_t kHuffSmem = (1u << kL0) * 4 + ((kHWords * 4 + 15) & ~15u) + kHSub * 20 +
+                               (kHGsBytes > kHOutBytes ? kHGsBytes : kHOutBytes);
+
+// inclusive huffman state: flag | term (61:60) | entry bit offset (59:55) | symbols (54:0)
+__device__ __forceinline__ unsigned long long huf_state(uint32_t term, uint32_t e, uint64_t cnt) {
+  return (static_cast<unsigned long long>(term & 3) << 60) | (static_cast<unsigned long long>(e & 31) << 55) |
+         (cnt & ((1ull << 55) - 1));
+}
+
+// Huffman block (8192 bits = 128 subsequences of 64 bits):
+//  A  every subsequence decodes one chain that starts 64 bits early (in the
+//     previous subsequence), so it has usually synchronised with the true
+//     codeword boundaries by the time it enters: its starts inside the
+//     subsequence (bitmap), exit and symbol count.  A second chain starts at
+//     the previous subsequence's exit and runs until it lands on one of those
+//     starts.
+//  B  per group of 32 subsequences, lane r follows entry offset r: a known
+//     start or the precomputed entry resolves in O(1), anything else decodes
+//     until it lands on a start.  Group and block maps then give the block's
+//     entry -> (exit, symbols) map, published for a decoupled look-back over
+//     the chunk's earlier blocks.
+//  C  with the true entry known, every subsequence decodes its symbols into
+//     shared memory; the block stores them coalesced.
+__device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
+  __shared__ HTab t;
+  __shared__ uint32_t G[4][32], BM[32];
+  __shared__ uint32_t s_ge[4], s_gt[4];
+  __shared__ unsigned long long s_gc[4];
+  __shared__ unsigned long long s_in;
+  __shared__ int s_use;
+  const uint32_t c = a.hblk_chunk[gb];
+  const DChunk& C = a.ch[c];
+  const uint32_t b = gb - C.blk0;
+  uint32_t* lut = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* W = lut + (1u << kL0);
+  uint64_t* B0 = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(W) + ((kHWords * 4 + 15) & ~15u));
+  uint32_t* X0 = reinterpret_cast<uint32_t*>(B0 + kHSub);
+  uint32_t* Y0 = X0 + kHSub;
+  uint32_t* Ye = Y0 + kHSub;
+  uint32_t(*Gs)[33] = reinterpret_cast<uint32_t(*)[33]>(Ye + kHSub);
+  uint16_t* outs = reinterpret_cast<uint16_t*>(Ye + kHSub);  // reuses Gs after phase B
+  DROLE(blockIdx.x, 2);
+  if (threadIdx.x == 0) {  // the chunk CTA (an earlier ticket) publishes the tables
+    uint32_t delay = 32;
+    while (!*reinterpret_cast<volatile uint32_t*>(&a.ready[c])) {
+      __nanosleep(delay);
+      delay = min(delay * 2, 512u);
+    }
+    __threadfence();
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&a.st[c].err);
+    s_use = e == ~0ull && !*reinterpret_cast<volatile uint32_t*>(&a.hflag[c]);
+  }
+  __syncthreads();
+  if (!s_use) {  // nothing to decode: still publish, so later blocks never wait
+    if (threadIdx.x == 0) st_vol(a.blk_status + gb, kStInc | huf_state(1, 0, 0));
+    return;
+  }
+  const DecState& S = a.st[c];
+  HView hv = hview(a.tabs, C);
+  // tables written by another CTA of this launch: read through L2
+  for (uint32_t i = threadIdx.x; i < (1u << kL0); i += blockDim.x) lut[i] = __ldcg(hv.lut + i);
+  for (uint32_t i = threadIdx.x; i < sizeof(HTab) / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(&t)[i] = __ldcg(reinterpret_cast<const unsigned int*>(hv.tab) + i);
+  __syncthreads();
+  const uint64_t bit0 = static_cast<uint64_t>(b) * kHBits;
+  const uint8_t* bits = C.in + __ldcg(reinterpret_cast<const unsigned long long*>(&S.pay_off)) + t.bit_off;
+  // W[kHPre + k] = word k of the block; the two words before hold the previous block's tail
+  if (b > 0) stage_bits(W, kHWords, bits, t.nbits / 8, bit0 - 32 * kHPre);
+  else {
+    if (threadIdx.x < kHPre) W[threadIdx.x] = 0;
+    stage_bits(W + kHPre, kHWords - kHPre, bits, t.nbits / 8, bit0);
+  }
+  __syncthreads();
+  DTS(blockIdx.x, 2);
+  const uint32_t R = t.max_len;
+  const uint64_t nbits = t.nbits;
+  const uint32_t nloc = min(kHSub, C.nsub - b * kHSub);
+  const uint32_t nent = t.nent;
+  // decode from relative bit q (of subsequence i) until q >= 64, a start in
+  // `stop` (the result then follows xs), or the end
+  auto run = [&](uint32_t i, uint32_t q, uint64_t stop, uint32_t xs) -> uint32_t {
+    const uint64_t gbase = bit0 + static_cast<uint64_t>(i) * kSubBits;
+    uint32_t n = 0;
+    for (;;) {
+      if (q >= kSubBits) return pk(q - kSubBits, 0, n);
+      if ((stop >> q) & 1) return pk(pk_off(xs), pk_term(xs), n + pk_cnt(xs) - popc_below(stop, q));
+      if (gbase + q >= nbits) return pk(0, 2, n);
+      uint32_t len = 0;
+      if (decode_one(lut, t, speek(W, (kHPre * 32) + i * kSubBits + q), &len) < 0) return pk(0, 1, n);
+      if (gbase + q + len > nbits) return pk(0, 2, n);
+      q += len;
+      ++n;
+    }
+  };
+  // ---- A
+  const uint32_t i_me = threadIdx.x;
+  if (i_me < nloc) {
+    const uint64_t gbase = bit0 + static_cast<uint64_t>(i_me) * kSubBits;
+    const uint32_t base = kHPre * 32 + i_me * kSubBits;  // W bit of the subsequence start
+    uint64_t bm = 0;
+    uint32_t x0 = 0;
+    // warm-up from 64 bits earlier (none at the very start of the stream)
+    int p = gbase == 0 ? 0 : -64;
+    for (;;) {
+      if (p < 0) {
+        uint32_t len = 0;
+        if (decode_one(lut, t, speek(W, base + p), &len) < 0) {
+          p = 0;  // the early chain died: start at the subsequence itself
+          continue;
+        }
+        p += static_cast<int>(len);
+        continue;
+      }
+      break;
+    }
+    uint32_t q = static_cast<uint32_t>(p), cnt = 0;
+    for (;;) {
+      if (q >= kSubBits) {
+        x0 = pk(q - kSubBits, 0, cnt);
+        break;
+      }
+      if (gbase + q >= nbits) {
+        x0 = pk(0, 2, cnt);
+        break;
+      }
+      uint32_t len = 0;
+      if (decode_one(lut, t, speek(W, base + q), &len) < 0) {
+        x0 = pk(0, 1, cnt);
+        break;
+      }
+      if (gbase + q + len > nbits) {
+        x0 = pk(0, 2, cnt);
+        break;
+      }
+      bm |= 1ull << q;
+      q += len;
+      ++cnt;
+    }
+    B0[i_me] = bm;
+    X0[i_me] = x0;
+  }
+  __syncthreads();
+  if (i_me < nloc) {
+    uint32_t r = 0xFFFFFFFFu, y = 0;
+    if (i_me > 0 && !pk_term(X0[i_me - 1])) {
+      r = pk_off(X0[i_me - 1]);
+      const uint64_t bm = B0[i_me];
+      const uint32_t x0 = X0[i_me];
+      y = ((bm >> r) & 1) ? pk(pk_off(x0), pk_term(x0), pk_cnt(x0) - popc_below(bm, r)) : run(i_me, r, bm, x0);
+    }
+    Ye[i_me] = r;
+    Y0[i_me] = y;
+  }
+  __syncthreads();
+  DTS(blockIdx.x, 3);
+  // ---- B: group walks (Gs[i][r] = state at the entry of subsequence i for group entry r)
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ng = (nloc + 31) / 32;
+  if (warp < ng) {
+    uint32_t e = lane, term = lane < R ? 0 : 3, cnt = 0;  // entries >= max_len are unreachable
+    for (uint32_t j = 0; j < 32; ++j) {
+      const uint32_t i = warp * 32 + j;
+      if (i >= nloc) break;
+      Gs[i][lane] = pk(e, term, cnt);
+      // lanes that reached the same entry share one result
+      const uint32_t peers = __match_any_sync(0xffffffffu, term ? 0xFFFFFFFFu : e);
+      const int leader = __ffs(peers) - 1;
+      uint32_t f = 0;
+      if (!term && static_cast<int>(lane) == leader) {
+        const uint64_t sbm = B0[i];
+        const uint32_t sx = X0[i];
+        if ((sbm >> e) & 1) f = pk(pk_off(sx), pk_term(sx), pk_cnt(sx) - popc_below(sbm, e));
+        else if (Ye[i] == e) f = Y0[i];
+        else f = run(i, e, sbm, sx);
+      }
+      f = __shfl_sync(0xffffffffu, f, leader);
+      if (!term) {
+        term = pk_term(f);
+        cnt += pk_cnt(f);
+        e = pk_off(f);
+      }
+    }
+    G[warp][lane] = pk(e, term, cnt);
+  }
+  __syncthreads();
+  DTS(blockIdx.x, 4);
+  unsigned long long* status = a.blk_status;
+  if (warp == 0) {
+    uint32_t e = lane, term = 0, cnt = 0;
+    for (uint32_t g = 0; g < ng; ++g) {
+      if (!term) {
+        const uint32_t f = G[g][e];
+        term = pk_term(f);
+        cnt += pk_cnt(f);
+        e = pk_off(f);
+      }
+    }
+    const uint32_t bm = pk(e, term, cnt);
+    BM[lane] = bm;
+    a.bmaps[static_cast<uint64_t>(gb) * 32 + lane] = bm;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0 && b > 0) st_vol(status + gb, kStAgg);
+    unsigned long long in;
+    if (b == 0) {
+      in = huf_state(0, 0, 0);
+    } else {
+      unsigned long long w;
+      const uint32_t q = find_inclusive(status, C.blk0, gb, &w);
+      uint32_t tm = static_cast<uint32_t>(w >> 60) & 3, ee = static_cast<uint32_t>(w >> 55) & 31;
+      uint64_t cc = w & ((1ull << 55) - 1);
+      // maps published after it: lane e holds entry e of each map (loads in
+      // flight together), applied in order by shuffles
+      for (uint32_t m0 = q + 1; m0 < gb && !tm; m0 += 8) {
+        uint32_t f[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] = m0 + k < gb ? __ldcg(a.bmaps + static_cast<uint64_t>(m0 + k) * 32 + lane) : 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t v = __shfl_sync(0xffffffffu, f[k], ee);
+          if (m0 + k < gb && !tm) {
+            tm = pk_term(v);
+            cc += pk_cnt(v);
+            ee = pk_off(v);
+          }
+        }
+      }
+      in = huf_state(tm, ee, cc);
+    }
+    if (lane == 0) {
+      uint32_t tm = static_cast<uint32_t>(in >> 60) & 3, ee = static_cast<uint32_t>(in >> 55) & 31;
+      uint64_t cc = in & ((1ull << 55) - 1);
+      if (!tm) {
+        const uint32_t f = BM[ee];
+        tm = pk_term(f);
+        cc += pk_cnt(f);
+        ee = pk_off(f);
+      }
+      st_vol(status + gb, kStInc | huf_state(tm, ee, cc));
+      // fewer decodable symbols than the count: exhaustion / invalid prefix
+      // (huffman.hpp:274-288) -> the exact walker reports it
+      if (b == C.nblk - 1 && cc < C.N) atomicOr(&a.hflag[c], 1u);
+      s_in = in;
+      uint32_t ge = static_cast<uint32_t>(in >> 55) & 31, gt = static_cast<uint32_t>(in >> 60) & 3;
+      unsigned long long gc = in & ((1ull << 55) - 1);
+      for (uint32_t g = 0; g < ng; ++g) {
+        s_ge[g] = ge;
+        s_gt[g] = gt;
+        s_gc[g] = gc;
+        if (!gt) {
+          const uint32_t f = G[g][ge];
+          gt = pk_term(f);
+          gc += pk_cnt(f);
+          ge = pk_off(f);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  DTS(blockIdx.x, 5);
+  const uint64_t blk_base = s_in & ((1ull << 55) - 1);
+  if ((s_in >> 60) & 3) return;  // the chain ended before this block
+  const uint64_t N = C.N;
+  if (blk_base >= N) return;
+  // ---- C: decode every subsequence from its true entry
+  uint32_t q = pk(0, 1, 0);
+  if (threadIdx.x < nloc) {
+    const uint32_t g = threadIdx.x / 32;
+    if (!s_gt[g]) q = Gs[threadIdx.x][s_ge[g]];
+  }
+  __syncthreads();  // Gs is dead: its bytes take the symbols
+  const bool staged = nent <= 65536;
+  const uint64_t* vals = hv.vals;
+  if (threadIdx.x < nloc && !pk_term(q)) {
+    const uint32_t i = threadIdx.x, g = i / 32;
+    const uint64_t gbase = bit0 + static_cast<uint64_t>(i) * kSubBits;
+    uint64_t gi = s_gc[g] + pk_cnt(q);  // index of this subsequence's first symbol
+    uint32_t p = pk_off(q);
+    while (p < kSubBits && gi < N && gbase + p < nbits) {
+      uint32_t len = 0;
+      const int ent = decode_one(lut, t, speek(W, kHPre * 32 + i * kSubBits + p), &len);
+      if (ent < 0 || gbase + p + len > nbits) break;
+      if (staged) {
+        outs[gi - blk_base] = static_cast<uint16_t>(ent);
+      } else {
+        const uint64_t v = __ldcg(vals + ent);
+        if (C.out_kind == EMBC_OUT_F64) static_cast<uint64_t*>(C.out)[gi] = v;
+        else static_cast<uint32_t*>(C.out)[gi] = static_cast<uint32_t>(v);
+      }
+      p += len;
+      ++gi;
+    }
+  }
+  __syncthreads();
+  DTS(blockIdx.x, 6);
+  if (!staged) return;
+  // ---- coalesced stores of this block's symbols
+  const uint32_t own = pk_cnt(BM[static_cast<uint32_t>(s_in >> 55) & 31]);
+  const uint64_t nout = umin64(own, N - blk_base);
+  if (C.out_kind == EMBC_OUT_F64) {
+    uint64_t* o = static_cast<uint64_t*>(C.out) + blk_base;
+    for (uint32_t k = threadIdx.x; k < nout; k += blockDim.x) o[k] = __ldcg(vals + outs[k]);
+  } else {
+    uint32_t* o = static_cast<uint32_t*>(C.out) + blk_base;
+    for (uint32_t k = threadIdx.x; k < nout; k += blockDim.x) o[k] = static_cast<uint32_t>(__ldcg(vals + outs[k]));
+  }
+}
+
+// ===========================================================================
+// D1 / D2
+// ===========================================================================
+constexpr uint32_t kDecSmem = kVlzSmem > kHuffSmem ? kVlzSmem : kHuffSmem;
+
+__global__ void __launch_bounds__(kBlock) k_dec_main(DecArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_t;
+  if (threadIdx.x == 0) s_t = atomicAdd(&a.tickets[0], 1u);
+  __syncthreads();
+  uint32_t t = s_t;  // roles in ticket order: look-back only ever waits on earlier tickets
+  DROLE(blockIdx.x, 0);
+  DTS(blockIdx.x, 1);
+  if (t < a.nchunks) {  // chunk CTA
+    const DChunk& C = a.ch[t];
+    if (threadIdx.x == 0) a.st[t] = parse_chunk(C);
+    __syncthreads();
+    if (C.codec == EMBC_CODEC_HUFFMAN) {
+      huff_tables(t, a.ch, a.st, a.keys, a.tabs, a.hflag, reinterpret_cast<uint64_t*>(smem), a.smem_bytes / 8);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t*>(&a.ready[t]) = 1;
+    }
+    DTS(blockIdx.x, 7);
+    return;
+  }
+  t -= a.nchunks;
+  if (t < a.nseg) {
+    vlz_segment(a, t, smem);
+    DTS(blockIdx.x, 7);
+    return;
+  }
+  t -= a.nseg;
+  if (t < a.nhblk) {
+    huff_block(a, t, smem);
+    DTS(blockIdx.x, 7);
+    return;
+  }
+  t -= a.nhblk;
+  DROLE(blockIdx.x, 3);
+  DTS(blockIdx.x, 1);
+  const RawTile T = a.raw[t];
+  const DChunk& C = a.ch[T.chunk];
+  raw_tile(C, parse_chunk(C), T);
+  DTS(blockIdx.x, 7);
+}
+
+__global__ void __launch_bounds__(kBlock) k_dec_fin(DecArgs a) {
   uint32_t b = blockIdx.x;
-  if (b < P.n_seg) {
-    k_vlz_map_cta(b, a.ch, a.st, a.segs, a.ustart, a.ukind, a.segu, a.maps, a.vflag);
-    const uint32_t c = a.segs[b].chunk;
-    if (last_of(&a.cnt[c], a.ch[c].nseg) && threadIdx.x == 0)
-      vlz_chain_one(a.ch, a.st, c, a.maps, a.sege, a.segr, a.vflag);
+  if (b < a.nctile) {  // reference rows <- their root rows
+    const uint32_t c = a.ctile[3 * b], r0 = a.ctile[3 * b + 1], nr = a.ctile[3 * b + 2];
+    const DChunk& C = a.ch[c];
+    if (a.st[c].err != ~0ull || a.vflag[c]) return;
+    const uint32_t* src = a.row_src + C.row_base;
+    const uint32_t D = C.dim;
+    // 16-B units per row when rows are 16-B aligned, else 4-B (8-B for fp64) elements
+    const uint32_t esz = C.out_kind == EMBC_OUT_F64 ? 8 : 4;
+    const bool vec = ((D * esz) & 15) == 0 && (reinterpret_cast<uintptr_t>(C.out) & 15) == 0;
+    const uint32_t upr = vec ? D * esz / 16 : D;  // units per row
+    const uint32_t total = nr * upr;
+    for (uint32_t k0 = 0; k0 < total; k0 += 4 * blockDim.x) {
+      uint32_t rr[4], ss[4], cc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t k = k0 + u * blockDim.x + threadIdx.x;
+        rr[u] = 0xFFFFFFFFu;
+        if (k < total) {
+          const uint32_t rl = k / upr;
+          cc[u] = k - rl * upr;
+          rr[u] = r0 + rl;
+          ss[u] = src[rr[u]];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (rr[u] == 0xFFFFFFFFu || ss[u] == rr[u]) continue;
+        if (vec) {
+          const uint4* in = reinterpret_cast<const uint4*>(C.out) + static_cast<uint64_t>(ss[u]) * upr + cc[u];
+          uint4* o = reinterpret_cast<uint4*>(C.out) + static_cast<uint64_t>(rr[u]) * upr + cc[u];
+          *o = *in;
+        } else if (esz == 8) {
+          static_cast<uint64_t*>(C.out)[static_cast<uint64_t>(rr[u]) * D + cc[u]] =
+              static_cast<const uint64_t*>(C.out)[static_cast<uint64_t>(ss[u]) * D + cc[u]];
+        } else {
+          static_cast<uint32_t*>(C.out)[static_cast<uint64_t>(rr[u]) * D + cc[u]] =
+              static_cast<const uint32_t*>(C.out)[static_cast<uint64_t>(ss[u]) * D + cc[u]];
+        }
+      }
+    }
     return;
   }
-  b -= P.n_seg;
-  if (b < P.n_htab) {
-    k_huff_tables_cta(b, a.ch, a.st, a.hlist, a.keys, a.tabs, a.hflag);
-    return;
-  }
-  b -= P.n_htab;
-  k_dec_raw_cta(b, a.ch, a.st, a.raw);
-}
-
-__global__ void __launch_bounds__(kBlock) k_dec_s2(DecPlan P, DecArgs a) {
-  extern __shared__ __align__(16) uint8_t dsm[];
-  uint32_t b = blockIdx.x;
-  if (b < P.n_seg) {
-    k_vlz_rows_cta(b, dsm, a.ch, a.st, a.segs, a.ustart, a.ukind, a.segu, a.sege, a.segr, a.rtag, a.rsrc,
-                   a.vflag);
-    const uint32_t c = a.segs[b].chunk;
-    if (last_of(&a.cnt[P.nchunks + c], a.ch[c].nseg))
-      k_vlz_roots_cta(c, dsm, a.ch, a.st, nullptr, a.vflag, a.rsrc, a.rtag, a.rroot);
-    return;
-  }
-  b -= P.n_seg;
-  k_huff_maps_cta(b, dsm, a.ch, a.st, a.subt, a.tabs, a.hflag, a.qmaps, a.gmaps, a.bmaps);
-  const uint32_t c = a.subt[b].chunk;
-  if (last_of(&a.cnt[P.nchunks + c], (a.ch[c].nsub + kSubPerBlock - 1) / kSubPerBlock))
-    k_huff_walk_cta(c, dsm, kStage2Smem / 4, a.ch, a.st, nullptr, a.tabs, a.hflag, a.bmaps, a.bentry, a.bbase);
-}
-
-__global__ void __launch_bounds__(kBlock) k_dec_s3(DecPlan P, DecArgs a) {
-  const uint32_t b = blockIdx.x;
-  if (b < P.n_vt) {
-    k_vlz_out_cta(b, a.ch, a.st, a.vtiles, a.vflag, a.ustart, a.segu, a.rroot);
-    return;
-  }
-  k_huff_out_cta(b - P.n_vt, a.ch, a.st, a.subt, a.tabs, a.hflag, a.qmaps, a.gmaps, a.bentry, a.bbase);
-}
-
-// Exact sequential walkers for chunks the parallel path flagged (they
-// reproduce the reference's first error and message), then the fold.
-__global__ void __launch_bounds__(32) k_dec_s4(DecPlan P, DecArgs a) {
-  const uint32_t c = blockIdx.x;
+  // exact sequential walkers for chunks the parallel path flagged, then the fold
+  const uint32_t c = b - a.nctile;
   const uint8_t codec = a.ch[c].codec;
   if (threadIdx.x == 0 && a.st[c].err == ~0ull &&
       ((codec == EMBC_CODEC_VLZ && (a.ch[c].seq || a.vflag[c])) || (codec == EMBC_CODEC_HUFFMAN && a.hflag[c])))
     atomicAdd(a.diag, 1u);
   if (codec == EMBC_CODEC_VLZ) k_dec_vlz_seq_cta(c, a.ch, a.st, nullptr, a.vflag);
   else if (codec == EMBC_CODEC_HUFFMAN) k_dec_huff_seq_cta(c, a.ch, a.st, nullptr, a.tabs, a.hflag);
-  if (last_of(&a.cnt[2 * P.nchunks], P.nchunks) && threadIdx.x == 0) dec_fold(a.st, P.nchunks, a.err);
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.tickets[1], 1u) == a.nchunks - 1;
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    dec_fold(a.st, a.nchunks, a.err);
+#ifdef EMBC_DEBUG
+    const uint32_t nb = a.nchunks + a.nseg + a.nhblk + a.nraw;
+    if (a.nchunks >= 26 && (++g_dcalls) % 8 == 7 && nb <= 16384) {
+      unsigned long long t0 = ~0ull;
+      for (uint32_t k = 0; k < nb; ++k) t0 = min(t0, g_dts[k][1]);
+      const char* names[4] = {"chunk", "vlzseg", "hufblk", "raw"};
+      for (uint32_t role = 0; role < 4; ++role) {
+        unsigned long long n = 0, mn = ~0ull, mx = 0, sum[12] = {0}, mxs[12] = {0};
+        for (uint32_t k = 0; k < nb; ++k) {
+          if (g_dts[k][0] != role) continue;
+          ++n;
+          mn = min(mn, g_dts[k][1] - t0);
+          mx = max(mx, g_dts[k][7] - t0);
+          unsigned long long prev = g_dts[k][1];
+          for (int q = 2; q <= 7; ++q) {
+            if (!g_dts[k][q]) continue;
+            if (q == 7 && g_dts[k][8]) {  // extra stamps 8..11 recorded between 6 and 7
+              for (int x = 8; x <= 11; ++x) {
+                if (!g_dts[k][x]) continue;
+                const unsigned long long d = g_dts[k][x] - prev;
+                sum[x] += d;
+                mxs[x] = max(mxs[x], d);
+                prev = g_dts[k][x];
+              }
+            }
+            const unsigned long long d = g_dts[k][q] - prev;
+            sum[q] += d;
+            mxs[q] = max(mxs[q], d);
+            prev = g_dts[k][q];
+          }
+        }
+        if (!n) continue;
+        printf("D1 %-6s n %4llu span [%6llu %6llu] phase mean/max ns: 2:%llu/%llu 3:%llu/%llu 4:%llu/%llu 5:%llu/%llu 6:%llu/%llu 8:%llu/%llu 9:%llu/%llu 10:%llu/%llu 11:%llu/%llu 7:%llu/%llu\n",
+               names[role], n, mn, mx, sum[2] / n, mxs[2], sum[3] / n, mxs[3], sum[4] / n, mxs[4], sum[5] / n, mxs[5],
+               sum[6] / n, mxs[6], sum[8] / n, mxs[8], sum[9] / n, mxs[9], sum[10] / n, mxs[10], sum[11] / n, mxs[11], sum[7] / n, mxs[7]);
+      }
+    }
+#endif
+  }
 }
 
 }  // namespace embc_dev
-
-namespace embc_host {
-cudaError_t decode_set_attributes() {
-  return cudaSuccess;
-}
-}  // namespace embc_host
 
 // ===========================================================================
 // host orchestration
@@ -1328,18 +1556,19 @@ using namespace embc_dev;
 
 static inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
+cudaError_t decode_set_attributes() {
+  return cudaFuncSetAttribute(k_dec_main, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
+}
+
 embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* refs, uint32_t n,
                    int out_kind, int payload_only, cudaStream_t stream) {
   if (n == 0) return EMBC_OK;
   if (!d_in) return set_error(ctx, EMBC_ERR_ARGUMENT, 0, 0, 0, 0, 0, "null input buffer");
   std::vector<DChunk> ch(n);
   std::vector<RawTile> raw_tiles;
-  std::vector<ElemTile> vlz_tiles;
   std::vector<SegPair> segs;
-  std::vector<SubTile> subtiles;
-  std::vector<uint32_t> vlz_list, huf_list;
-  uint64_t map_total = 0, row_total = 0, tab_total = 0, sub_total = 0;
-  uint32_t seg_total = 0, max_blocks = 1;
+  std::vector<uint32_t> hblk, ctiles;
+  uint64_t map_total = 0, row_total = 0, tab_total = 0;
   const uint64_t hdr = payload_only ? 0 : kHeader;
   for (uint32_t c = 0; c < n; ++c) {
     const embc_chunk_ref& r = refs[c];
@@ -1363,19 +1592,22 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
       const uint64_t per = 8192;
       for (uint64_t e = 0; e < C.N; e += per) raw_tiles.push_back(RawTile{c, 0, e, std::min(per, C.N - e)});
     } else if (r.codec == EMBC_CODEC_VLZ) {
-      vlz_list.push_back(c);
-      C.seq = (r.dim == 0 || r.dim > kVlzMaxDim || C.N >= (1ull << 31) || (pay == 0 && r.count > 0)) ? 1 : 0;
+      C.seq = (r.dim == 0 || r.dim > kVlzMaxDim || C.N >= (1ull << 31) || pay >= (1ull << 31) ||
+               (pay == 0 && r.count > 0)) ? 1 : 0;
       if (!C.seq) {
         C.nseg = static_cast<uint32_t>((pay + kSeg - 1) / kSeg);
-        C.seg0 = seg_total;
-        seg_total += C.nseg;
+        C.seg0 = static_cast<uint32_t>(segs.size());
         C.map_base = map_total;
         map_total += static_cast<uint64_t>(C.nseg) * (r.dim + 1);
         C.row_base = row_total;
         row_total += r.count;
         for (uint32_t s = 0; s < C.nseg; ++s) segs.push_back(SegPair{c, s});
-        const uint64_t per = 8192;
-        for (uint64_t e = 0; e < C.N; e += per) vlz_tiles.push_back(ElemTile{c, 0, e, std::min(per, C.N - e)});
+        const uint32_t per = std::max<uint32_t>(8, 8192 / std::max<uint32_t>(r.dim, 1));
+        for (uint32_t r0 = 0; r0 < r.count; r0 += per) {
+          ctiles.push_back(c);
+          ctiles.push_back(r0);
+          ctiles.push_back(std::min(per, r.count - r0));
+        }
       }
     } else {
       const uint64_t cap = pay > 12 ? (pay - 12) / 5 + 1 : 1;
@@ -1385,13 +1617,13 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
       C.tab_off = tab_total;
       tab_total += std::max<uint64_t>(htab_bytes(C.book_cap), 8 * p2 + 16);
       C.nsub = static_cast<uint32_t>((8 * (pay > 12 ? pay - 12 : 0) + kSubBits - 1) / kSubBits);
-      C.sub0 = sub_total;  // block-aligned so each CTA's subsequences share one block map
-      sub_total += (C.nsub + kSubPerBlock - 1) / kSubPerBlock * kSubPerBlock;
-      max_blocks = std::max<uint32_t>(max_blocks, (C.nsub + kSubPerBlock - 1) / kSubPerBlock);
-      for (uint32_t s = 0; s < C.nsub; s += kSubPerBlock) subtiles.push_back(SubTile{c, s});
-      huf_list.push_back(c);
+      C.nblk = (C.nsub + kHSub - 1) / kHSub;
+      C.blk0 = static_cast<uint32_t>(hblk.size());
+      for (uint32_t k = 0; k < C.nblk; ++k) hblk.push_back(c);
     }
   }
+  const uint32_t nseg = static_cast<uint32_t>(segs.size()), nhb = static_cast<uint32_t>(hblk.size());
+  const uint32_t nct = static_cast<uint32_t>(ctiles.size() / 3);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t o = off;
@@ -1400,101 +1632,76 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   };
   const size_t o_ch = take(sizeof(DChunk) * n);
   const size_t o_raw = take(sizeof(RawTile) * (raw_tiles.size() + 1));
-  const size_t o_vt = take(sizeof(ElemTile) * (vlz_tiles.size() + 1));
-  const size_t o_segs = take(sizeof(SegPair) * (segs.size() + 1));
-  const size_t o_st2 = take(sizeof(SubTile) * (subtiles.size() + 1));
-  const size_t o_vl = take(sizeof(uint32_t) * (vlz_list.size() + 1));
-  const size_t o_hl = take(sizeof(uint32_t) * (huf_list.size() + 1));
-  const size_t o_flags = take(sizeof(uint32_t) * (5 * n + 1));  // vflag | hflag | tickets, zeroed by the upload
-  const size_t host_bytes = off;
+  const size_t o_segs = take(sizeof(SegPair) * (nseg + 1));
+  const size_t o_hblk = take(sizeof(uint32_t) * (nhb + 1));
+  const size_t o_ct = take(sizeof(uint32_t) * (ctiles.size() + 1));
+  const size_t o_flags = take(sizeof(uint32_t) * (4 * n + 4));  // vflag | hflag | ready | cnt | tickets
+  const size_t o_sst = take(sizeof(unsigned long long) * (nseg + 1));
+  const size_t o_bst = take(sizeof(unsigned long long) * (nhb + 1));
+  const size_t host_bytes = off;  // uploaded (status words and flags start at zero)
   const size_t o_st = take(sizeof(DecState) * n);
-  const size_t o_ustart = take(sizeof(uint32_t) * (static_cast<size_t>(seg_total) * kSeg + 1));
-  const size_t o_ukind = take(static_cast<size_t>(seg_total) * kSeg + 1);
-  const size_t o_segu = take(sizeof(uint32_t) * (seg_total + 1));
-  const size_t o_sege = take(sizeof(uint32_t) * (seg_total + 1));
-  const size_t o_segr = take(sizeof(uint32_t) * (seg_total + 1));
-  const size_t o_maps = take(sizeof(uint64_t) * (map_total + 1));
-  const size_t o_rtag = take(sizeof(uint32_t) * (row_total + 1));
+  const size_t o_maps = take(sizeof(uint32_t) * (map_total + 1));
+  const size_t o_bmaps = take(sizeof(uint32_t) * 32 * (nhb + 1));
   const size_t o_rsrc = take(sizeof(uint32_t) * (row_total + 1));
-  const size_t o_rroot = take(sizeof(uint32_t) * (row_total + 1));
   const size_t o_tabs = take(tab_total + 16);
   const size_t o_keys = take(tab_total + 16);
-  const size_t o_pmaps = take(sizeof(uint32_t) * 32 * (sub_total + 1));
-  const size_t o_gmaps = take(sizeof(uint32_t) * 32 * (sub_total / kGroup + 1));
-  const size_t o_bmaps = take(sizeof(uint32_t) * 32 * (sub_total / kSubPerBlock + 1));
-  const size_t o_bentry = take(sizeof(uint32_t) * (sub_total / kSubPerBlock + 1));
-  const size_t o_bbase = take(sizeof(uint64_t) * (sub_total / kSubPerBlock + 1));
   cudaError_t ce = ensure_scratch(ctx, off);
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "scratch allocation");
   uint8_t* hs = nullptr;
   int slot = -1;
   ce = stage_acquire(ctx, host_bytes, stream, &hs, &slot);
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "staging allocation");
+  std::memset(hs, 0, host_bytes);
   std::memcpy(hs + o_ch, ch.data(), sizeof(DChunk) * n);
   std::memcpy(hs + o_raw, raw_tiles.data(), sizeof(RawTile) * raw_tiles.size());
-  std::memcpy(hs + o_vt, vlz_tiles.data(), sizeof(ElemTile) * vlz_tiles.size());
-  std::memcpy(hs + o_segs, segs.data(), sizeof(SegPair) * segs.size());
-  std::memcpy(hs + o_st2, subtiles.data(), sizeof(SubTile) * subtiles.size());
-  std::memcpy(hs + o_vl, vlz_list.data(), sizeof(uint32_t) * vlz_list.size());
-  std::memcpy(hs + o_hl, huf_list.data(), sizeof(uint32_t) * huf_list.size());
-  std::memset(hs + o_flags, 0, sizeof(uint32_t) * (5 * n + 1));
+  std::memcpy(hs + o_segs, segs.data(), sizeof(SegPair) * nseg);
+  std::memcpy(hs + o_hblk, hblk.data(), sizeof(uint32_t) * nhb);
+  std::memcpy(hs + o_ct, ctiles.data(), sizeof(uint32_t) * ctiles.size());
   uint8_t* d = ctx->d_scratch;
   ce = cudaMemcpyAsync(d, hs, host_bytes, cudaMemcpyHostToDevice, stream);
   if (ce == cudaSuccess) ce = stage_commit(ctx, slot, stream);
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "descriptor upload");
-  const DChunk* d_ch = reinterpret_cast<const DChunk*>(d + o_ch);
-  DecState* d_st = reinterpret_cast<DecState*>(d + o_st);
-  uint32_t* vflag = reinterpret_cast<uint32_t*>(d + o_flags);
-  uint32_t* hflag = vflag + n;
-  const uint32_t* d_vl = reinterpret_cast<const uint32_t*>(d + o_vl);
-  const uint32_t* d_hl = reinterpret_cast<const uint32_t*>(d + o_hl);
-  uint8_t* tabs = d + o_tabs;
   DecArgs a{};
-  a.ch = d_ch;
-  a.st = d_st;
+  a.ch = reinterpret_cast<const DChunk*>(d + o_ch);
+  a.st = reinterpret_cast<DecState*>(d + o_st);
   a.segs = reinterpret_cast<const SegPair*>(d + o_segs);
-  a.vlist = d_vl;
-  a.hlist = d_hl;
+  a.hblk_chunk = reinterpret_cast<const uint32_t*>(d + o_hblk);
   a.raw = reinterpret_cast<const RawTile*>(d + o_raw);
-  a.vtiles = reinterpret_cast<const ElemTile*>(d + o_vt);
-  a.subt = reinterpret_cast<const SubTile*>(d + o_st2);
-  a.vflag = vflag;
-  a.hflag = hflag;
-  a.cnt = vflag + 2 * n;
-  a.ustart = reinterpret_cast<uint32_t*>(d + o_ustart);
-  a.ukind = d + o_ukind;
-  a.segu = reinterpret_cast<uint32_t*>(d + o_segu);
-  a.sege = reinterpret_cast<uint32_t*>(d + o_sege);
-  a.segr = reinterpret_cast<uint32_t*>(d + o_segr);
-  a.maps = reinterpret_cast<uint64_t*>(d + o_maps);
-  a.rtag = reinterpret_cast<uint32_t*>(d + o_rtag);
-  a.rsrc = reinterpret_cast<uint32_t*>(d + o_rsrc);
-  a.rroot = reinterpret_cast<uint32_t*>(d + o_rroot);
-  a.keys = reinterpret_cast<uint64_t*>(d + o_keys);
-  a.tabs = tabs;
-  a.qmaps = reinterpret_cast<uint32_t*>(d + o_pmaps);
-  a.gmaps = reinterpret_cast<uint32_t*>(d + o_gmaps);
+  a.ctile = reinterpret_cast<const uint32_t*>(d + o_ct);
+  uint32_t* flags = reinterpret_cast<uint32_t*>(d + o_flags);
+  a.vflag = flags;
+  a.hflag = flags + n;
+  a.ready = flags + 2 * n;
+  a.cnt = flags + 3 * n;
+  a.tickets = flags + 4 * n;
+  a.seg_status = reinterpret_cast<unsigned long long*>(d + o_sst);
+  a.blk_status = reinterpret_cast<unsigned long long*>(d + o_bst);
+  a.maps = reinterpret_cast<uint32_t*>(d + o_maps);
   a.bmaps = reinterpret_cast<uint32_t*>(d + o_bmaps);
-  a.bentry = reinterpret_cast<uint32_t*>(d + o_bentry);
-  a.bbase = reinterpret_cast<uint64_t*>(d + o_bbase);
+  a.row_src = reinterpret_cast<uint32_t*>(d + o_rsrc);
+  a.keys = reinterpret_cast<uint64_t*>(d + o_keys);
+  a.tabs = d + o_tabs;
   a.err = ctx->d_err;
   a.diag = ctx->d_diag;
+  a.nchunks = n;
+  a.nseg = nseg;
+  a.nhblk = nhb;
+  a.nraw = static_cast<uint32_t>(raw_tiles.size());
+  a.nctile = nct;
   cudaMemsetAsync(ctx->d_diag, 0, sizeof(uint32_t), stream);
-  DecPlan P{};
-  P.n_seg = static_cast<uint32_t>(segs.size());
-  P.n_htab = static_cast<uint32_t>(huf_list.size());
-  P.n_raw = static_cast<uint32_t>(raw_tiles.size());
-  P.n_sub = static_cast<uint32_t>(subtiles.size());
-  P.n_vt = static_cast<uint32_t>(vlz_tiles.size());
-  P.nchunks = n;
-  EMBC_TIMED(ctx, "k_dec_parse", stream, k_dec_parse<<<(n + 127) / 128, 128, 0, stream>>>(d_ch, d_st, n));
-  if (P.n_seg + P.n_htab + P.n_raw)
-    EMBC_TIMED(ctx, "k_dec_s1", stream, k_dec_s1<<<P.n_seg + P.n_htab + P.n_raw, kBlock, 0, stream>>>(P, a));
-  if (P.n_seg + P.n_sub)
-    EMBC_TIMED(ctx, "k_dec_s2", stream, k_dec_s2<<<P.n_seg + P.n_sub, kBlock, kStage2Smem, stream>>>(P, a));
-  if (P.n_vt + P.n_sub)
-    EMBC_TIMED(ctx, "k_dec_s3", stream, k_dec_s3<<<P.n_vt + P.n_sub, kBlock, 0, stream>>>(P, a));
-  EMBC_TIMED(ctx, "k_dec_s4", stream, k_dec_s4<<<n, 32, 0, stream>>>(P, a));
+  const uint32_t g1 = n + nseg + nhb + a.nraw;
+  uint32_t dmax = 1;
+  for (uint32_t c = 0; c < n; ++c)
+    if (ch[c].codec == EMBC_CODEC_VLZ && !ch[c].seq) dmax = std::max(dmax, ch[c].dim);
+  a.vlz_dmax = dmax;
+  uint32_t rmax = 0;  // rows of the largest vlz chunk: the root tail keeps them in smem
+  for (uint32_t c = 0; c < n; ++c)
+    if (ch[c].codec == EMBC_CODEC_VLZ && !ch[c].seq) rmax = std::max(rmax, ch[c].count);
+  uint32_t smem = std::max<uint32_t>(std::max<uint32_t>(nseg ? vlz_smem(dmax) : 0, nhb ? kHuffSmem : 0), 16384);
+  if (nseg) smem = std::max<uint32_t>(smem, std::min<uint32_t>(4 * rmax + 64, 48 * 1024));
+  a.smem_bytes = smem;
+  EMBC_TIMED(ctx, "k_dec_main", stream, k_dec_main<<<g1, kBlock, smem, stream>>>(a));
+  EMBC_TIMED(ctx, "k_dec_fin", stream, k_dec_fin<<<nct + n, kBlock, 0, stream>>>(a));
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "decode launch");
   return EMBC_OK;

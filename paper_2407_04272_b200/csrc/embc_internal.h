@@ -70,8 +70,9 @@ struct DChunk {
   uint64_t row_base;       // first per-row entry
   // huffman plan
   uint64_t tab_off;        // byte offset of this chunk's decode tables
-  uint64_t sub0;           // first subsequence slot
-  uint32_t nsub, pad2;
+  uint32_t nsub;           // 64-bit subsequences of the bitstream
+  uint32_t blk0, nblk;     // global index range of this chunk's decode blocks
+  uint32_t pad2;
 };
 
 // Per-chunk decode state (device).
