@@ -7,7 +7,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_kg_${TAG}.log 2>&1
 timeout 600 python bench.py --workload tb --no-cpu-baseline > gpurun_out/bench_tb_${TAG}.log 2>&1
 tail -5 gpurun_out/pytest_gpu_${TAG}.log; tail -2 gpurun_out/smoke_${TAG}.log
-for w in kg tb; do python - gpurun_out/bench_${w}_${TAG}.log <<'PY'
+python tools/show_bench.py gpurun_out/bench_kg_${TAG}.log gpurun_out/bench_tb_${TAG}.log; exit 0
 import json,sys
 t=open(sys.argv[1]).read().strip().splitlines()
 try:
