@@ -42,8 +42,8 @@ constexpr uint32_t kSmemBook = 1024;     // codebook symbols sorted fully in sha
 __host__ __device__ constexpr uint32_t emit_codes_bytes(uint32_t vals, uint32_t rows) {
   return ((vals + rows + 64) * 4 + 15) & ~15u;
 }
-__host__ __device__ constexpr uint32_t emit_stage_bytes(uint32_t vals, uint32_t rows) {
-  return (rows + 5 * vals + 128 + 15) & ~15u;
+__host__ __device__ constexpr uint32_t emit_stage_bytes(uint32_t vals, uint32_t rows, bool vlz = true) {
+  return ((vlz ? rows + 5 * vals : 4 * vals) + 128 + 15) & ~15u;
 }
 constexpr uint32_t kAuxBytes = kHashStage * 4 + kMaxTileRows * 20;  // hashes | dec, lits, cand, plist, miss
 constexpr uint32_t kEmitSmemMax = emit_codes_bytes(kMaxRowVals, kMaxTileRows) +
@@ -332,6 +332,22 @@ __device__ void build_book(const DJob& J, JobState* Sp, const BookArgs& a, uint8
   }
 }
 
+#ifdef EMBC_DEBUG
+__device__ unsigned long long g_dbg[8];
+__device__ unsigned long long g_ts[16384][6];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TS(k) do { if (threadIdx.x == 0 && tid < 16384) g_ts[tid][k] = gtime(); } while (0)
+__device__ unsigned long long g_ts1[16384][6];
+#define TS1(k) do { if (threadIdx.x == 0 && blockIdx.x < 16384) g_ts1[blockIdx.x][k] = gtime(); } while (0)
+#else
+#define TS(k) do {} while (0)
+#define TS1(k) do {} while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // E1: quantize + per-tile statistics (+ codebook tail)
 // ---------------------------------------------------------------------------
@@ -347,18 +363,23 @@ struct StatsArgs {
   uint32_t hist_off;  // dynamic smem offset of the histogram window
 };
 
-__global__ void __launch_bounds__(kBlock) k_stats(StatsArgs a) {
+__global__ void __launch_bounds__(kBlock, 5) k_stats(StatsArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ unsigned long long s_err;
   __shared__ int s_min, s_max, s_last;
   const uint32_t tid = blockIdx.x;
+  TS1(0);
   const DTile T = a.tiles[tid];
   const DJob& J = a.jobs[T.job];
   // E2 scratch of this call starts clean
   if (threadIdx.x == 0) {
     a.tile_status[tid] = 0;
     a.edge_slot[tid] = 0;
-    if (tid == J.tile0) a.job_status[T.job * kJobStride] = 0;
+    if (tid == J.tile0) {  // job status word, payload-bit sum, sized-tile count
+      a.job_status[T.job * kJobStride] = 0;
+      a.job_status[T.job * kJobStride + 1] = 0;
+      a.job_status[T.job * kJobStride + 2] = 0;
+    }
     if (tid == 0) a.book.flags[CF_TICKET] = 0;
     s_err = ~0ull;
     s_min = INT_MAX;
@@ -485,6 +506,9 @@ __global__ void __launch_bounds__(kBlock) k_stats(StatsArgs a) {
       }
     }
   }
+  TS1(1);
+  TS1(3);
+  TS1(4);
   // fold the tile's failure key and code range into the job state
   JobState* Sp = &a.st[T.job];
   lerr = warp_min_u64(lerr);
@@ -521,6 +545,7 @@ __global__ void __launch_bounds__(kBlock) k_stats(StatsArgs a) {
       if (v) atomicAdd(&gh[b], v);
     }
   }
+  TS1(2);
   if (!huf) return;
   // the job's last tile to finish builds the codebook
   __threadfence();
@@ -529,7 +554,9 @@ __global__ void __launch_bounds__(kBlock) k_stats(StatsArgs a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  TS1(3);
   build_book(J, Sp, a.book, smem);
+  TS1(4);
 }
 
 // ---------------------------------------------------------------------------
@@ -558,6 +585,7 @@ struct EmitArgs {
   DevError* err;
   unsigned long long* d_stats;  // match_stats mode: (literals, references); no bytes
   uint32_t stage_off, aux_off;  // dynamic smem carve
+  uint32_t hash_cap, rows_cap;  // aux: staged row hashes | 5 per-row arrays
 };
 
 __device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
@@ -567,18 +595,6 @@ __device__ __forceinline__ unsigned long long ld_status(const unsigned long long
 // Warp-cooperative decoupled look-back: the exclusive prefix of element `i`
 // over status[first .. i-1], where status[first] always publishes an
 // inclusive value and `base` is the prefix before `first`.
-#ifdef EMBC_DEBUG
-__device__ unsigned long long g_dbg[8];
-__device__ unsigned long long g_ts[16384][6];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define TS(k) do { if (threadIdx.x == 0 && tid < 16384) g_ts[tid][k] = gtime(); } while (0)
-#else
-#define TS(k) do {} while (0)
-#endif
 
 __device__ __forceinline__ uint64_t look_back(const unsigned long long* status, uint32_t first, uint32_t i,
                                               uint64_t base, uint32_t stride = 1) {
@@ -647,7 +663,7 @@ __device__ __forceinline__ void copy_range(uint8_t* dst, const uint8_t* stage, u
   copy_out_staged(dst + a, stage + (mis + a - m2), b - a);
 }
 
-__global__ void __launch_bounds__(kBlock) k_emit(EmitArgs a) {
+__global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_tmp32[33];
   __shared__ unsigned long long s_tmp64[33];
@@ -737,25 +753,25 @@ __global__ void __launch_bounds__(kBlock) k_emit(EmitArgs a) {
   // ---- 2. tile size in bits (payload only; the header / codebook bytes are
   //         added at the job level)
   uint64_t my_bits = 0;
-  uint32_t* dec = reinterpret_cast<uint32_t*>(aux + kHashStage * 4);  // vlz: match offset per row
-  uint32_t* lits = dec + kMaxTileRows;                                  // vlz: token bytes per row
-  uint32_t* cand = lits + kMaxTileRows;                                 // vlz: candidate offset under test
-  uint32_t* plist = cand + kMaxTileRows;                                // vlz: rows with a pending candidate
-  uint32_t* miss = plist + kMaxTileRows;                                // vlz: candidate disproved
+  uint32_t* dec = reinterpret_cast<uint32_t*>(aux + a.hash_cap * 4);  // vlz: match offset per row
+  uint32_t* lits = dec + a.rows_cap;                                   // vlz: token bytes per row
+  uint32_t* cand = lits + a.rows_cap;                                  // vlz: candidate offset under test
+  uint32_t* plist = cand + a.rows_cap;                                 // vlz: rows with a pending candidate
+  uint32_t* miss = plist + a.rows_cap;                                 // vlz: candidate disproved
   uint32_t pos_thread = 0;                                              // huffman: this thread's first bit
   const uint32_t per_h = (ne + kBlock - 1) / kBlock;
   const uint64_t* L = a.lut + S.lut_off;
   uint64_t* sl = reinterpret_cast<uint64_t*>(aux);
   const int32_t cmin = S.cmin;
   const uint32_t span = codec == EMBC_CODEC_HUFFMAN ? static_cast<uint32_t>(S.cmax - cmin + 1) : 0;
-  const bool lut_staged = span <= kLutStage;
+  const bool lut_staged = span <= kLutStage && 8 * span <= a.hash_cap * 4 + a.rows_cap * 20;
   if (codec == EMBC_CODEC_RAW) {
     my_bits = 32ull * ne;
   } else if (codec == EMBC_CODEC_VLZ) {
     const uint32_t W = J.window;
     const uint32_t lo = T.row0 > W ? T.row0 - W : 0;
     const uint32_t nh = T.row0 + T.rows - lo;
-    const bool staged = nh <= kHashStage;
+    const bool staged = nh <= a.hash_cap;
     uint32_t* sh = reinterpret_cast<uint32_t*>(aux);
     const uint64_t* ri = a.row_info + J.row_base;
     if (staged)
@@ -898,6 +914,19 @@ __global__ void __launch_bounds__(kBlock) k_emit(EmitArgs a) {
   // ---- 3. offsets: look-back over the job's tiles (bits), then over jobs (bytes)
   const uint64_t hdr = J.header;
   const uint64_t book_bytes = codec == EMBC_CODEC_HUFFMAN ? 12 + 5ull * S.nsym : 0;
+  if (threadIdx.x == 0 && jid > 0) {
+    // the job's size is known once every tile of it is sized: the last one to
+    // get here publishes it, so later jobs never wait on this job's look-back
+    unsigned long long* js = a.job_status + jid * kJobStride;
+    atomicAdd(js + 1, static_cast<unsigned long long>(my_bits));
+    __threadfence();
+    if (atomicAdd(js + 2, 1ull) == J.ntiles - 1) {
+      __threadfence();
+      const unsigned long long bits = atomicAdd(js + 1, 0ull);
+      const unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(js);
+      if ((w >> 62) == 0) atomicCAS(js, 0ull, kFlagAgg | (hdr + book_bytes + (bits + 7) / 8));
+    }
+  }
   if (threadIdx.x < 32) {
     uint64_t pre = 0;
     if (first) {
@@ -910,7 +939,6 @@ __global__ void __launch_bounds__(kBlock) k_emit(EmitArgs a) {
     TS(3);
     const uint64_t job_bytes = hdr + book_bytes + (pre + my_bits + 7) / 8;
     const uint64_t base = a.layout == EMBC_LAYOUT_PACKED ? 4 + 16ull * a.njobs : 0;
-    if (last && jid > 0 && threadIdx.x == 0) st_status(a.job_status + jid * kJobStride, kFlagAgg | job_bytes);
     const uint64_t start = jid == 0 ? base : look_back(a.job_status, 0, jid, 0, kJobStride);
     if (last && threadIdx.x == 0) st_status(a.job_status + jid * kJobStride, kFlagInc | (start + job_bytes));
     TS(4);
@@ -980,6 +1008,22 @@ __global__ void __launch_bounds__(kBlock) k_emit(EmitArgs a) {
   if (threadIdx.x == 0 && atomicAdd(&g_dbg[2], 1ull) == a.ntiles - 1 && (g_dbg[2] = 0, a.ntiles > 1000) &&
       atomicAdd(&g_dbg[3], 1ull) % 8 == 7) {
     printf("k_emit: tiles %u tile-spins %llu job-spins %llu\n", a.ntiles, g_dbg[0], g_dbg[1]);
+    {
+      unsigned long long t0 = ~0ull, mxe = 0, sl = 0, ml = 0, sb = 0, mb = 0, nb = 0;
+      for (uint32_t t = 0; t < a.ntiles; ++t) t0 = min(t0, g_ts1[t][0]);
+      for (uint32_t t = 0; t < a.ntiles; ++t) {
+        mxe = max(mxe, g_ts1[t][4] - t0);
+        sl += g_ts1[t][1] - g_ts1[t][0];
+        ml = max(ml, g_ts1[t][1] - g_ts1[t][0]);
+        if (g_ts1[t][4] != g_ts1[t][3]) {
+          ++nb;
+          sb += g_ts1[t][4] - g_ts1[t][3];
+          mb = max(mb, g_ts1[t][4] - g_ts1[t][3]);
+        }
+      }
+      printf("k_stats: span %llu ns, tile main mean %llu max %llu, books %llu mean %llu max %llu ns\n", mxe,
+             sl / a.ntiles, ml, nb, nb ? sb / nb : 0, mb);
+    }
     g_dbg[0] = g_dbg[1] = 0;
     unsigned long long t0 = ~0ull;
     for (uint32_t t = 0; t < a.ntiles; ++t) t0 = min(t0, g_ts[t][0]);
@@ -1422,9 +1466,21 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   ea.d_total = d_total;
   ea.err = ctx->d_err;
   ea.d_stats = d_stats;
+  bool has_vlz = false, has_huf = false;
+  uint32_t wmax = 0;
+  for (uint32_t j = 0; j < njobs; ++j) {
+    has_vlz |= jobs[j].codec == EMBC_CODEC_VLZ;
+    has_huf |= jobs[j].codec == EMBC_CODEC_HUFFMAN;
+    if (jobs[j].codec == EMBC_CODEC_VLZ) wmax = std::max(wmax, jobs[j].window);
+  }
   ea.stage_off = emit_codes_bytes(vals_max, rows_max);
-  ea.aux_off = ea.stage_off + emit_stage_bytes(vals_max, rows_max);
-  const uint32_t emit_smem = ea.aux_off + kAuxBytes;
+  ea.aux_off = ea.stage_off + emit_stage_bytes(vals_max, rows_max, has_vlz);
+  ea.rows_cap = rows_max;
+  ea.hash_cap = has_vlz ? static_cast<uint32_t>(std::min<uint64_t>(kHashStage, static_cast<uint64_t>(wmax) + rows_max)) : 0;
+  uint32_t aux_bytes = ea.hash_cap * 4 + ea.rows_cap * 20;
+  if (has_huf) aux_bytes = std::max<uint32_t>(aux_bytes, 8 * kLutStage);
+  ea.hash_cap = (aux_bytes - ea.rows_cap * 20) / 4;  // any slack widens the hash stage
+  const uint32_t emit_smem = ea.aux_off + aux_bytes;
   EMBC_TIMED(ctx, "k_emit", stream, k_emit<<<ntiles, kBlock, emit_smem, stream>>>(ea));
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "encode launch");
