@@ -151,7 +151,9 @@ __device__ __forceinline__ int32_t unzigzag(uint32_t z) {
 }
 // bytes in the LEB128 encoding of a u32
 __device__ __forceinline__ uint32_t varint_len(uint32_t v) {
-  return 1u + (v >= (1u << 7)) + (v >= (1u << 14)) + (v >= (1u << 21)) + (v >= (1u << 28));
+  // ceil(bits / 7) for bits = significant bits of v (>= 1): ((bits + 6) * 37) >> 8 is exact for bits <= 32
+  const uint32_t bits = 32u - __clz(v | 1u);
+  return ((bits + 6u) * 37u) >> 8;
 }
 __device__ __forceinline__ uint8_t* put_varint(uint8_t* p, uint32_t v) {
   while (v >= 0x80u) {

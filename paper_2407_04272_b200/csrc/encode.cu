@@ -30,6 +30,22 @@
 
 namespace embc_dev {
 
+#ifdef EMBC_DEBUG
+__device__ unsigned long long g_dbg[8];
+__device__ unsigned long long g_ts[16384][6];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TS(k) do { if (threadIdx.x == 0 && tid < 16384) g_ts[tid][k] = gtime(); } while (0)
+__device__ unsigned long long g_ts1[16384][12];
+#define TS1(k) do { if (threadIdx.x == 0 && blockIdx.x < 16384) g_ts1[blockIdx.x][k] = gtime(); } while (0)
+#else
+#define TS(k) do {} while (0)
+#define TS1(k) do {} while (0)
+#endif
+
 constexpr uint32_t kTileVals = 4096;     // values per tile (whole rows): 3 CTAs of E2 per SM
 constexpr uint32_t kMaxRowVals = 8192;   // a single row (dim) may exceed kTileVals up to this
 constexpr uint32_t kMaxTileRows = 1024;  // rows per tile (bounds the per-row smem arrays)
@@ -73,17 +89,18 @@ __device__ __forceinline__ int32_t job_code(const DJob& J, uint64_t e, uint32_t*
   return __ldg(static_cast<const int32_t*>(J.src) + e);
 }
 
-// Row hash: a sum of per-element mixes, so partial sums combine in any order
-// (warp shuffles); equality is verified exactly (CodeRowEq, vlz.hpp:75-79),
+// Row hash: sum_j code_j * K(j) mod 2^32 with pseudo-random odd per-column
+// multipliers, so partial sums combine in any order (warp shuffles) at one
+// IMAD per element.  Equality is verified exactly (CodeRowEq, vlz.hpp:75-79),
 // so only the hit rate depends on the function.
-__device__ __forceinline__ uint32_t elem_mix(int32_t c, uint32_t col) {
-  uint32_t x = static_cast<uint32_t>(c) * 0x9E3779B1u ^ (col * 0x85EBCA77u + 0x165667B1u);
+__device__ __forceinline__ uint32_t col_key(uint32_t col) {
+  uint32_t x = col * 0x9E3779B1u + 0x7F4A7C15u;
   x ^= x >> 16;
   x *= 0x7FEB352Du;
   x ^= x >> 15;
   x *= 0x846CA68Bu;
   x ^= x >> 16;
-  return x;
+  return x | 1u;
 }
 
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
@@ -144,6 +161,202 @@ struct BookArgs {
   uint32_t* flags;      // call flags
 };
 
+// Warp-level bitonic sort of p2 keys in shared memory.
+__device__ __forceinline__ void warp_bitonic(uint64_t* key, uint32_t p2) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t k = 2; k <= p2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = lane; i < p2; i += 32) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t x = key[i], y = key[ixj];
+          if ((x > y) == ((i & k) == 0)) {
+            key[i] = y;
+            key[ixj] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Ascending bitonic sort of 32*K keys held in registers across one warp:
+// element (r, lane) is position r*32 + lane.
+template <int K>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[K]) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (uint32_t k = 2; k <= 32u * K; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const int r2 = r ^ static_cast<int>(j >> 5);
+          if (r2 > r) {
+            const uint32_t i = static_cast<uint32_t>(r) * 32 + lane;
+            const bool up = (i & k) == 0;
+            const uint64_t x = v[r], y = v[r2];
+            if ((x > y) == up) {
+              v[r] = y;
+              v[r2] = x;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const uint32_t i = static_cast<uint32_t>(r) * 32 + lane;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[r], j);
+          const bool up = (i & k) == 0;
+          const bool lower = (lane & j) == 0;  // this lane holds the smaller index of the pair
+          // lower keeps min when ascending, max when descending; the upper the opposite
+          const bool keep_min = (lower == up);
+          v[r] = keep_min ? (v[r] < o ? v[r] : o) : (v[r] > o ? v[r] : o);
+        }
+      }
+    }
+  }
+}
+
+// Sort p2 (<= 256) keys of shared memory with one warp, through registers.
+__device__ __forceinline__ void warp_sort_smem(uint64_t* key, uint32_t p2) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (p2 <= 32) {
+    uint64_t v[1] = {lane < p2 ? key[lane] : ~0ull};
+    warp_sort_regs<1>(v);
+    if (lane < p2) key[lane] = v[0];
+  } else if (p2 <= 64) {
+    uint64_t v[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) v[r] = key[r * 32 + lane];
+    warp_sort_regs<2>(v);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) key[r * 32 + lane] = v[r];
+  } else if (p2 <= 128) {
+    uint64_t v[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) v[r] = key[r * 32 + lane];
+    warp_sort_regs<4>(v);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) key[r * 32 + lane] = v[r];
+  } else {
+    uint64_t v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = key[r * 32 + lane];
+    warp_sort_regs<8>(v);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) key[r * 32 + lane] = v[r];
+  }
+  __syncwarp();
+}
+
+// Codebook of an alphabet of <= 256 symbols by one warp: the same steps as the
+// block version below (huffman.hpp:49-120 lengths, :165-186 canonical codes).
+__device__ void book_warp(const DJob& J, JobState* Sp, const BookArgs& a, uint64_t* key, uint64_t* wgt,
+                          int32_t* parent, uint32_t nsym, uint32_t p2, uint32_t* gh, uint64_t span, int32_t cmin,
+                          uint64_t* L, uint8_t* book, uint64_t lut_off) {
+  const uint32_t lane = threadIdx.x & 31;
+  // 2. leaves sorted by (count, symbol) (huffman.hpp:74-77)
+  if (nsym > 1) warp_sort_smem(key, p2);
+  TS1(8);
+  // 3. two-queue merge, leaf queue preferred on ties (huffman.hpp:91-109)
+  for (uint32_t i = lane; i < nsym; i += 32) wgt[i] = key[i] >> 32;
+  __syncwarp();
+  if (nsym > 1 && lane == 0) {
+    // the merged queue's weights are created in non-decreasing order; its head
+    // and the leaf head are kept in registers, the next leaf prefetched
+    const uint32_t n = nsym, total = 2 * n - 1;
+    uint32_t size = n, lh = 0, mh = n;
+    uint64_t wl = wgt[0], wl_next = n > 1 ? wgt[1] : 0, wm = 0;
+    while (size < total) {
+      uint32_t ab[2];
+      uint64_t w2 = 0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (lh < n && (mh >= size || wl <= wm)) {
+          ab[k] = lh++;
+          w2 += wl;
+          wl = wl_next;
+          wl_next = lh + 1 < n ? wgt[lh + 1] : 0;
+        } else {
+          ab[k] = mh++;
+          w2 += wm;
+          wm = mh < size ? wgt[mh] : 0;
+        }
+      }
+      wgt[size] = w2;
+      if (mh == size) wm = w2;  // the new node is the merged head
+      parent[ab[0]] = static_cast<int32_t>(size);
+      parent[ab[1]] = static_cast<int32_t>(size);
+      ++size;
+    }
+    parent[total - 1] = -1;
+  }
+  __syncwarp();
+  TS1(9);
+  // 4. lengths = leaf depth; the first leaf (sorted order) past 32 bits fails (huffman.hpp:110-118)
+  unsigned long long cap = ~0ull;
+  for (uint32_t i = lane; i < nsym; i += 32) {
+    uint32_t depth = 0;
+    if (nsym == 1) depth = 1;
+    else
+      for (int32_t q = parent[i]; q != -1; q = parent[q]) ++depth;
+    if (depth > 32) cap = min(cap, (static_cast<unsigned long long>(i) << 32) | depth);
+    key[i] = (static_cast<uint64_t>(depth > 32 ? 63 : depth) << 32) | (key[i] & 0xFFFFFFFFull);
+  }
+  cap = warp_min_u64(cap);
+  if (cap != ~0ull) {
+    if (lane == 0) {
+      Sp->aux = cap & 0xFFFFFFFFull;
+      atomicMin(reinterpret_cast<unsigned long long*>(&Sp->err), err_key(cap >> 32, EMBC_R_HUF_LEN_CAP) | (1ull << 63));
+      atomicOr(&a.flags[CF_ABORT], JF_ABORT);
+    }
+    for (uint64_t b = lane; b < span; b += 32) gh[b] = 0;
+    return;
+  }
+  __syncwarp();
+  TS1(10);
+  // 5. canonical order (length asc, symbol asc)
+  if (nsym > 1) warp_sort_smem(key, p2);
+  TS1(11);
+  // 6. canonical codes: code_i = sum_{j<i} 2^(len_i - len_j) (finalize, huffman.hpp:170-181)
+  unsigned long long carry = 0, bits = 0;
+  for (uint32_t i0 = 0; i0 < nsym; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    uint32_t len = 0, symoff = 0;
+    unsigned long long kraft = 0;
+    if (i < nsym) {
+      len = static_cast<uint32_t>(key[i] >> 32);
+      symoff = static_cast<uint32_t>(key[i]);
+      kraft = 1ull << (32 - len);
+    }
+    const unsigned long long inc = warp_incl_scan<unsigned long long>(kraft);
+    if (i < nsym) {
+      const uint64_t prefix = carry + inc - kraft;
+      const uint32_t cw = static_cast<uint32_t>(prefix >> (32 - len));
+      L[symoff] = (static_cast<uint64_t>(cw) << 8) | len;
+      uint8_t* e = book + 12 + 5ull * i;
+      st_be(e, static_cast<uint32_t>(static_cast<int32_t>(static_cast<int64_t>(cmin) + symoff)), 4);
+      e[4] = static_cast<uint8_t>(len);
+      bits += static_cast<unsigned long long>(__ldcg(gh + symoff)) * len;
+    }
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  bits = warp_sum<unsigned long long>(bits);
+  __syncwarp();
+  for (uint64_t b = lane; b < span; b += 32) gh[b] = 0;  // clean for the next call
+  if (lane == 0) {
+    st_be(book, J.N, 8);       // u64be symbol_count (huffman.hpp:203)
+    st_be(book + 8, nsym, 4);  // u32be entry_count (huffman.hpp:204)
+    Sp->nsym = nsym;
+    Sp->bits = bits;
+    Sp->lut_off = lut_off;
+    Sp->payload = 12 + 5ull * nsym + (bits + 7) / 8;
+  }
+}
+
 __device__ void build_book(const DJob& J, JobState* Sp, const BookArgs& a, uint8_t* smem) {
   __shared__ uint32_t s_tmp32[33];
   __shared__ unsigned long long s_tmp64[33];
@@ -169,6 +382,7 @@ __device__ void build_book(const DJob& J, JobState* Sp, const BookArgs& a, uint8
     }
     return;
   }
+  TS1(5);
   const int32_t cmin = s_cmin;
   const uint64_t span = static_cast<uint64_t>(static_cast<int64_t>(s_cmax) - cmin + 1);
   uint32_t* gh;
@@ -211,6 +425,7 @@ __device__ void build_book(const DJob& J, JobState* Sp, const BookArgs& a, uint8
   uint32_t cnt = 0;
   for (uint64_t b = threadIdx.x; b < span; b += blockDim.x) cnt += __ldcg(gh + b) != 0;
   const uint32_t nsym = block_sum<uint32_t>(cnt, s_tmp32);
+  TS1(6);
   uint32_t p2 = 1;
   while (p2 < nsym) p2 <<= 1;
   const bool in_smem = p2 <= kSmemBook;
@@ -232,6 +447,11 @@ __device__ void build_book(const DJob& J, JobState* Sp, const BookArgs& a, uint8
   __syncthreads();
   uint8_t* book = a.books + hj * a.book_stride;
   uint64_t* L = a.lut + lut_off;
+  TS1(7);
+  if (p2 <= 256 && in_smem) {  // small alphabets: one warp, no block barriers
+    if (threadIdx.x < 32) book_warp(J, Sp, a, key, wgt, parent, nsym, p2, gh, span, cmin, L, book, lut_off);
+    return;
+  }
   // 2. leaves sorted by (count, symbol): stable_sort (huffman.hpp:74-77)
   if (nsym > 1) bitonic_sort(key, p2);
   // 3. two-queue merge, leaf queue preferred on ties (huffman.hpp:91-109)
@@ -332,21 +552,6 @@ __device__ void build_book(const DJob& J, JobState* Sp, const BookArgs& a, uint8
   }
 }
 
-#ifdef EMBC_DEBUG
-__device__ unsigned long long g_dbg[8];
-__device__ unsigned long long g_ts[16384][6];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define TS(k) do { if (threadIdx.x == 0 && tid < 16384) g_ts[tid][k] = gtime(); } while (0)
-__device__ unsigned long long g_ts1[16384][6];
-#define TS1(k) do { if (threadIdx.x == 0 && blockIdx.x < 16384) g_ts1[blockIdx.x][k] = gtime(); } while (0)
-#else
-#define TS(k) do {} while (0)
-#define TS1(k) do {} while (0)
-#endif
 
 // ---------------------------------------------------------------------------
 // E1: quantize + per-tile statistics (+ codebook tail)
@@ -408,6 +613,10 @@ __global__ void __launch_bounds__(kBlock, 5) k_stats(StatsArgs a) {
     const QParams qp = J.qp;
     const bool f32 = J.src_kind == EMBC_SRC_F32;
     const uint4* src4 = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(J.src) + e0);
+    uint32_t ck[4] = {0, 0, 0, 0};  // this thread's columns are fixed: q % qpr == threadIdx.x % qpr
+    if (vlz)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ck[k] = col_key((threadIdx.x & (qpr - 1)) * 4 + k);
     for (uint32_t base = 0; base < nq; base += 4 * kBlock) {
       uint4 v[4];
 #pragma unroll
@@ -431,8 +640,10 @@ __global__ void __launch_bounds__(kBlock, 5) k_stats(StatsArgs a) {
             } else {
               c[k] = static_cast<int32_t>(w[k]);
             }
-            lmin = min(lmin, c[k]);
-            lmax = max(lmax, c[k]);
+            if (huf) {
+              lmin = min(lmin, c[k]);
+              lmax = max(lmax, c[k]);
+            }
           }
         }
         if (huf) {
@@ -448,11 +659,10 @@ __global__ void __launch_bounds__(kBlock, 5) k_stats(StatsArgs a) {
           }
         }
         if (vlz) {
-          const uint32_t col = (q & (qpr - 1)) * 4;
           uint32_t h = 0, lit = 0;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            h += elem_mix(c[k], col + k);
+            h += static_cast<uint32_t>(c[k]) * ck[k];
             lit += varint_len(zigzag(c[k]));
           }
           for (uint32_t o = 1; o < qpr; o <<= 1) {
@@ -499,7 +709,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_stats(StatsArgs a) {
         const int32_t* row = codes + r * stride;
         uint32_t h = 0, lit = 1;
         for (uint32_t j = 0; j < dim; ++j) {
-          h += elem_mix(row[j], j);
+          h += static_cast<uint32_t>(row[j]) * col_key(j);
           lit += varint_len(zigzag(row[j]));
         }
         a.row_info[gbase + r] = (static_cast<uint64_t>(lit) << 32) | h;
@@ -586,6 +796,12 @@ struct EmitArgs {
   unsigned long long* d_stats;  // match_stats mode: (literals, references); no bytes
   uint32_t stage_off, aux_off;  // dynamic smem carve
   uint32_t hash_cap, rows_cap;  // aux: staged row hashes | 5 per-row arrays
+  uint32_t* row_dec;            // vlz: match offset per row (phase 0 -> phase 1)
+  uint64_t* tile_bits;          // payload bits per tile (phase 0)
+  uint64_t* tile_off;           // bit offset of each tile inside its job's payload data (layout)
+  uint64_t* job_start;          // chunk offset of each job (layout)
+  uint32_t* done;               // phase-0 completion ticket
+  int phase;                    // 0: sizes + layout (last CTA), 1: bytes
 };
 
 __device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
@@ -663,20 +879,115 @@ __device__ __forceinline__ void copy_range(uint8_t* dst, const uint8_t* stage, u
   copy_out_staged(dst + a, stage + (mis + a - m2), b - a);
 }
 
+// Layout of the call (the last phase-0 CTA): tile offsets inside each job's
+// payload (bits), chunk offsets in job order (container.hpp:245-250), chunk
+// headers (container.hpp:74-85), pack table (container.hpp:244-250), 25-B
+// metadata (container.hpp:196-209), capacity check.
+__device__ void layout_tail(const EmitArgs& a) {
+  __shared__ unsigned long long s_tmp64[33];
+  // 1. exclusive prefix of the tile bits over all tiles
+  unsigned long long carry = 0;
+  for (uint32_t t0 = 0; t0 < a.ntiles; t0 += blockDim.x) {
+    const uint32_t t = t0 + threadIdx.x;
+    const unsigned long long v = t < a.ntiles ? __ldcg(a.tile_bits + t) : 0;
+    unsigned long long tot;
+    const unsigned long long pre = block_excl_scan<unsigned long long>(v, s_tmp64, &tot);
+    if (t < a.ntiles) a.tile_off[t] = carry + pre;
+    carry += tot;
+  }
+  __threadfence_block();
+  __syncthreads();
+  // 2. relative to each job's first tile (the job's prefix parked in job_start)
+  for (uint32_t j = threadIdx.x; j < a.njobs; j += blockDim.x) a.job_start[j] = __ldcg(a.tile_off + a.jobs[j].tile0);
+  __threadfence_block();
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < a.ntiles; t += blockDim.x)
+    a.tile_off[t] = __ldcg(a.tile_off + t) - __ldcg(a.job_start + a.tiles[t].job);
+  __threadfence_block();
+  __syncthreads();
+  // 3. chunk sizes -> offsets in job order, then the per-chunk records
+  const uint64_t base = a.layout == EMBC_LAYOUT_PACKED ? 4 + 16ull * a.njobs : 0;
+  carry = base;
+  for (uint32_t j0 = 0; j0 < a.njobs; j0 += blockDim.x) {
+    const uint32_t j = j0 + threadIdx.x;
+    uint64_t P = 0, len = 0;
+    if (j < a.njobs) {
+      const DJob& J = a.jobs[j];
+      const uint32_t lt = J.tile0 + J.ntiles - 1;
+      const uint64_t bits = __ldcg(a.tile_off + lt) + __ldcg(a.tile_bits + lt);
+      P = (J.codec == EMBC_CODEC_HUFFMAN ? 12 + 5ull * a.st[j].nsym : 0) + (bits + 7) / 8;
+      len = J.header + P;
+    }
+    unsigned long long tot;
+    const unsigned long long pre = block_excl_scan<unsigned long long>(len, s_tmp64, &tot);
+    if (j < a.njobs) {
+      const DJob& J = a.jobs[j];
+      const uint64_t start = carry + pre;
+      a.job_start[j] = start;
+      if (a.d_offsets) a.d_offsets[j] = start;
+      if (a.d_lengths) a.d_lengths[j] = len;
+      if (a.layout == EMBC_LAYOUT_PACKED && 20 + 16ull * j <= a.cap) {
+        st_le(a.out + 4 + 16ull * j, start, 8);
+        st_le(a.out + 12 + 16ull * j, len, 8);
+      }
+      uint64_t ebits;
+      memcpy(&ebits, &J.qp.eb, 8);
+      if (J.header && start + kHeader <= a.cap) {
+        uint8_t* h = a.out + start;
+        h[0] = 'E';
+        h[1] = 'M';
+        h[2] = 'B';
+        h[3] = 'C';
+        h[4] = 1;
+        h[5] = J.codec;
+        st_le(h + 6, ebits, 8);
+        st_le(h + 14, J.dim, 4);
+        st_le(h + 18, J.n, 4);
+        st_le(h + 22, P, 8);
+      }
+      if (a.d_meta) {
+        uint8_t* m = a.d_meta + static_cast<uint64_t>(kMetaSize) * j;
+        st_le(m, kHeader + P, 8);
+        m[8] = J.codec;
+        st_le(m + 9, ebits, 8);
+        st_le(m + 17, J.dim, 4);
+        st_le(m + 21, J.n, 4);
+      }
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    const uint64_t total = carry;
+    if (a.layout == EMBC_LAYOUT_PACKED && a.cap >= 4) st_le(a.out, a.njobs, 4);
+    if (total > a.cap) {
+      if (a.d_total) *a.d_total = 0;
+      a.flags[CF_ABORT] |= JF_ABORT;  // phase 1 writes nothing
+      if (!a.err->valid) {
+        a.err->valid = 1;
+        a.err->job = 0;
+        a.err->reason = EMBC_R_CAPACITY;
+        a.err->index = 0;
+        a.err->a = total;
+        a.err->b = a.cap;
+        a.err->status = EMBC_ERR_CAPACITY;
+      }
+    } else if (a.d_total) {
+      *a.d_total = total;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_tmp32[33];
   __shared__ unsigned long long s_tmp64[33];
-  __shared__ uint32_t s_t;
-  __shared__ unsigned long long s_pre, s_start;
-  if (threadIdx.x == 0) s_t = atomicAdd(&a.flags[CF_TICKET], 1u);
-  __syncthreads();
-  const uint32_t tid = s_t;  // tiles are processed in ticket order: look-back never waits on a later CTA
+  const uint32_t tid = blockIdx.x;
   TS(0);
-  if (a.flags[CF_ABORT] & JF_ABORT) {
-    if (tid == 0 && !a.d_stats) fold_failure(a);
+  if (*reinterpret_cast<volatile uint32_t*>(&a.flags[CF_ABORT]) & JF_ABORT) {
+    if (tid == 0 && a.phase == 0 && !a.d_stats) fold_failure(a);
     return;
   }
+  const int phase = a.phase;
   const DTile T = a.tiles[tid];
   const uint32_t jid = T.job;
   const DJob& J = a.jobs[jid];
@@ -691,6 +1002,21 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
   const uint32_t codec = J.codec;
   const uint32_t stride = codec == EMBC_CODEC_VLZ ? (dim | 1u) : 0;
 
+  uint32_t* dec = reinterpret_cast<uint32_t*>(aux + a.hash_cap * 4);  // vlz: match offset per row
+  uint32_t* lits = dec + a.rows_cap;                                   // vlz: token bytes per row
+  uint32_t* cand = lits + a.rows_cap;                                  // vlz: candidate offset under test
+  uint32_t* plist = cand + a.rows_cap;                                 // vlz: rows with a pending candidate
+  uint32_t* miss = plist + a.rows_cap;                                 // vlz: candidate disproved
+  const bool vlz_lit_only = phase == 1 && codec == EMBC_CODEC_VLZ;     // phase 1 needs literal rows only
+  if (vlz_lit_only) {
+    const uint64_t* ri = a.row_info + J.row_base + T.row0;
+    for (uint32_t r = threadIdx.x; r < T.rows; r += kBlock) {
+      const uint32_t o = a.row_dec[J.row_base + T.row0 + r];
+      dec[r] = o;
+      lits[r] = o ? 1u + varint_len(o) : static_cast<uint32_t>(__ldg(ri + r) >> 32);
+    }
+    __syncthreads();
+  }
   // ---- 1. codes of the tile into shared memory (vlz: row stride dim|1;
   //         huffman: l + l/32, conflict-free thread-contiguous reads)
   if (codec != EMBC_CODEC_RAW && ne) {
@@ -704,12 +1030,12 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t q = base + u * kBlock + threadIdx.x;
-          if (q < nq) v[u] = __ldg(src4 + q);
+          if (q < nq && !(vlz_lit_only && dec[fdiv(4 * q, J.fd)])) v[u] = __ldg(src4 + q);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t q = base + u * kBlock + threadIdx.x;
-          if (q >= nq) continue;
+          if (q >= nq || (vlz_lit_only && dec[fdiv(4 * q, J.fd)])) continue;
           const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -734,16 +1060,17 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
       }
     } else {
       for (uint32_t l = threadIdx.x; l < ne; l += kBlock) {
-        uint32_t r = 0;
-        const int32_t c = job_code(J, e0 + l, &r);
         uint32_t at;
+        uint32_t rr = 0;
         if (stride) {
-          const uint32_t rr = fdiv(l, J.fd);
+          rr = fdiv(l, J.fd);
           at = rr * stride + (l - rr * dim);
+          if (vlz_lit_only && dec[rr]) continue;
         } else {
           at = l + (l >> 5);
         }
-        codes[at] = c;
+        uint32_t r = 0;
+        codes[at] = job_code(J, e0 + l, &r);
       }
     }
   }
@@ -753,11 +1080,6 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
   // ---- 2. tile size in bits (payload only; the header / codebook bytes are
   //         added at the job level)
   uint64_t my_bits = 0;
-  uint32_t* dec = reinterpret_cast<uint32_t*>(aux + a.hash_cap * 4);  // vlz: match offset per row
-  uint32_t* lits = dec + a.rows_cap;                                   // vlz: token bytes per row
-  uint32_t* cand = lits + a.rows_cap;                                  // vlz: candidate offset under test
-  uint32_t* plist = cand + a.rows_cap;                                 // vlz: rows with a pending candidate
-  uint32_t* miss = plist + a.rows_cap;                                 // vlz: candidate disproved
   uint32_t pos_thread = 0;                                              // huffman: this thread's first bit
   const uint32_t per_h = (ne + kBlock - 1) / kBlock;
   const uint64_t* L = a.lut + S.lut_off;
@@ -767,6 +1089,10 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
   const bool lut_staged = span <= kLutStage && 8 * span <= a.hash_cap * 4 + a.rows_cap * 20;
   if (codec == EMBC_CODEC_RAW) {
     my_bits = 32ull * ne;
+  } else if (codec == EMBC_CODEC_VLZ && phase == 1) {
+    uint64_t local = 0;
+    for (uint32_t r = threadIdx.x; r < T.rows; r += kBlock) local += lits[r];
+    my_bits = 8ull * block_sum<unsigned long long>(local, s_tmp64);
   } else if (codec == EMBC_CODEC_VLZ) {
     const uint32_t W = J.window;
     const uint32_t lo = T.row0 > W ? T.row0 - W : 0;
@@ -885,6 +1211,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
       lits[r] = sz;
       local += sz;
       nref += found != 0;
+      a.row_dec[J.row_base + T.row0 + r] = found;
     }
     if (a.d_stats) {  // match_stats (vlz.hpp:162-168)
       nref = block_sum<unsigned long long>(nref, s_tmp64);
@@ -911,128 +1238,48 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
   }
 
   TS(2);
-  // ---- 3. offsets: look-back over the job's tiles (bits), then over jobs (bytes)
   const uint64_t hdr = J.header;
   const uint64_t book_bytes = codec == EMBC_CODEC_HUFFMAN ? 12 + 5ull * S.nsym : 0;
-  if (threadIdx.x == 0 && jid > 0) {
-    // the job's size is known once every tile of it is sized: the last one to
-    // get here publishes it, so later jobs never wait on this job's look-back
-    unsigned long long* js = a.job_status + jid * kJobStride;
-    atomicAdd(js + 1, static_cast<unsigned long long>(my_bits));
+  if (phase == 0) {
+    // ---- 3a. sizes out; the last CTA to finish lays the call out
+    __shared__ int s_last;
+    if (threadIdx.x == 0) a.tile_bits[tid] = my_bits;
     __threadfence();
-    if (atomicAdd(js + 2, 1ull) == J.ntiles - 1) {
-      __threadfence();
-      const unsigned long long bits = atomicAdd(js + 1, 0ull);
-      const unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(js);
-      if ((w >> 62) == 0) atomicCAS(js, 0ull, kFlagAgg | (hdr + book_bytes + (bits + 7) / 8));
-    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    layout_tail(a);
+    return;
   }
-  if (threadIdx.x < 32) {
-    uint64_t pre = 0;
-    if (first) {
-      if (threadIdx.x == 0) st_status(a.tile_status + tid, kFlagInc | my_bits);
-    } else {
-      if (threadIdx.x == 0) st_status(a.tile_status + tid, kFlagAgg | my_bits);
-      pre = look_back(a.tile_status, J.tile0, tid, 0);
-      if (threadIdx.x == 0) st_status(a.tile_status + tid, kFlagInc | (pre + my_bits));
-    }
-    TS(3);
-    const uint64_t job_bytes = hdr + book_bytes + (pre + my_bits + 7) / 8;
-    const uint64_t base = a.layout == EMBC_LAYOUT_PACKED ? 4 + 16ull * a.njobs : 0;
-    const uint64_t start = jid == 0 ? base : look_back(a.job_status, 0, jid, 0, kJobStride);
-    if (last && threadIdx.x == 0) st_status(a.job_status + jid * kJobStride, kFlagInc | (start + job_bytes));
-    TS(4);
-    if (threadIdx.x == 0) {
-      s_pre = pre;
-      s_start = start;
-    }
-  }
-  __syncthreads();
-  const uint64_t pre = s_pre, start = s_start;
-  const uint64_t pay_end = start + hdr + book_bytes + (pre + my_bits + 7) / 8;  // end of this job's bytes so far
+  // ---- 3b. offsets from the layout
+  if (*reinterpret_cast<volatile uint32_t*>(&a.flags[CF_ABORT]) & JF_ABORT) return;  // capacity
+  const uint64_t pre = a.tile_off[tid], start = a.job_start[jid];
+  const uint64_t pay_end = start + hdr + book_bytes + (pre + my_bits + 7) / 8;  // end of this tile's bytes
   uint8_t* pay = a.out + start + hdr;
-
-  // ---- 4. job-level records by the job's last tile (header, pack table, metadata)
-  if (last && threadIdx.x == 0) {
-    const uint64_t P = book_bytes + (pre + my_bits + 7) / 8;
-    const uint64_t len = hdr + P;
-    if (a.d_offsets) a.d_offsets[jid] = start;
-    if (a.d_lengths) a.d_lengths[jid] = len;
-    if (a.layout == EMBC_LAYOUT_PACKED && 20 + 16ull * jid <= a.cap) {  // pack table (container.hpp:244-250)
-      st_le(a.out + 4 + 16ull * jid, start, 8);
-      st_le(a.out + 12 + 16ull * jid, len, 8);
-    }
-    uint64_t ebits;
-    memcpy(&ebits, &J.qp.eb, 8);
-    if (hdr && start + kHeader <= a.cap) {  // serialize_chunk header (container.hpp:74-85)
-      uint8_t* h = a.out + start;
-      h[0] = 'E';
-      h[1] = 'M';
-      h[2] = 'B';
-      h[3] = 'C';
-      h[4] = 1;
-      h[5] = J.codec;
-      st_le(h + 6, ebits, 8);
-      st_le(h + 14, J.dim, 4);
-      st_le(h + 18, J.n, 4);
-      st_le(h + 22, P, 8);
-    }
-    if (a.d_meta) {  // serialize_metadata(metadata_for(chunk)) (container.hpp:196-209)
-      uint8_t* m = a.d_meta + static_cast<uint64_t>(kMetaSize) * jid;
-      st_le(m, kHeader + P, 8);
-      m[8] = J.codec;
-      st_le(m + 9, ebits, 8);
-      st_le(m + 17, J.dim, 4);
-      st_le(m + 21, J.n, 4);
-    }
-    if (tid == a.ntiles - 1) {  // the call's last byte
-      const uint64_t total = start + len;
-      if (total > a.cap) {
-        if (a.d_total) *a.d_total = 0;
-        if (!a.err->valid) {
-          a.err->valid = 1;
-          a.err->job = 0;
-          a.err->reason = EMBC_R_CAPACITY;
-          a.err->index = 0;
-          a.err->a = total;
-          a.err->b = a.cap;
-          a.err->status = EMBC_ERR_CAPACITY;
-        }
-      } else if (a.d_total) {
-        *a.d_total = total;
-      }
-    }
-  }
-  if (tid == 0 && threadIdx.x == 0 && a.layout == EMBC_LAYOUT_PACKED && a.cap >= 4) st_le(a.out, a.njobs, 4);
 #ifdef EMBC_DEBUG
   if (threadIdx.x == 0 && atomicAdd(&g_dbg[2], 1ull) == a.ntiles - 1 && (g_dbg[2] = 0, a.ntiles > 1000) &&
       atomicAdd(&g_dbg[3], 1ull) % 8 == 7) {
-    printf("k_emit: tiles %u tile-spins %llu job-spins %llu\n", a.ntiles, g_dbg[0], g_dbg[1]);
-    {
-      unsigned long long t0 = ~0ull, mxe = 0, sl = 0, ml = 0, sb = 0, mb = 0, nb = 0;
-      for (uint32_t t = 0; t < a.ntiles; ++t) t0 = min(t0, g_ts1[t][0]);
-      for (uint32_t t = 0; t < a.ntiles; ++t) {
-        mxe = max(mxe, g_ts1[t][4] - t0);
-        sl += g_ts1[t][1] - g_ts1[t][0];
-        ml = max(ml, g_ts1[t][1] - g_ts1[t][0]);
-        if (g_ts1[t][4] != g_ts1[t][3]) {
-          ++nb;
-          sb += g_ts1[t][4] - g_ts1[t][3];
-          mb = max(mb, g_ts1[t][4] - g_ts1[t][3]);
-        }
+    unsigned long long t0 = ~0ull, mxe = 0, sl = 0, ml = 0, sb = 0, mb = 0, nb = 0;
+    for (uint32_t t = 0; t < a.ntiles; ++t) t0 = min(t0, g_ts1[t][0]);
+    for (uint32_t t = 0; t < a.ntiles; ++t) {
+      mxe = max(mxe, g_ts1[t][4] - t0);
+      sl += g_ts1[t][1] - g_ts1[t][0];
+      ml = max(ml, g_ts1[t][1] - g_ts1[t][0]);
+      if (g_ts1[t][4] != g_ts1[t][3]) {
+        ++nb;
+        sb += g_ts1[t][4] - g_ts1[t][3];
+        mb = max(mb, g_ts1[t][4] - g_ts1[t][3]);
       }
-      printf("k_stats: span %llu ns, tile main mean %llu max %llu, books %llu mean %llu max %llu ns\n", mxe,
-             sl / a.ntiles, ml, nb, nb ? sb / nb : 0, mb);
     }
-    g_dbg[0] = g_dbg[1] = 0;
-    unsigned long long t0 = ~0ull;
-    for (uint32_t t = 0; t < a.ntiles; ++t) t0 = min(t0, g_ts[t][0]);
-    for (uint32_t j = 0; j < a.njobs; ++j) {
-      unsigned long long mn[5] = {~0ull, ~0ull, ~0ull, ~0ull, ~0ull}, mx[5] = {0, 0, 0, 0, 0};
-      for (uint32_t t = a.jobs[j].tile0; t < a.jobs[j].tile0 + a.jobs[j].ntiles; ++t)
-        for (int k = 0; k < 5; ++k) { mn[k] = min(mn[k], g_ts[t][k] - t0); mx[k] = max(mx[k], g_ts[t][k] - t0); }
-      printf("job %2u codec %u start [%6llu %6llu] loaded [%6llu %6llu] sized [%6llu %6llu] tilelb [%6llu %6llu] joblb [%6llu %6llu] ns\n",
-             j, a.jobs[j].codec, mn[0], mx[0], mn[1], mx[1], mn[2], mx[2], mn[3], mx[3], mn[4], mx[4]);
+    printf("k_stats: span %llu ns, tile main mean %llu max %llu, books %llu mean %llu max %llu ns\n", mxe,
+           sl / a.ntiles, ml, nb, nb ? sb / nb : 0, mb);
+    for (uint32_t t = 0; t < a.ntiles; ++t) {
+      if (g_ts1[t][4] - g_ts1[t][3] != mb) continue;
+      const unsigned long long* g = g_ts1[t];
+      printf("  slowest book: S %llu count %llu compact %llu sort %llu merge %llu depth %llu csort %llu rest %llu\n",
+             g[5] - g[3], g[6] - g[5], g[7] - g[6], g[8] - g[7], g[9] - g[8], g[10] - g[9], g[11] - g[10], g[4] - g[11]);
     }
   }
 #endif
@@ -1379,6 +1626,10 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   const size_t o_tstat = cv.take<unsigned long long>(ntiles + 1);
   const size_t o_jstat = cv.take<unsigned long long>(kJobStride * (njobs + 1), 128);
   const size_t o_slot = cv.take<uint32_t>(ntiles + 1);
+  const size_t o_rdec = cv.take<uint32_t>(total_rows + 1);
+  const size_t o_tbits = cv.take<uint64_t>(ntiles + 1);
+  const size_t o_toff = cv.take<uint64_t>(ntiles + 1);
+  const size_t o_jstart = cv.take<uint64_t>(njobs + 1);
   hist_entries += kWidePool;  // [nhuff windows | wide pool], LUT mirrors the layout
   const size_t o_lut = cv.take<uint64_t>(hist_entries + 1);
   const size_t o_books = cv.take<uint8_t>(book_stride * std::max<uint32_t>(nhuff, 1));
@@ -1481,7 +1732,17 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   if (has_huf) aux_bytes = std::max<uint32_t>(aux_bytes, 8 * kLutStage);
   ea.hash_cap = (aux_bytes - ea.rows_cap * 20) / 4;  // any slack widens the hash stage
   const uint32_t emit_smem = ea.aux_off + aux_bytes;
-  EMBC_TIMED(ctx, "k_emit", stream, k_emit<<<ntiles, kBlock, emit_smem, stream>>>(ea));
+  ea.row_dec = reinterpret_cast<uint32_t*>(d + o_rdec);
+  ea.tile_bits = reinterpret_cast<uint64_t*>(d + o_tbits);
+  ea.tile_off = reinterpret_cast<uint64_t*>(d + o_toff);
+  ea.job_start = reinterpret_cast<uint64_t*>(d + o_jstart);
+  ea.done = sa.book.flags + CF_TICKET;  // zeroed by k_stats
+  ea.phase = 0;
+  EMBC_TIMED(ctx, "k_sizes", stream, k_emit<<<ntiles, kBlock, emit_smem, stream>>>(ea));
+  if (!d_stats) {
+    ea.phase = 1;
+    EMBC_TIMED(ctx, "k_emit", stream, k_emit<<<ntiles, kBlock, emit_smem, stream>>>(ea));
+  }
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "encode launch");
   return EMBC_OK;
