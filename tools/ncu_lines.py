@@ -3,7 +3,8 @@ usage: python tools/ncu_lines.py <report> <kernel-regex> [topN]"""
 import csv, io, subprocess, sys
 rep, k = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", "regex:" + k, "--print-source", "cuda,sass"],
+extra = ["--launch-skip", sys.argv[4], "--launch-count", "1"] if len(sys.argv) > 4 else []
+raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", "regex:" + k, "--print-source", "cuda,sass"] + extra,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 fname, cur, agg, tot = None, None, {}, 0
