@@ -409,7 +409,7 @@ def run_multi(args):
     tables = {t: W.Table(specs[t], dev) for t in range(T)}
     samples = {t: tables[t].lookup_batch(B, 0) for t in range(T)}
     profiles, cfg = build_profiles(preset, samples, geb)
-    ex = X.CompressedAllToAll(T, dim, B, profiles, cfg, device=dev)
+    ex = X.CompressedAllToAll(T, dim, B, profiles, cfg, device=dev, groups=args.groups)
     P = 8
     lookups = []
     for it in range(P):
@@ -456,6 +456,7 @@ def run_multi(args):
                            "tables": T, "dim": dim, "batch_per_rank": B, "parallelism": f"model-parallel tables over {R} ranks",
                            "compression_ratio": round(tot[2].item() / max(tot[1].item(), 1), 3)},
                 "exchange": {"compressed_ms": round(t_ms, 4), "uncompressed_nccl_ms": round(float(bms.item()), 4),
+                             "groups": args.groups,
                              "speedup_vs_uncompressed": round(float(bms.item()) / t_ms, 3)},
                 "e2e": None, "gpu_launches": None, "clocks": clk.summary()}
         print(json.dumps(line))
@@ -471,6 +472,7 @@ def main():
     ap.add_argument("--workload", default="kg", choices=["kg", "tb", "cfg1"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--groups", type=int, default=4, help="N > 1: table groups pipelined through the exchange")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

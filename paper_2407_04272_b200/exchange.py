@@ -42,15 +42,17 @@ META = K.META_SIZE
 
 
 class GpuCodec:
-    """The product backend: sm_100a kernels through the C ABI."""
+    """The product backend: sm_100a kernels through the C ABI.  Encode and
+    decode own separate contexts (scratch + staging), so a pipelined exchange
+    can run them concurrently on different streams."""
 
-    def __init__(self, ctx: Optional[K.Context] = None):
+    def __init__(self, ctx: Optional[K.Context] = None, dec_ctx: Optional[K.Context] = None):
         self.ctx = ctx or K.Context.default()
+        self.dec_ctx = dec_ctx or K.Context(self.ctx.device)
 
-    def encode(self, jobs: Sequence[K.EncodeJob], out: Optional[torch.Tensor] = None):
+    def encode(self, jobs: Sequence[K.EncodeJob], out: Optional[torch.Tensor] = None, stream=None):
         """-> (device uint8 buffer, device lengths int64 [njobs], device metadata uint8 [njobs, 25])."""
         cj = [j.to_c() for j in jobs]
-        import ctypes as C
         arr = (K._lib.Job * len(cj))(*cj)
         bound = int(self.ctx._L.embc_encode_bound(arr, len(cj), K.LAYOUT_CHUNKS))
         dev = jobs[0].batch.device
@@ -58,11 +60,10 @@ class GpuCodec:
             out = torch.empty(max(bound, 1), dtype=torch.uint8, device=dev)
         lens = torch.empty(len(cj), dtype=torch.int64, device=dev)
         meta = torch.empty((len(cj), META), dtype=torch.uint8, device=dev)
-        self.ctx.encode_raw(cj, K.LAYOUT_CHUNKS, out, None, lens, meta, None)
-        del C
+        self.ctx.encode_raw(cj, K.LAYOUT_CHUNKS, out, None, lens, meta, None, stream=stream)
         return out, lens, meta
 
-    def decode(self, buf: torch.Tensor, refs: Sequence[tuple], outs: Sequence[torch.Tensor]) -> None:
+    def decode(self, buf: torch.Tensor, refs: Sequence[tuple], outs: Sequence[torch.Tensor], stream=None) -> None:
         crefs = []
         for (off, length, codec, dim, count), o in zip(refs, outs):
             r = K._lib.ChunkRef()
@@ -71,10 +72,11 @@ class GpuCodec:
             crefs.append(r)
         if crefs:
             kind = K.OUT_F64 if outs[0].dtype == torch.float64 else K.OUT_F32
-            self.ctx.decode_raw(buf, crefs, kind, False)
+            self.dec_ctx.decode_raw(buf, crefs, kind, False, stream=stream)
 
     def check(self) -> None:
         self.ctx.sync()
+        self.dec_ctx.sync()
 
 
 @dataclass
@@ -107,7 +109,7 @@ class CompressedAllToAll:
                  cfg: P.PolicyConfig, backend=None, group=None, device=None, window: int = 255,
                  grad_profiles: Optional[Dict[int, P.TableProfile]] = None,
                  grad_cfg: Optional[P.PolicyConfig] = None, timing: bool = False,
-                 out_dtype: torch.dtype = torch.float32):
+                 out_dtype: torch.dtype = torch.float32, groups: int = 1):
         self.group = group
         self.R = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -123,6 +125,12 @@ class CompressedAllToAll:
         self.out_dtype = out_dtype  # float64 reproduces the reference's delivered doubles bit for bit
         self.stats = ExchangeStats()
         self._send_buf: Optional[torch.Tensor] = None
+        # > 1: the exchange runs as a pipeline of table groups: group g+1
+        # compresses while group g is on the wire and group g-1 decompresses
+        self.groups = max(1, groups)
+        cuda = self.device.type == "cuda"
+        self._s_enc = torch.cuda.Stream(self.device) if cuda and self.groups > 1 else None
+        self._s_dec = torch.cuda.Stream(self.device) if cuda and self.groups > 1 else None
 
     def owner(self, t: int) -> int:
         return t % self.R
@@ -218,6 +226,115 @@ class CompressedAllToAll:
         self.stats = st
         return st
 
+    def _exchange_pipelined(self, jobs_by: List[List[K.EncodeJob]], dst_by: List[List[int]],
+                            plan_by: List[List[List[tuple]]], outs_by: List[List[List[torch.Tensor]]]) -> ExchangeStats:
+        """The same four stages per table group, overlapped: every group's
+        compression is queued on the encode stream up front; each group's
+        metadata and payload rounds go out as soon as its compression is done,
+        and its decompression runs on the decode stream while the next group
+        is on the wire.  Byte-for-byte the same chunks as one big exchange."""
+        import contextlib
+        cuda = self._s_enc is not None
+        cur = torch.cuda.current_stream(self.device) if cuda else None
+        enc_ctx = (lambda: torch.cuda.stream(self._s_enc)) if cuda else contextlib.nullcontext
+        dec_ctx = (lambda: torch.cuda.stream(self._s_dec)) if cuda else contextlib.nullcontext
+        st = ExchangeStats()
+        t0 = t1 = None
+        if self.timing:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t0.record(cur)
+        if cuda:
+            self._s_enc.wait_stream(cur)  # the inputs were produced on the caller's stream
+        encoded = []
+        for jobs in jobs_by:
+            if not jobs:
+                encoded.append(None)
+                continue
+            with enc_ctx():
+                if cuda:
+                    buf, lens, meta = self.backend.encode(jobs, None, stream=self._s_enc)
+                else:
+                    buf, lens, meta = self.backend.encode(jobs, None)
+                ev = None
+                if cuda:
+                    ev = torch.cuda.Event()
+                    ev.record(self._s_enc)
+            encoded.append((buf, lens, meta, ev))
+        R = self.R
+        for g, jobs in enumerate(jobs_by):
+            recv_plan, outs, job_dst = plan_by[g], outs_by[g], dst_by[g]
+            send_cnt = [sum(1 for d in job_dst if d == r) for r in range(R)]
+            recv_cnt = [len(recv_plan[s]) for s in range(R)]
+            if encoded[g] is None:
+                buf = torch.zeros(1, dtype=torch.uint8, device=self.device)
+                lens = torch.zeros(0, dtype=torch.int64, device=self.device)
+                meta = torch.zeros((0, META), dtype=torch.uint8, device=self.device)
+            else:
+                buf, lens, meta, ev = encoded[g]
+                if ev is not None:
+                    cur.wait_event(ev)
+            meta_recv = torch.empty((sum(recv_cnt), META), dtype=torch.uint8, device=self.device)
+            if R > 1:
+                dist.all_to_all_single(meta_recv.view(-1), meta.reshape(-1), [c * META for c in recv_cnt],
+                                       [c * META for c in send_cnt], group=self.group)
+            else:
+                meta_recv.copy_(meta)
+            host = torch.cat([lens.view(-1), meta_recv.view(-1).to(torch.int64)]).cpu()
+            lens_h = host[:len(jobs)].tolist()
+            meta_h = bytes(host[len(jobs):].to(torch.uint8).numpy().tobytes())
+            send_bytes = [0] * R
+            for l, d in zip(lens_h, job_dst):
+                send_bytes[d] += l
+            recs = [_parse_meta(meta_h[i * META:(i + 1) * META]) for i in range(sum(recv_cnt))]
+            recv_bytes = [0] * R
+            k = 0
+            for src in range(R):
+                for _ in range(recv_cnt[src]):
+                    recv_bytes[src] += recs[k][0]
+                    k += 1
+            total_send = sum(send_bytes)
+            recv = torch.empty(max(sum(recv_bytes), 1), dtype=torch.uint8, device=self.device)
+            if R > 1:
+                dist.all_to_all_single(recv[:sum(recv_bytes)], buf[:total_send], recv_bytes, send_bytes,
+                                       group=self.group)
+            else:
+                recv[:total_send].copy_(buf[:total_send])
+            refs, dst_tensors = [], []
+            off, k = 0, 0
+            for src in range(R):
+                for j, (count, dim) in enumerate(recv_plan[src]):
+                    clen, codec, _eb, mdim, mcount = recs[k]
+                    refs.append((off, clen, codec, mdim, mcount))
+                    dst_tensors.append(outs[src][j])
+                    if (mdim, mcount) != (dim, count):
+                        from ._lib import CodecFormatError
+                        raise CodecFormatError(f"rank {self.rank} decompress stage (from rank {src}): metadata from "
+                                               f"rank {src} disagrees with its chunk", status=2, reason=32)
+                    off += clen
+                    k += 1
+            if cuda:
+                self._s_dec.wait_stream(cur)
+                with dec_ctx():
+                    self.backend.decode(recv, refs, dst_tensors, stream=self._s_dec)
+                    recv.record_stream(self._s_dec)
+            else:
+                self.backend.decode(recv, refs, dst_tensors)
+            for l, d, j in zip(lens_h, job_dst, jobs):
+                if d != self.rank:
+                    st.payload_bytes += l
+                    st.metadata_bytes += META
+                    st.uncompressed_bytes += j.batch.numel() * 4
+        if cuda:
+            cur.wait_stream(self._s_dec)  # outputs are ready on the caller's stream
+        if self.timing:
+            t1 = torch.cuda.Event(enable_timing=True)
+            t1.record(cur)
+            t1.synchronize()
+            st.times_ms["total"] = t0.elapsed_time(t1)
+        self.backend.check()
+        self.stats = st
+        return st
+
     def forward(self, iteration: int, lookups: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
         """lookups[t] for owned t: [R*B, dim] with rows d*B..(d+1)*B destined to
         rank d.  Returns {t: [B, dim]} for every table (rank's data-parallel slice)."""
@@ -231,10 +348,40 @@ class CompressedAllToAll:
                                         self.window))
                 job_dst.append(d)
         out = {t: torch.empty((B, self.dim), dtype=self.out_dtype, device=self.device) for t in range(self.T)}
+        if self.groups > 1:  # group k = the k-th run of every rank's owned tables
+            jobs_by, dst_by, plan_by, outs_by = [], [], [], []
+            G = min(self.groups, max(len(self.owned(r)) for r in range(R)))  # identical on every rank
+            mine = [self._split_of(len(own), G, k) for k in range(G)]
+            for k in range(G):
+                jg, dg = [], []
+                for d in range(R):
+                    for i in mine[k]:
+                        t = own[i]
+                        eb = P.eb_at(t, iteration, self.profiles, self.cfg)
+                        jg.append(K.EncodeJob(lookups[t][d * B:(d + 1) * B], eb, self._codec(self.profiles, t),
+                                              self.window))
+                        dg.append(d)
+                plan, og = [], []
+                for src in range(R):
+                    theirs = self.owned(src)
+                    part = self._split_of(len(theirs), G, k)
+                    plan.append([(B, self.dim) for _ in part])
+                    og.append([out[theirs[i]] for i in part])
+                jobs_by.append(jg)
+                dst_by.append(dg)
+                plan_by.append(plan)
+                outs_by.append(og)
+            self._exchange_pipelined(jobs_by, dst_by, plan_by, outs_by)
+            return out
         recv_plan = [[(B, self.dim) for _ in self.owned(s)] for s in range(R)]
         outs = [[out[t] for t in self.owned(s)] for s in range(R)]
         self._exchange(jobs, job_dst, recv_plan, outs)
         return out
+
+    def _split_of(self, n: int, ngroups: int, k: int) -> List[int]:
+        """Positions of group k when n items are cut into ngroups runs (every
+        rank uses the same group count so the rounds line up)."""
+        return list(range(k * n // ngroups, (k + 1) * n // ngroups))
 
     def backward(self, iteration: int, grads: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
         """grads[t] for every table: [B, dim] local gradient slice.  Returns
