@@ -286,6 +286,12 @@ def run_single(args):
         "k_dec_fin": 8 * ref_vals,                             # reference rows copied from their roots
     }
     hbm, peak_kind = peaks()
+    traffic = None  # DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f)[args.workload]["bytes_per_launch"].get(dom)
+    except Exception:
+        traffic = None
     ab = algo.get(dom)
     achieved = (ab / (dom_ms * 1e-3) / 1e9) if ab else None
     step_kernel_ms = sum(sum(v) for v in per.values()) / nprof
@@ -378,7 +384,9 @@ def run_single(args):
                 "pipeline": "H2D / kernels / D2H on three streams, steps overlapped"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2) if achieved else None,
                      "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4) if achieved else None, "traffic": None,
+                     "frac": round(achieved / hbm, 4) if achieved else None,
+                     "traffic": round(traffic) if traffic else None,
+                     "traffic_source": "profiles/traffic.json (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
                      "kernel_ms": round(dom_ms, 5), "algorithmic_bytes": ab,
                      "step_kernel_ms": round(step_kernel_ms, 4),
                      "step_bytes": round(2 * step_bytes + 2 * packed_mean),
