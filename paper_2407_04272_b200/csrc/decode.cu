@@ -741,6 +741,7 @@ struct DecArgs {
   uint32_t* diag;
   uint32_t nchunks, nseg, nhblk, nraw, nctile;
   uint32_t vlz_dmax;    // largest vlz dim of the call (sizes the segment smem carve)
+  uint32_t hsub;        // subsequences per huffman block (128 or 256)
   uint32_t smem_bytes;  // dynamic shared memory of k_dec_main
 };
 
@@ -1081,16 +1082,17 @@ __device__ void vlz_roots(const DecArgs& a, uint32_t c, uint8_t* smem) {
 // ===========================================================================
 // Huffman blocks: 128 subsequences of 64 bits.
 // ===========================================================================
-constexpr uint32_t kHSub = 128;                        // subsequences per block
+constexpr uint32_t kHSub = 256;                        // subsequences per block (one per thread)
 constexpr uint32_t kHBits = kSubBits * kHSub;          // 8192 bits
 constexpr uint32_t kHPre = 2;                          // words staged before the block (warm-up)
 constexpr uint32_t kHWords = kHPre + kHBits / 32 + 4;  // + look-ahead past the block
 constexpr uint32_t kHOut = kHBits;                     // at most one symbol per bit
 // smem: LUT | staged words | per-subsequence chain summaries | group states, later the symbols (u16)
-constexpr uint32_t kHGsBytes = kHSub * 33 * 4;
-constexpr uint32_t kHOutBytes = kHOut * 2;
-constexpr uint32_t kHuffSmem = (1u << kL0) * 4 + ((kHWords * 4 + 15) & ~15u) + kHSub * 20 +
-                               (kHGsBytes > kHOutBytes ? kHGsBytes : kHOutBytes);
+__host__ __device__ constexpr uint32_t huff_smem(uint32_t hsub) {
+  return (1u << kL0) * 4 + (((kHPre + hsub * 2 + 4) * 4 + 15) & ~15u) + hsub * 20 +
+         (hsub * 33 * 4 > hsub * kSubBits * 2 ? hsub * 33 * 4 : hsub * kSubBits * 2);
+}
+constexpr uint32_t kHuffSmem = huff_smem(kHSub);
 
 // inclusive huffman state: flag | term (61:60) | entry bit offset (59:55) | symbols (54:0)
 __device__ __forceinline__ unsigned long long huf_state(uint32_t term, uint32_t e, uint64_t cnt) {
@@ -1098,7 +1100,7 @@ __device__ __forceinline__ unsigned long long huf_state(uint32_t term, uint32_t 
          (cnt & ((1ull << 55) - 1));
 }
 
-// Huffman block (8192 bits = 128 subsequences of 64 bits):
+// Huffman block (16384 bits = 256 subsequences of 64 bits, one per thread):
 //  A  every subsequence decodes one chain that starts 64 bits early (in the
 //     previous subsequence), so it has usually synchronised with the true
 //     codeword boundaries by the time it enters: its starts inside the
@@ -1114,22 +1116,23 @@ __device__ __forceinline__ unsigned long long huf_state(uint32_t term, uint32_t 
 //     shared memory; the block stores them coalesced.
 __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   __shared__ HTab t;
-  __shared__ uint32_t G[4][32], BM[32];
-  __shared__ uint32_t s_ge[4], s_gt[4];
-  __shared__ unsigned long long s_gc[4];
+  __shared__ uint32_t G[kHSub / 32][32], BM[32];
+  __shared__ uint32_t s_ge[kHSub / 32], s_gt[kHSub / 32];
+  __shared__ unsigned long long s_gc[kHSub / 32];
   __shared__ unsigned long long s_in;
   __shared__ int s_use;
   const uint32_t c = a.hblk_chunk[gb];
   const DChunk& C = a.ch[c];
   const uint32_t b = gb - C.blk0;
+  const uint32_t hsub = a.hsub, hbits = hsub * kSubBits, hwords = kHPre + hbits / 32 + 4;
   uint32_t* lut = reinterpret_cast<uint32_t*>(smem);
   uint32_t* W = lut + (1u << kL0);
-  uint64_t* B0 = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(W) + ((kHWords * 4 + 15) & ~15u));
-  uint32_t* X0 = reinterpret_cast<uint32_t*>(B0 + kHSub);
-  uint32_t* Y0 = X0 + kHSub;
-  uint32_t* Ye = Y0 + kHSub;
-  uint32_t(*Gs)[33] = reinterpret_cast<uint32_t(*)[33]>(Ye + kHSub);
-  uint16_t* outs = reinterpret_cast<uint16_t*>(Ye + kHSub);  // reuses Gs after phase B
+  uint64_t* B0 = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(W) + ((hwords * 4 + 15) & ~15u));
+  uint32_t* X0 = reinterpret_cast<uint32_t*>(B0 + hsub);
+  uint32_t* Y0 = X0 + hsub;
+  uint32_t* Ye = Y0 + hsub;
+  uint32_t(*Gs)[33] = reinterpret_cast<uint32_t(*)[33]>(Ye + hsub);
+  uint16_t* outs = reinterpret_cast<uint16_t*>(Ye + hsub);  // reuses Gs after phase B
   DROLE(blockIdx.x, 2);
   if (threadIdx.x == 0) {  // the chunk CTA (an earlier ticket) publishes the tables
     uint32_t delay = 32;
@@ -1153,19 +1156,19 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   for (uint32_t i = threadIdx.x; i < sizeof(HTab) / 4; i += blockDim.x)
     reinterpret_cast<uint32_t*>(&t)[i] = __ldcg(reinterpret_cast<const unsigned int*>(hv.tab) + i);
   __syncthreads();
-  const uint64_t bit0 = static_cast<uint64_t>(b) * kHBits;
+  const uint64_t bit0 = static_cast<uint64_t>(b) * hbits;
   const uint8_t* bits = C.in + __ldcg(reinterpret_cast<const unsigned long long*>(&S.pay_off)) + t.bit_off;
   // W[kHPre + k] = word k of the block; the two words before hold the previous block's tail
-  if (b > 0) stage_bits(W, kHWords, bits, t.nbits / 8, bit0 - 32 * kHPre);
+  if (b > 0) stage_bits(W, hwords, bits, t.nbits / 8, bit0 - 32 * kHPre);
   else {
     if (threadIdx.x < kHPre) W[threadIdx.x] = 0;
-    stage_bits(W + kHPre, kHWords - kHPre, bits, t.nbits / 8, bit0);
+    stage_bits(W + kHPre, hwords - kHPre, bits, t.nbits / 8, bit0);
   }
   __syncthreads();
   DTS(blockIdx.x, 2);
   const uint32_t R = t.max_len;
   const uint64_t nbits = t.nbits;
-  const uint32_t nloc = min(kHSub, C.nsub - b * kHSub);
+  const uint32_t nloc = min(hsub, C.nsub - b * hsub);
   const uint32_t nent = t.nent;
   // decode from relative bit q (of subsequence i) until q >= 64, a start in
   // `stop` (the result then follows xs), or the end
@@ -1568,7 +1571,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   std::vector<RawTile> raw_tiles;
   std::vector<SegPair> segs;
   std::vector<uint32_t> hblk, ctiles;
-  uint64_t map_total = 0, row_total = 0, tab_total = 0;
+  uint64_t map_total = 0, row_total = 0, tab_total = 0, huf_subs = 0;
   const uint64_t hdr = payload_only ? 0 : kHeader;
   for (uint32_t c = 0; c < n; ++c) {
     const embc_chunk_ref& r = refs[c];
@@ -1617,10 +1620,18 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
       C.tab_off = tab_total;
       tab_total += std::max<uint64_t>(htab_bytes(C.book_cap), 8 * p2 + 16);
       C.nsub = static_cast<uint32_t>((8 * (pay > 12 ? pay - 12 : 0) + kSubBits - 1) / kSubBits);
-      C.nblk = (C.nsub + kHSub - 1) / kHSub;
-      C.blk0 = static_cast<uint32_t>(hblk.size());
-      for (uint32_t k = 0; k < C.nblk; ++k) hblk.push_back(c);
+      huf_subs += C.nsub;
     }
+  }
+  // huffman block size: 256 subsequences when there are enough for ~3 blocks per
+  // SM slot, else 128 (more, shorter blocks for small calls)
+  const uint32_t hsub = huf_subs >= 256ull * 600 ? 256 : 128;
+  for (uint32_t c = 0; c < n; ++c) {
+    DChunk& C = ch[c];
+    if (C.codec != EMBC_CODEC_HUFFMAN) continue;
+    C.nblk = (C.nsub + hsub - 1) / hsub;
+    C.blk0 = static_cast<uint32_t>(hblk.size());
+    for (uint32_t k = 0; k < C.nblk; ++k) hblk.push_back(c);
   }
   const uint32_t nseg = static_cast<uint32_t>(segs.size()), nhb = static_cast<uint32_t>(hblk.size());
   const uint32_t nct = static_cast<uint32_t>(ctiles.size() / 3);
@@ -1694,10 +1705,11 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   for (uint32_t c = 0; c < n; ++c)
     if (ch[c].codec == EMBC_CODEC_VLZ && !ch[c].seq) dmax = std::max(dmax, ch[c].dim);
   a.vlz_dmax = dmax;
+  a.hsub = hsub;
   uint32_t rmax = 0;  // rows of the largest vlz chunk: the root tail keeps them in smem
   for (uint32_t c = 0; c < n; ++c)
     if (ch[c].codec == EMBC_CODEC_VLZ && !ch[c].seq) rmax = std::max(rmax, ch[c].count);
-  uint32_t smem = std::max<uint32_t>(std::max<uint32_t>(nseg ? vlz_smem(dmax) : 0, nhb ? kHuffSmem : 0), 16384);
+  uint32_t smem = std::max<uint32_t>(std::max<uint32_t>(nseg ? vlz_smem(dmax) : 0, nhb ? huff_smem(hsub) : 0), 16384);
   if (nseg) smem = std::max<uint32_t>(smem, std::min<uint32_t>(4 * rmax + 64, 48 * 1024));
   a.smem_bytes = smem;
   EMBC_TIMED(ctx, "k_dec_main", stream, k_dec_main<<<g1, kBlock, smem, stream>>>(a));
