@@ -105,7 +105,12 @@ __device__ DecState parse_chunk(const DChunk& C) {
   S.nsym = 0;
   S.bit_off = 0;
   if (!C.payload_only) {
-    const uint8_t* p = C.in;
+    // the 30 header bytes in one round of independent loads, then parsed from registers
+    uint8_t hb[kHeader];
+    const uint8_t* src = C.in;
+#pragma unroll
+    for (uint32_t k = 0; k < kHeader; ++k) hb[k] = k < C.length ? __ldg(src + k) : 0;
+    const uint8_t* p = hb;
     const uint64_t L = C.length;
     // field layout: magic[4] ver codec eb:8 dim:4 count:4 paylen:8
     const uint32_t need_at[] = {0, 1, 2, 3, 4, 5, 6, 14, 18, 22};
@@ -319,7 +324,7 @@ __device__ __forceinline__ uint64_t value_bits(int32_t code, double w, int kind)
   return static_cast<uint32_t>(code);
 }
 
-__device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState* __restrict__ st,
+__device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState& S,
                             uint64_t* __restrict__ keys, uint8_t* __restrict__ tabs,
                             uint32_t* __restrict__ hflag, uint64_t* skey, uint32_t skey_cap) {
   __shared__ unsigned long long s_tmp64[33];
@@ -327,7 +332,7 @@ __device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState*
   __shared__ int s_stop;
   __shared__ HTab tb;
   const DChunk C = ch[c];
-  DecState& S = st[c];
+  DTS(8000 + c, 8);
   if (S.err != ~0ull) return;
   const uint8_t* p = C.in + S.pay_off;
   const uint64_t L = S.pay_len;
@@ -388,7 +393,11 @@ __device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState*
   // canonical order (length, symbol): key = len << 32 | (symbol ^ 0x80000000)
   uint32_t p2 = 1;
   while (p2 < nent) p2 <<= 1;
-  if (p2 <= skey_cap) key = skey;  // small codebooks sort in shared memory
+  uint32_t* ssym = nullptr;  // symbols in canonical order, kept in smem when there is room
+  if (p2 + (p2 + 1) / 2 <= skey_cap) {
+    key = skey;  // small codebooks sort in shared memory
+    ssym = reinterpret_cast<uint32_t*>(skey + p2);
+  }
   for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x) {
     if (i < nent) {
       const uint32_t s = static_cast<uint32_t>(ld_be(p + 12 + 5ull * i, 4));
@@ -398,11 +407,19 @@ __device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState*
     }
   }
   __syncthreads();
-  DTS(blockIdx.x, 2);
-  bitonic_sort_u64(key, p2);
-  DTS(blockIdx.x, 3);
-  for (uint32_t i = threadIdx.x; i < nent; i += blockDim.x)
-    hv.syms[i] = static_cast<int32_t>(static_cast<uint32_t>(key[i]) ^ 0x80000000u);
+  DTS(8000 + c, 2);
+  if (ssym && p2 <= 256) {  // one warp, in registers
+    if (threadIdx.x < 32) warp_sort_smem(key, p2);
+    __syncthreads();
+  } else {
+    bitonic_sort_u64(key, p2);
+  }
+  DTS(8000 + c, 3);
+  for (uint32_t i = threadIdx.x; i < nent; i += blockDim.x) {
+    const uint32_t sy = static_cast<uint32_t>(key[i]) ^ 0x80000000u;
+    hv.syms[i] = static_cast<int32_t>(sy);
+    if (ssym) ssym[i] = sy;
+  }
   if (threadIdx.x < 33) {
     tb.count[threadIdx.x] = 0;
     tb.first[threadIdx.x] = 0;
@@ -430,12 +447,12 @@ __device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState*
         tb.base[len] = i;
       }
       atomicAdd(&tb.count[len], 1u);
-      hv.vals[i] = value_bits(hv.syms[i], w, C.out_kind);
+      hv.vals[i] = value_bits(static_cast<int32_t>(static_cast<uint32_t>(key[i]) ^ 0x80000000u), w, C.out_kind);
     }
     carry += tot;
   }
   __syncthreads();
-  DTS(blockIdx.x, 4);
+  DTS(8000 + c, 4);
   // left-aligned code starts, ascending in canonical order -> prefix LUT
   for (uint32_t i = threadIdx.x; i < nent; i += blockDim.x) {
     const uint32_t len = static_cast<uint32_t>(key[i] >> 32);
@@ -468,13 +485,19 @@ __device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState*
     hv.lut[s] = ent;
   }
   __syncthreads();  // the code starts in key[] are read above; reused below
-  DTS(blockIdx.x, 5);
+  DTS(8000 + c, 5);
   // duplicate symbols (huffman.hpp:183-185) across all lengths
   for (uint32_t i = threadIdx.x; i < p2; i += blockDim.x)
-    key[i] = i < nent ? (static_cast<uint64_t>(static_cast<uint32_t>(hv.syms[i]) ^ 0x80000000u) << 32) | i : ~0ull;
+    key[i] = i < nent ? (static_cast<uint64_t>((ssym ? ssym[i] : static_cast<uint32_t>(hv.syms[i])) ^ 0x80000000u) << 32) | i
+                      : ~0ull;
   __syncthreads();
-  bitonic_sort_u64(key, p2);
-  DTS(blockIdx.x, 6);
+  if (ssym && p2 <= 256) {
+    if (threadIdx.x < 32) warp_sort_smem(key, p2);
+    __syncthreads();
+  } else {
+    bitonic_sort_u64(key, p2);
+  }
+  DTS(8000 + c, 6);
   bool dup = false;
   for (uint32_t i = 1 + threadIdx.x; i < nent; i += blockDim.x) dup |= (key[i] >> 32) == (key[i - 1] >> 32);
   dup = __syncthreads_or(dup);
@@ -1138,7 +1161,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     uint32_t delay = 32;
     while (!*reinterpret_cast<volatile uint32_t*>(&a.ready[c])) {
       __nanosleep(delay);
-      delay = min(delay * 2, 512u);
+      delay = min(delay * 2, 256u);
     }
     __threadfence();
     const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&a.st[c].err);
@@ -1413,15 +1436,18 @@ __global__ void __launch_bounds__(kBlock, 5) k_dec_main(DecArgs a) {
   uint32_t t = s_t;  // roles in ticket order: look-back only ever waits on earlier tickets
   DROLE(blockIdx.x, 0);
   DTS(blockIdx.x, 1);
-  if (t < a.nchunks) {  // chunk CTA
+  if (t < a.nchunks) {  // chunk CTA: header + (huffman) decode tables, then the ready flag
+    __shared__ DecState sS;
     const DChunk& C = a.ch[t];
-    if (threadIdx.x == 0) a.st[t] = parse_chunk(C);
+    if (threadIdx.x == 0) sS = parse_chunk(C);
     __syncthreads();
-    if (C.codec == EMBC_CODEC_HUFFMAN) {
-      huff_tables(t, a.ch, a.st, a.keys, a.tabs, a.hflag, reinterpret_cast<uint64_t*>(smem), a.smem_bytes / 8);
+    if (C.codec == EMBC_CODEC_HUFFMAN)
+      huff_tables(t, a.ch, sS, a.keys, a.tabs, a.hflag, reinterpret_cast<uint64_t*>(smem), a.smem_bytes / 8);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a.st[t] = sS;
       __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t*>(&a.ready[t]) = 1;
+      *reinterpret_cast<volatile uint32_t*>(&a.ready[t]) = 1;
     }
     DTS(blockIdx.x, 7);
     return;
@@ -1560,7 +1586,8 @@ using namespace embc_dev;
 static inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
 cudaError_t decode_set_attributes() {
-  return cudaFuncSetAttribute(k_dec_main, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
+  cudaError_t e = cudaFuncSetAttribute(k_dec_main, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
+  return e;
 }
 
 embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* refs, uint32_t n,

@@ -140,6 +140,11 @@ __device__ __forceinline__ double reconstruct(int32_t c, double w) {
   return __dmul_rn(static_cast<double>(c), w);
 }
 
+// Programmatic dependent launch (sm_90+): let the next kernel of the stream be
+// scheduled early / wait for the previous kernel's results.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 // zigzag (bytes.hpp:168-174) and unsigned LEB128 (bytes.hpp:61-67)
 // ---------------------------------------------------------------------------
@@ -256,6 +261,77 @@ __device__ __forceinline__ uint64_t ld_be(const uint8_t* p, int nb) {
   uint64_t v = 0;
   for (int i = 0; i < nb; ++i) v = (v << 8) | p[i];
   return v;
+}
+
+// Ascending bitonic sort of 32*K keys held in registers across one warp:
+// element (r, lane) is position r*32 + lane.
+template <int K>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[K]) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (uint32_t k = 2; k <= 32u * K; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const int r2 = r ^ static_cast<int>(j >> 5);
+          if (r2 > r) {
+            const uint32_t i = static_cast<uint32_t>(r) * 32 + lane;
+            const bool up = (i & k) == 0;
+            const uint64_t x = v[r], y = v[r2];
+            if ((x > y) == up) {
+              v[r] = y;
+              v[r2] = x;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const uint32_t i = static_cast<uint32_t>(r) * 32 + lane;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[r], j);
+          const bool up = (i & k) == 0;
+          const bool lower = (lane & j) == 0;  // this lane holds the smaller index of the pair
+          // lower keeps min when ascending, max when descending; the upper the opposite
+          const bool keep_min = (lower == up);
+          v[r] = keep_min ? (v[r] < o ? v[r] : o) : (v[r] > o ? v[r] : o);
+        }
+      }
+    }
+  }
+}
+
+// Sort p2 (<= 256) keys of shared memory with one warp, through registers.
+__device__ __forceinline__ void warp_sort_smem(uint64_t* key, uint32_t p2) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (p2 <= 32) {
+    uint64_t v[1] = {lane < p2 ? key[lane] : ~0ull};
+    warp_sort_regs<1>(v);
+    if (lane < p2) key[lane] = v[0];
+  } else if (p2 <= 64) {
+    uint64_t v[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) v[r] = key[r * 32 + lane];
+    warp_sort_regs<2>(v);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) key[r * 32 + lane] = v[r];
+  } else if (p2 <= 128) {
+    uint64_t v[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) v[r] = key[r * 32 + lane];
+    warp_sort_regs<4>(v);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) key[r * 32 + lane] = v[r];
+  } else {
+    uint64_t v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = key[r * 32 + lane];
+    warp_sort_regs<8>(v);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) key[r * 32 + lane] = v[r];
+  }
+  __syncwarp();
 }
 
 }  // namespace embc_dev
