@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_stats(StatsArgs a) {
   const uint32_t tid = blockIdx.x;
   TS1(0);
   const DTile T = a.tiles[tid];
-  const DJob& J = a.jobs[T.job];
+  const DJob J = a.jobs[T.job];
   // E2 scratch of this call starts clean
   if (threadIdx.x == 0) {
     a.tile_status[tid] = 0;
@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_stats(StatsArgs a) {
   if (!s_last) return;
   __threadfence();
   TS1(3);
-  build_book(J, Sp, a.book, smem);
+  build_book(a.jobs[T.job], Sp, a.book, smem);
   TS1(4);
 }
 
@@ -919,7 +919,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
   const int phase = a.phase;
   const DTile T = a.tiles[tid];
   const uint32_t jid = T.job;
-  const DJob& J = a.jobs[jid];
+  const DJob J = a.jobs[jid];  // by value: the fields live in registers, not re-read after global stores
   const JobState& S = a.st[jid];
   const uint32_t dim = J.dim;
   const uint64_t e0 = static_cast<uint64_t>(T.row0) * dim;
