@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_stats(StatsArgs a) {
   const uint32_t tid = blockIdx.x;
   TS1(0);
   const DTile T = a.tiles[tid];
-  const DJob J = a.jobs[T.job];
+  const DJob& J = a.jobs[T.job];
   // E2 scratch of this call starts clean
   if (threadIdx.x == 0) {
     a.tile_status[tid] = 0;
@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_stats(StatsArgs a) {
   if (!s_last) return;
   __threadfence();
   TS1(3);
-  build_book(a.jobs[T.job], Sp, a.book, smem);
+  build_book(J, Sp, a.book, smem);
   TS1(4);
 }
 
@@ -929,7 +929,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
   uint8_t* stage = smem + a.stage_off;
   uint8_t* aux = smem + a.aux_off;
   const uint32_t codec = J.codec;
-  const uint32_t stride = codec == EMBC_CODEC_VLZ ? (dim | 1u) : 0;
+  const uint32_t stride = codec == EMBC_CODEC_VLZ ? dim : 0;  // vlz rows unpadded: warps read rows along lanes
 
   uint32_t* dec = reinterpret_cast<uint32_t*>(aux + a.hash_cap * 4);  // vlz: match offset per row
   uint32_t* lits = dec + a.rows_cap;                                   // vlz: token bytes per row
@@ -966,6 +966,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
           const uint32_t q = base + u * kBlock + threadIdx.x;
           if (q >= nq || (vlz_lit_only && dec[fdiv(4 * q, J.fd)])) continue;
           const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+          int32_t vq[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t l = 4 * q + k;
@@ -976,15 +977,10 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
             } else {
               c = static_cast<int32_t>(w[k]);
             }
-            uint32_t at;
-            if (stride) {
-              const uint32_t r = fdiv(l, J.fd);
-              at = r * stride + (l - r * dim);
-            } else {
-              at = l + (l >> 5);
-            }
-            codes[at] = c;
+            if (!stride) codes[l + (l >> 5)] = c;
+            else vq[k] = c;
           }
+          if (stride) reinterpret_cast<int4*>(codes)[q] = make_int4(vq[0], vq[1], vq[2], vq[3]);  // row-major
         }
       }
     } else {
@@ -1085,7 +1081,51 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
       }
       if (np == 0) break;
       __syncthreads();
-      const uint32_t work = np * dim;
+      const bool vq = (dim & 3) == 0 && (reinterpret_cast<uintptr_t>(J.src) & 15) == 0;
+      const uint32_t work = vq ? np * (dim >> 2) : np * dim;
+      if (vq) {  // four codes per work item: 16-B smem / global loads
+        const uint32_t qpr = dim >> 2;
+        for (uint32_t e0w = 0; e0w < work; e0w += 2 * kBlock) {
+          int4 cj[2], ci[2];
+          uint32_t pp[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const uint32_t e = e0w + u * kBlock + threadIdx.x;
+            pp[u] = 0xFFFFFFFFu;
+            if (e < work) {
+              const uint32_t pi = e / qpr;
+              const uint32_t qc = e - pi * qpr;
+              const uint32_t r = plist[pi];
+              const uint32_t i = T.row0 + r, j = i - cand[r];
+              pp[u] = pi;
+              ci[u] = reinterpret_cast<const int4*>(codes + r * dim)[qc];
+              if (j >= T.row0) {
+                cj[u] = reinterpret_cast<const int4*>(codes + (j - T.row0) * dim)[qc];
+              } else {
+                const uint4 g = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(J.src) +
+                                                                     static_cast<uint64_t>(j) * dim) + qc);
+                cj[u] = make_int4(static_cast<int32_t>(g.x), static_cast<int32_t>(g.y), static_cast<int32_t>(g.z),
+                                  static_cast<int32_t>(g.w));
+                if (J.src_kind == EMBC_SRC_F32) pp[u] |= 0x80000000u;  // needs quantizing
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (pp[u] == 0xFFFFFFFFu) continue;
+            int4 c = cj[u];
+            if (pp[u] & 0x80000000u) {
+              uint32_t rr = 0;
+              c.x = quantize_f32(__int_as_float(c.x), J.qp, &rr);
+              c.y = quantize_f32(__int_as_float(c.y), J.qp, &rr);
+              c.z = quantize_f32(__int_as_float(c.z), J.qp, &rr);
+              c.w = quantize_f32(__int_as_float(c.w), J.qp, &rr);
+            }
+            if (c.x != ci[u].x || c.y != ci[u].y || c.z != ci[u].z || c.w != ci[u].w)
+              miss[pp[u] & 0x7FFFFFFFu] = 1;
+          }
+        }
+      } else
       for (uint32_t e0w = 0; e0w < work; e0w += 4 * kBlock) {
         int32_t cj[4], ci[4];
         uint32_t pp[4];
