@@ -268,7 +268,7 @@ __device__ __forceinline__ void k_dec_vlz_seq_cta(uint32_t bid, const DChunk* __
 //   H3 k_huff_out     decode again from the true starts and write values.
 // Failures flag the chunk; k_dec_huff_seq then reproduces the exact error.
 // ===========================================================================
-constexpr int kL0 = 11;
+constexpr int kL0 = 10;
 constexpr uint32_t kSubBits = 64;
 constexpr uint32_t kLong = 63;
 
