@@ -639,26 +639,27 @@ __device__ __forceinline__ void k_dec_huff_seq_cta(uint32_t bid, const DChunk* _
 // ---------------------------------------------------------------------------
 // D9: fold the lowest failing chunk into the sticky record.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void dec_fold(const DecState* __restrict__ st, uint32_t n, DevError* err) {
-  for (uint32_t c = 0; c < n; ++c) {
-    const DecState& S = st[c];
-    if (S.err == ~0ull) continue;
-    if (err->valid) return;
-    err->valid = 1;
-    err->job = c;
-    err->reason = static_cast<int32_t>(S.err & 63);
-    err->index = S.err >> 6;
-    err->a = S.a;
-    err->b = S.b;
-    err->eb = S.eb;
-    const int r = err->reason;
-    err->status = (r == EMBC_R_BAD_EB) ? EMBC_ERR_VALUE
-                  : (r == EMBC_R_RANGE) ? EMBC_ERR_UNSUPPORTED
-                                        : EMBC_ERR_FORMAT;
-    return;
-  }
+// The lowest failing chunk -> the sticky record (all threads of the CTA scan).
+__device__ void dec_fold(const DecState* __restrict__ st, uint32_t n, DevError* err) {
+  __shared__ uint32_t s_first;
+  if (threadIdx.x == 0) s_first = 0xFFFFFFFFu;
+  __syncthreads();
+  for (uint32_t c = threadIdx.x; c < n; c += blockDim.x)
+    if (__ldcg(reinterpret_cast<const unsigned long long*>(&st[c].err)) != ~0ull) atomicMin(&s_first, c);
+  __syncthreads();
+  if (threadIdx.x != 0 || s_first == 0xFFFFFFFFu || err->valid) return;
+  const uint32_t c = s_first;
+  const DecState& S = st[c];
+  err->valid = 1;
+  err->job = c;
+  err->reason = static_cast<int32_t>(S.err & 63);
+  err->index = S.err >> 6;
+  err->a = S.a;
+  err->b = S.b;
+  err->eb = S.eb;
+  const int r = err->reason;
+  err->status = (r == EMBC_R_BAD_EB) ? EMBC_ERR_VALUE : (r == EMBC_R_RANGE) ? EMBC_ERR_UNSUPPORTED : EMBC_ERR_FORMAT;
 }
-
 
 // ===========================================================================
 // look-back status words (flag in bits 63:62; 1 = aggregate map published,
@@ -1530,10 +1531,11 @@ __global__ void __launch_bounds__(kBlock) k_dec_fin(DecArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&a.tickets[1], 1u) == a.nchunks - 1;
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
+  if (s_last) {
     __threadfence();
     dec_fold(a.st, a.nchunks, a.err);
 #ifdef EMBC_DEBUG
+    if (threadIdx.x != 0) return;
     const uint32_t nb = a.nchunks + a.nseg + a.nhblk + a.nraw;
     if (a.nchunks >= 26 && (++g_dcalls) % 8 == 7 && nb <= 16384) {
       unsigned long long t0 = ~0ull;
