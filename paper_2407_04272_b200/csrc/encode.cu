@@ -56,7 +56,8 @@ constexpr uint32_t kSmemBook = 1024;     // codebook symbols sorted fully in sha
 // E2 dynamic shared memory carve (bytes) for tiles of <= vals values / rows rows:
 //   [codes: padded, rows*(dim|1) or l + l/32][stage: output bytes][aux: hashes + dec/lit | LUT]
 __host__ __device__ constexpr uint32_t emit_codes_bytes(uint32_t vals, uint32_t rows) {
-  return ((vals + rows + 64) * 4 + 15) & ~15u;
+  // vlz / raw: vals (row-major); huffman: l + l/32 padding
+  return (((vals + vals / 32 + 64) * 4 + 15) & ~15u) + 0 * rows;
 }
 __host__ __device__ constexpr uint32_t emit_stage_bytes(uint32_t vals, uint32_t rows, bool vlz = true) {
   return ((vlz ? rows + 5 * vals : 4 * vals) + 128 + 15) & ~15u;

@@ -1,0 +1,87 @@
+"""GPU parity on the envelope edges of the tiled kernels: rows wider than a
+tile (single-row tiles, sequential VLZ decode past dim 1023), VLZ windows wider
+than the staged hash window, Huffman alphabets past the one-warp codebook path
+(block builder, global sort scratch, wide histogram pool) and past the 16-bit
+symbol staging of the decoder, and a packed multi-chunk call mixing every
+codec and shape.  Reference: the oracle restatement (pinned to the reference
+by tests/test_oracle.py)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2407_04272_b200 import codec as K
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def roundtrip(oracle, x32, dim, eb, codec, window=255):
+    want = oracle.encode_chunk(x32.astype(np.float64), dim, eb, codec, window)
+    got = K.encode_chunk(dev(x32.reshape(-1, dim)), eb, codec, window)
+    assert got == want, (dim, codec, window, len(got), len(want))
+    d = K.decode_chunk(got, K.OUT_F64).cpu().numpy().ravel()
+    assert np.array_equal(d.view(np.uint64), oracle.decode_chunk(want).ravel().view(np.uint64))
+    f = K.decode_chunk(got, K.OUT_F32).cpu().numpy().ravel()
+    assert np.array_equal(f, oracle.decode_chunk(want).ravel().astype(np.float32))
+    return got
+
+
+@pytest.mark.parametrize("dim", [1024, 2048, 4095, 4096, 5000, 8192])
+def test_wide_rows(ctx, oracle, dim):
+    rng = np.random.default_rng(dim)
+    base = (rng.standard_normal((5, dim)) * 0.05).astype(np.float32)
+    x = base[rng.integers(0, 5, 12)]  # repeated rows -> vlz references across single-row tiles
+    for codec in (0, 1, 2):
+        roundtrip(oracle, x.ravel(), dim, 0.01, codec)
+
+
+def test_windows_past_the_hash_stage(ctx, oracle):
+    rng = np.random.default_rng(5)
+    rows = (rng.integers(-2, 3, (40, 2)) * 0.02).astype(np.float32)
+    x = rows[rng.integers(0, 40, 6000)]
+    for w in (1, 300, 2047, 2048, 4095, 65536):
+        roundtrip(oracle, x.ravel(), 2, 0.01, 1, w)
+
+
+def test_large_alphabets(ctx, oracle):
+    rng = np.random.default_rng(9)
+    # ~1500 symbols: block codebook builder, shared-memory sort
+    x = (rng.standard_normal(60000) * 0.3).astype(np.float32)
+    roundtrip(oracle, x, 4, 1e-3, 2)
+    # > 4096-code span: wide histogram pool; > 1024 symbols sorted in global scratch
+    x = (rng.standard_normal(80000) * 1.0).astype(np.float32)
+    roundtrip(oracle, x, 8, 1e-4, 2)
+
+
+def test_decoder_symbols_past_16_bits(ctx, oracle):
+    # 70000 distinct codes: the decoder stores symbols straight to the output
+    x = (np.arange(70000, dtype=np.float64) * 0.02 - 700.0).astype(np.float32)
+    np.random.default_rng(3).shuffle(x)
+    roundtrip(oracle, x, 7, 0.01, 2)
+
+
+def test_packed_mixed_call(ctx, oracle):
+    rng = np.random.default_rng(17)
+    jobs, want = [], []
+    shapes = [(2048, 16), (300, 64), (1, 3), (0, 8), (4096, 1), (64, 1500), (1000, 33)]
+    for k, (n, dim) in enumerate(shapes):
+        for codec in (0, 1, 2):
+            if n == 0 and codec == 2:
+                continue  # huffman on an empty batch is a ValueError (tested elsewhere)
+            rows = (rng.standard_normal((max(1, n // 7), dim)) * 0.05).astype(np.float32)
+            x = rows[rng.integers(0, len(rows), n)] if n else np.zeros((0, dim), np.float32)
+            eb = [0.01, 0.003, 0.05][k % 3]
+            jobs.append(K.EncodeJob(dev(x), eb, codec))
+            want.append(oracle.encode_chunk(x.astype(np.float64).ravel(), dim, eb, codec))
+    buf = K.pack_encode(jobs)
+    table = K.unpack_table(buf)
+    assert [buf[o:o + ln] for o, ln in table] == want
+    outs = K.decode_packed(buf, K.OUT_F64)
+    for o, w in zip(outs, want):
+        assert np.array_equal(o.cpu().numpy().ravel().view(np.uint64), oracle.decode_chunk(w).ravel().view(np.uint64))
+    # only the vlz chunk wider than the parallel decoder's envelope (dim > 1023) takes the sequential walker
+    assert K.decode_fallbacks() == 1
