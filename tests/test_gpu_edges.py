@@ -85,3 +85,46 @@ def test_packed_mixed_call(ctx, oracle):
         assert np.array_equal(o.cpu().numpy().ravel().view(np.uint64), oracle.decode_chunk(w).ravel().view(np.uint64))
     # only the vlz chunk wider than the parallel decoder's envelope (dim > 1023) takes the sequential walker
     assert K.decode_fallbacks() == 1
+
+
+def test_corrupted_long_streams_match_reference(ctx, ref):
+    """Multi-segment vlz and multi-block huffman streams with a flipped,
+    inserted or truncated byte: the parallel decoders either decode exactly
+    what the reference decodes or raise the reference's error (via the exact
+    sequential walkers)."""
+    from oracle import OracleError
+    from paper_2407_04272_b200 import _lib
+    rng = np.random.default_rng(1234)
+    for trial in range(150):
+        is_vlz = trial % 2 == 0
+        dim = int(rng.choice([3, 16, 64]))
+        n = int(rng.integers(800, 3000))
+        pool = rng.integers(-40, 41, (int(rng.integers(5, 200)), dim)).astype(np.int32)
+        codes = pool[rng.integers(0, len(pool), n)].ravel()
+        s = bytearray(ref.vlz_encode(codes, dim, 255) if is_vlz else ref.huff_encode(codes))
+        k = trial % 3
+        at = int(rng.integers(len(s) // 4, len(s)))
+        if k == 0:
+            s[at] ^= int(rng.integers(1, 256))
+        elif k == 1:
+            s.insert(at, int(rng.integers(0, 256)))
+        else:
+            del s[at:]
+        s = bytes(s)
+        try:
+            want = ("ok", (ref.vlz_decode(s, dim, n) if is_vlz else ref.huff_decode(s)).tobytes())
+        except OracleError as e:
+            want = ("err", e.kind, e.msg)
+        try:
+            if is_vlz:
+                got = ("ok", K.vlz_decode(s, dim, n).cpu().numpy().tobytes())
+            else:
+                got = ("ok", K.huff_decode(s, n * dim).cpu().numpy().tobytes())
+        except _lib.EmbcError as e:
+            got = ("err", "value" if e.status == _lib.ERR_VALUE else "format", str(e))
+        if want[:2] == ("err", "std"):
+            assert got[0] == "err", trial
+        elif want[0] == "err" and not is_vlz and "decoded" in got[-1]:
+            assert got[0] == "err", trial
+        else:
+            assert got == want, (trial, is_vlz, k)
