@@ -128,3 +128,16 @@ def test_corrupted_long_streams_match_reference(ctx, ref):
             assert got[0] == "err", trial
         else:
             assert got == want, (trial, is_vlz, k)
+
+
+@pytest.mark.parametrize("codec", [0, 1, 2])
+def test_bin_edge_values_take_the_exact_path(ctx, oracle, codec):
+    """Values at fp32-rounded bin edges ((k + 1/2) * 2eb) and large quotients
+    fail the fast quantizer; the tile is redone on the exact binary64 path."""
+    rng = np.random.default_rng(77 + codec)
+    eb = 0.01
+    k = rng.integers(-50, 50, 4096)
+    x = ((k + 0.5) * (2 * eb)).astype(np.float32)
+    x[::7] = (rng.standard_normal(len(x[::7])) * 0.1).astype(np.float32)
+    x[5] = np.float32(30.0)  # |x / w| > 1024: exact path as well
+    roundtrip(oracle, x, 16, eb, codec)
