@@ -359,8 +359,10 @@ def run_single(args):
     e2e_steps = min(args.steps, 60)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s_h2d)
+    th0 = time.perf_counter()
     for k in range(e2e_steps):
         e2e_step(k)
+    host_enqueue_ms = (time.perf_counter() - th0) * 1e3 / e2e_steps
     e1.record(s_d2h)
     torch.cuda.synchronize()
     ctx.sync()
@@ -397,6 +399,7 @@ def run_single(args):
                    "graph": use_graph, "parallelism": "single GPU"},
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": step_bytes,
                 "d2h_bytes_per_step": step_bytes, "ms_per_step": round(e2e_ms, 4),
+                "host_enqueue_ms_per_step": round(host_enqueue_ms, 4),
                 "pipeline": "H2D / kernels / D2H on three streams, steps overlapped; the compress + decompress "
                             "calls of each slot replayed from a CUDA graph" if use_graph else
                             "H2D / kernels / D2H on three streams, steps overlapped"},
