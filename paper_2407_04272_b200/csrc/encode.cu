@@ -809,6 +809,61 @@ __device__ __forceinline__ void copy_range(uint8_t* dst, const uint8_t* stage, u
   copy_out_staged(dst + a, stage + (mis + a - m2), b - a);
 }
 
+// One chunk's records: pack table entry (container.hpp:244-250), header
+// (container.hpp:74-85), 25-B metadata (container.hpp:196-209), offsets.
+__device__ void write_job_records(const EmitArgs& a, uint32_t j, uint64_t start, uint64_t P) {
+  const DJob& J = a.jobs[j];
+  const uint64_t len = J.header + P;
+  if (a.d_offsets) a.d_offsets[j] = start;
+  if (a.d_lengths) a.d_lengths[j] = len;
+  if (a.layout == EMBC_LAYOUT_PACKED && 20 + 16ull * j <= a.cap) {
+    st_le(a.out + 4 + 16ull * j, start, 8);
+    st_le(a.out + 12 + 16ull * j, len, 8);
+  }
+  uint64_t ebits;
+  memcpy(&ebits, &J.qp.eb, 8);
+  if (J.header && start + kHeader <= a.cap) {
+    uint8_t* h = a.out + start;
+    h[0] = 'E';
+    h[1] = 'M';
+    h[2] = 'B';
+    h[3] = 'C';
+    h[4] = 1;
+    h[5] = J.codec;
+    st_le(h + 6, ebits, 8);
+    st_le(h + 14, J.dim, 4);
+    st_le(h + 18, J.n, 4);
+    st_le(h + 22, P, 8);
+  }
+  if (a.d_meta) {
+    uint8_t* m = a.d_meta + static_cast<uint64_t>(kMetaSize) * j;
+    st_le(m, kHeader + P, 8);
+    m[8] = J.codec;
+    st_le(m + 9, ebits, 8);
+    st_le(m + 17, J.dim, 4);
+    st_le(m + 21, J.n, 4);
+  }
+}
+
+// The call's total: d_total, or the capacity error (then nothing more is written).
+__device__ void finish_call(const EmitArgs& a, uint64_t total) {
+  if (total > a.cap) {
+    if (a.d_total) *a.d_total = 0;
+    a.flags[CF_ABORT] |= JF_ABORT;
+    if (!a.err->valid) {
+      a.err->valid = 1;
+      a.err->job = 0;
+      a.err->reason = EMBC_R_CAPACITY;
+      a.err->index = 0;
+      a.err->a = total;
+      a.err->b = a.cap;
+      a.err->status = EMBC_ERR_CAPACITY;
+    }
+  } else if (a.d_total) {
+    *a.d_total = total;
+  }
+}
+
 // Layout of the call (the last phase-0 CTA): tile offsets inside each job's
 // payload (bits), chunk offsets in job order (container.hpp:245-250), chunk
 // headers (container.hpp:74-85), pack table (container.hpp:244-250), 25-B
@@ -907,17 +962,25 @@ __device__ void layout_tail(const EmitArgs& a) {
   }
 }
 
-__global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
+// PHASE 0: sizes + layout (last CTA); 1: bytes; 2: fused (sizes, look-back, bytes)
+template <int PHASE>
+__global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_tmp32[33];
   __shared__ unsigned long long s_tmp64[33];
-  const uint32_t tid = blockIdx.x;
+  __shared__ uint32_t s_t;
+  __shared__ unsigned long long s_pre, s_start;
+  // phase 2 (fused, small calls): tiles in ticket order, so the look-back only
+  // ever waits on CTAs that are already running
+  if (threadIdx.x == 0) s_t = PHASE == 2 ? atomicAdd(&a.flags[CF_TICKET], 1u) : blockIdx.x;
+  __syncthreads();
+  const uint32_t tid = s_t;
   TS(0);
   if (*reinterpret_cast<volatile uint32_t*>(&a.flags[CF_ABORT]) & JF_ABORT) {
-    if (tid == 0 && a.phase == 0 && !a.d_stats) fold_failure(a);
+    if (tid == 0 && PHASE != 1 && !a.d_stats) fold_failure(a);
     return;
   }
-  const int phase = a.phase;
+  constexpr int phase = PHASE;
   const DTile T = a.tiles[tid];
   const uint32_t jid = T.job;
   const DJob J = a.jobs[jid];  // by value: the fields live in registers, not re-read after global stores
@@ -1210,7 +1273,51 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
   TS(2);
   const uint64_t hdr = J.header;
   const uint64_t book_bytes = codec == EMBC_CODEC_HUFFMAN ? 12 + 5ull * S.nsym : 0;
-  if (phase == 0) {
+  uint64_t pre = 0, start = 0;
+  if (phase == 2) {
+    // ---- 3c. fused: decoupled look-back over the job's tiles (bits), then over jobs (bytes)
+    if (threadIdx.x == 0 && jid > 0) {
+      // the job's size is known once every tile of it is sized: the last one to
+      // get here publishes it, so later jobs never wait on this job's look-back
+      unsigned long long* js = a.job_status + jid * kJobStride;
+      atomicAdd(js + 1, static_cast<unsigned long long>(my_bits));
+      __threadfence();
+      if (atomicAdd(js + 2, 1ull) == J.ntiles - 1) {
+        __threadfence();
+        const unsigned long long bits = atomicAdd(js + 1, 0ull);
+        const unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(js);
+        if ((w >> 62) == 0) atomicCAS(js, 0ull, kFlagAgg | (hdr + book_bytes + (bits + 7) / 8));
+      }
+    }
+
+    if (threadIdx.x < 32) {
+      uint64_t p = 0;
+      if (first) {
+        if (threadIdx.x == 0) st_status(a.tile_status + tid, kFlagInc | my_bits);
+      } else {
+        if (threadIdx.x == 0) st_status(a.tile_status + tid, kFlagAgg | my_bits);
+        p = look_back(a.tile_status, J.tile0, tid, 0);
+        if (threadIdx.x == 0) st_status(a.tile_status + tid, kFlagInc | (p + my_bits));
+      }
+      const uint64_t job_bytes = hdr + book_bytes + (p + my_bits + 7) / 8;
+      const uint64_t base = a.layout == EMBC_LAYOUT_PACKED ? 4 + 16ull * a.njobs : 0;
+      const uint64_t st0 = jid == 0 ? base : look_back(a.job_status, 0, jid, 0, kJobStride);
+      if (last && threadIdx.x == 0) st_status(a.job_status + jid * kJobStride, kFlagInc | (st0 + job_bytes));
+      if (threadIdx.x == 0) {
+        s_pre = p;
+        s_start = st0;
+      }
+    }
+    __syncthreads();
+    pre = s_pre;
+    start = s_start;
+    if (last && threadIdx.x == 0) {  // the job's records (header, pack table, metadata)
+      const uint64_t P = book_bytes + (pre + my_bits + 7) / 8;
+      write_job_records(a, jid, start, P);
+      if (tid == a.ntiles - 1) finish_call(a, start + hdr + P);
+    }
+    if (tid == 0 && threadIdx.x == 0 && a.layout == EMBC_LAYOUT_PACKED && a.cap >= 4) st_le(a.out, a.njobs, 4);
+  } else if (phase == 0) {
     // ---- 3a. sizes out; the last CTA to finish lays the call out
     __shared__ int s_last;
     if (threadIdx.x == 0) a.tile_bits[tid] = my_bits;
@@ -1223,9 +1330,11 @@ __global__ void __launch_bounds__(kBlock, 5) k_emit(EmitArgs a) {
     layout_tail(a);
     return;
   }
-  // ---- 3b. offsets from the layout
-  if (*reinterpret_cast<volatile uint32_t*>(&a.flags[CF_ABORT]) & JF_ABORT) return;  // capacity
-  const uint64_t pre = a.tile_off[tid], start = a.job_start[jid];
+  if (phase == 1) {  // ---- 3b. offsets from the layout
+    if (*reinterpret_cast<volatile uint32_t*>(&a.flags[CF_ABORT]) & JF_ABORT) return;  // capacity
+    pre = a.tile_off[tid];
+    start = a.job_start[jid];
+  }
   const uint64_t pay_end = start + hdr + book_bytes + (pre + my_bits + 7) / 8;  // end of this tile's bytes
   uint8_t* pay = a.out + start + hdr;
 #ifdef EMBC_DEBUG
@@ -1707,11 +1816,19 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   ea.tile_off = reinterpret_cast<uint64_t*>(d + o_toff);
   ea.job_start = reinterpret_cast<uint64_t*>(d + o_jstart);
   ea.done = sa.book.flags + CF_TICKET;  // zeroed by k_stats
-  ea.phase = 0;
-  EMBC_TIMED(ctx, "k_sizes", stream, k_emit<<<ntiles, kBlock, emit_smem, stream>>>(ea));
-  if (!d_stats) {
-    ea.phase = 1;
-    EMBC_TIMED(ctx, "k_emit", stream, k_emit<<<ntiles, kBlock, emit_smem, stream>>>(ea));
+  // small calls: one fused pass (sizes, decoupled look-back, bytes) -- the
+  // look-back is cheap when every tile is resident at once; large calls: sizes
+  // + layout, then bytes, with no waiting at all
+  if (!d_stats && ntiles <= 1024) {
+    ea.phase = 2;
+    EMBC_TIMED(ctx, "k_emit", stream, k_emit<2><<<ntiles, kBlock, emit_smem, stream>>>(ea));
+  } else {
+    ea.phase = 0;
+    EMBC_TIMED(ctx, "k_sizes", stream, k_emit<0><<<ntiles, kBlock, emit_smem, stream>>>(ea));
+    if (!d_stats) {
+      ea.phase = 1;
+      EMBC_TIMED(ctx, "k_emit", stream, k_emit<1><<<ntiles, kBlock, emit_smem, stream>>>(ea));
+    }
   }
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "encode launch");
@@ -1719,7 +1836,9 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
 }
 
 cudaError_t encode_set_attributes() {
-  cudaError_t e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmemMax);
+  cudaError_t e = cudaFuncSetAttribute(k_emit<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmemMax);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_emit<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmemMax);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_emit<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmemMax);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, kStatsSmemMax);
 }

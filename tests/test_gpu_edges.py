@@ -141,3 +141,19 @@ def test_bin_edge_values_take_the_exact_path(ctx, oracle, codec):
     x[::7] = (rng.standard_normal(len(x[::7])) * 0.1).astype(np.float32)
     x[5] = np.float32(30.0)  # |x / w| > 1024: exact path as well
     roundtrip(oracle, x, 16, eb, codec)
+
+
+def test_two_pass_encode_large_call(ctx, oracle):
+    """> 1024 tiles: the encoder runs its two-pass mode (sizes + layout, then
+    bytes) instead of the fused single pass; bytes equal the reference's."""
+    rng = np.random.default_rng(2048)
+    jobs, want = [], []
+    for t in range(5):
+        pool = (rng.standard_normal((300, 128)) * 0.05).astype(np.float32)
+        x = pool[rng.integers(0, 300, 8192)]
+        codec = [1, 2, 0, 1, 2][t]
+        jobs.append(K.EncodeJob(dev(x), 0.01, codec))
+        want.append(oracle.encode_chunk(x.astype(np.float64).ravel(), 128, 0.01, codec))
+    buf = K.pack_encode(jobs)
+    table = K.unpack_table(buf)
+    assert [buf[o:o + ln] for o, ln in table] == want
