@@ -1429,7 +1429,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
 // ===========================================================================
 constexpr uint32_t kDecSmem = kVlzSmem > kHuffSmem ? kVlzSmem : kHuffSmem;
 
-__global__ void __launch_bounds__(kBlock, 5) k_dec_main(DecArgs a) {
+__global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_t;
   if (threadIdx.x == 0) s_t = atomicAdd(&a.tickets[0], 1u);

@@ -498,7 +498,7 @@ struct StatsArgs {
   uint32_t hist_off;  // dynamic smem offset of the histogram window
 };
 
-__global__ void __launch_bounds__(kBlock, 5) k_stats(StatsArgs a) {
+__global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ unsigned long long s_err;
   __shared__ int s_min, s_max, s_last;
