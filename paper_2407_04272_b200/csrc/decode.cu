@@ -324,6 +324,144 @@ __device__ __forceinline__ uint64_t value_bits(int32_t code, double w, int kind)
   return static_cast<uint32_t>(code);
 }
 
+// Codebook of <= 64 entries: validation (huffman.hpp:132-148, entry order),
+// canonical codes (finalize, :165-186), duplicate check (:183-185) by one warp
+// in registers (two entries per lane); the prefix LUT by the whole CTA.
+__device__ void huff_tables_small(const DChunk& C, DecState& S, const uint8_t* p, uint64_t L, HView hv, HTab& tb,
+                                  uint64_t* starts, uint32_t c, uint32_t* __restrict__ hflag) {
+  __shared__ int s_stop2;
+  const uint32_t nent = S.nent;
+  const uint32_t lane = threadIdx.x & 31;
+  if (threadIdx.x < 33) {
+    tb.count[threadIdx.x] = 0;
+    tb.first[threadIdx.x] = 0;
+    tb.base[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) s_stop2 = 0;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t sym[2], len[2];
+    unsigned long long bad = ~0ull, kraft = 0;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint32_t i = r * 32 + lane;
+      sym[r] = 0;
+      len[r] = 0;
+      if (i < nent) {
+        sym[r] = static_cast<uint32_t>(ld_be(p + 12 + 5ull * i, 4));
+        len[r] = p[12 + 5ull * i + 4];
+        if (len[r] == 0 || len[r] > 32) bad = min(bad, (static_cast<unsigned long long>(i) << 8) | len[r]);
+        else kraft += 1ull << (32 - len[r]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+      kraft += __shfl_xor_sync(0xffffffffu, kraft, o);
+    }
+    if (bad != ~0ull || kraft > (1ull << 32)) {  // length range in entry order, then Kraft
+      if (lane == 0) {
+        if (bad != ~0ull) dec_fail(S, bad >> 8, EMBC_R_HUF_LEN_RANGE, bad & 0xFF, 0);
+        else dec_fail(S, 0, EMBC_R_HUF_KRAFT, 0, 0);
+        s_stop2 = 1;
+      }
+    } else {
+      // canonical order (length, symbol)
+      uint64_t k[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+        k[r] = r * 32 + lane < nent ? (static_cast<uint64_t>(len[r]) << 32) | (sym[r] ^ 0x80000000u) : ~0ull;
+      warp_sort_regs<2>(k);
+      const double w = 2.0 * S.eb;
+      unsigned long long carry = 0;
+      uint32_t prev_last = 0;  // length of the previous register's last element
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t i = r * 32 + lane;
+        const bool v = i < nent;
+        const uint32_t ln = v ? static_cast<uint32_t>(k[r] >> 32) : 0;
+        const unsigned long long kr = v ? (1ull << (32 - ln)) : 0;
+        const unsigned long long inc = warp_incl_scan<unsigned long long>(kr);
+        const uint32_t lp = __shfl_up_sync(0xffffffffu, ln, 1);
+        const uint32_t lprev = lane ? lp : prev_last;
+        if (v) {
+          const uint32_t code = static_cast<uint32_t>((carry + inc - kr) >> (32 - ln));
+          const uint32_t sy = static_cast<uint32_t>(k[r]) ^ 0x80000000u;
+          if (i == 0 || lprev != ln) {
+            tb.first[ln] = code;
+            tb.base[ln] = i;
+          }
+          atomicAdd(&tb.count[ln], 1u);
+          hv.syms[i] = static_cast<int32_t>(sy);
+          hv.vals[i] = value_bits(static_cast<int32_t>(sy), w, C.out_kind);
+          starts[i] = (static_cast<uint64_t>(code) << (32 - ln)) | (static_cast<uint64_t>(ln) << 56);
+        }
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+        prev_last = __shfl_sync(0xffffffffu, ln, 31);
+      }
+      // duplicate symbols (huffman.hpp:183-185): sort by symbol, compare neighbours
+      uint64_t d[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+        d[r] = r * 32 + lane < nent ? (static_cast<uint64_t>(static_cast<uint32_t>(k[r]) ) << 32) | (r * 32 + lane) : ~0ull;
+      warp_sort_regs<2>(d);
+      bool dup = false;
+      uint64_t prevd = 0;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t i = r * 32 + lane;
+        const uint64_t up = __shfl_up_sync(0xffffffffu, d[r], 1);
+        const uint64_t before = lane ? up : prevd;
+        if (i > 0 && i < nent && (before >> 32) == (d[r] >> 32)) dup = true;
+        prevd = __shfl_sync(0xffffffffu, d[r], 31);
+      }
+      if (__any_sync(0xffffffffu, dup) && lane == 0) {
+        dec_fail(S, 0, EMBC_R_HUF_DUP, 0, 0);
+        s_stop2 = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_stop2) return;
+  // left-aligned code starts ascending in canonical order -> prefix LUT
+  for (uint32_t sl = threadIdx.x; sl < (1u << kL0); sl += blockDim.x) {
+    const uint64_t V = static_cast<uint64_t>(sl) << (32 - kL0);
+    const uint64_t Vend = V + (1ull << (32 - kL0));
+    int lo = 0, hi = static_cast<int>(nent) - 1, f = -1;
+    while (lo <= hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((starts[mid] & 0xFFFFFFFFFFull) <= V) {
+        f = mid;
+        lo = mid + 1;
+      } else {
+        hi = mid - 1;
+      }
+    }
+    uint32_t ent = 0;
+    if (f >= 0) {
+      const uint32_t ln = static_cast<uint32_t>(starts[f] >> 56);
+      const uint64_t a0 = starts[f] & 0xFFFFFFFFFFull;
+      if (V < a0 + (1ull << (32 - ln))) ent = ln <= kL0 ? (static_cast<uint32_t>(f) << 6) | ln : kLong;
+    }
+    if (!ent && f + 1 < static_cast<int>(nent) && (starts[f + 1] & 0xFFFFFFFFFFull) < Vend) ent = kLong;
+    hv.lut[sl] = ent;
+  }
+  if (threadIdx.x == 0) {
+    uint32_t max_len = 0;  // entries().back().length (huffman.hpp:257)
+    for (uint32_t l = 1; l <= 32; ++l)
+      if (tb.count[l]) max_len = l;
+    tb.max_len = max_len;
+    tb.nent = nent;
+    tb.nsym = S.nsym;
+    tb.bit_off = 12 + 5ull * nent;
+    tb.nbits = 8 * (L - tb.bit_off);
+    *hv.tab = tb;
+    S.max_len = max_len;
+    S.bit_off = tb.bit_off;
+    if (S.nsym != C.N) hflag[c] = 1;  // decoded count != dim*count (container.hpp:169-172)
+  }
+}
+
 __device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState& S,
                             uint64_t* __restrict__ keys, uint8_t* __restrict__ tabs,
                             uint32_t* __restrict__ hflag, uint64_t* skey, uint32_t skey_cap) {
@@ -371,6 +509,10 @@ __device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState&
   __syncthreads();
   if (s_stop) return;
   const uint32_t nent = S.nent;
+  if (nent <= 64 && skey_cap >= 64) {  // small codebooks: one warp in registers, the LUT by the CTA
+    huff_tables_small(C, S, p, L, hv, tb, reinterpret_cast<uint64_t*>(skey), c, hflag);
+    return;
+  }
   // length range, in entry order (huffman.hpp:137-141), and Kraft sum
   unsigned long long kraft = 0;
   for (uint32_t i = threadIdx.x; i < nent; i += blockDim.x) {
