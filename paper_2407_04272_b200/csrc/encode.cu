@@ -498,6 +498,79 @@ struct StatsArgs {
   uint32_t hist_off;  // dynamic smem offset of the histogram window
 };
 
+// E1's vector loop, one instantiation per codec (no codec branches inside):
+// 128-bit loads, 4 quads in flight per thread; a vlz row is qpr consecutive lanes.
+template <int CODEC>
+__device__ __forceinline__ void stats_vec(const DJob& J, uint64_t e0, uint32_t ne, uint32_t qpr, uint64_t gbase,
+                                          uint64_t* __restrict__ row_info, uint32_t* shist, unsigned long long& lerr,
+                                          int& lmin, int& lmax, bool& lwide) {
+  constexpr bool vlz = CODEC == EMBC_CODEC_VLZ, huf = CODEC == EMBC_CODEC_HUFFMAN;
+  const uint32_t nq = ne >> 2;
+  const QParams qp = J.qp;
+  const bool f32 = J.src_kind == EMBC_SRC_F32;
+  const uint4* src4 = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(J.src) + e0);
+  uint32_t ck[4] = {0, 0, 0, 0};  // this thread's columns are fixed: q % qpr == threadIdx.x % qpr
+  if (vlz)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ck[k] = col_key((threadIdx.x & (qpr - 1)) * 4 + k);
+  for (uint32_t base = 0; base < nq; base += 4 * kBlock) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t q = base + u * kBlock + threadIdx.x;
+      if (q < nq) v[u] = __ldg(src4 + q);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t q = base + u * kBlock + threadIdx.x;
+      const bool ok = q < nq;
+      int32_t c[4] = {0, 0, 0, 0};
+      if (ok) {
+        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (f32) {
+            uint32_t reason = 0;
+            c[k] = quantize_f32(__uint_as_float(w[k]), qp, &reason);
+            if (reason) lerr = min(lerr, static_cast<unsigned long long>(err_key(e0 + 4ull * q + k, reason)));
+          } else {
+            c[k] = static_cast<int32_t>(w[k]);
+          }
+          if (huf) {
+            lmin = min(lmin, c[k]);
+            lmax = max(lmax, c[k]);
+          }
+        }
+      }
+      if (huf) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t bin = 0xFFFFFFFFu;
+          if (ok) {
+            const uint32_t b = static_cast<uint32_t>(c[k] + static_cast<int32_t>(kWin / 2));
+            if (b < kWin) bin = b;
+            else lwide = true;
+          }
+          hist_add(shist, bin);
+        }
+      }
+      if (vlz) {
+        uint32_t h = 0, lit = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          h += static_cast<uint32_t>(c[k]) * ck[k];
+          lit += varint_len(zigzag(c[k]));
+        }
+        for (uint32_t o = 1; o < qpr; o <<= 1) {
+          h += __shfl_xor_sync(0xffffffffu, h, o);
+          lit += __shfl_xor_sync(0xffffffffu, lit, o);
+        }
+        if (ok && (q & (qpr - 1)) == 0) row_info[gbase + q / qpr] = (static_cast<uint64_t>(1 + lit) << 32) | h;
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ unsigned long long s_err;
@@ -538,72 +611,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
                    (!vlz || (qpr <= 32 && (qpr & (qpr - 1)) == 0));
   const uint64_t gbase = J.row_base + T.row0;
   if (vec) {
-    // 128-bit loads, 4 quads in flight per thread; a row is qpr consecutive lanes
-    const uint32_t nq = ne >> 2;
-    const QParams qp = J.qp;
-    const bool f32 = J.src_kind == EMBC_SRC_F32;
-    const uint4* src4 = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(J.src) + e0);
-    uint32_t ck[4] = {0, 0, 0, 0};  // this thread's columns are fixed: q % qpr == threadIdx.x % qpr
-    if (vlz)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) ck[k] = col_key((threadIdx.x & (qpr - 1)) * 4 + k);
-    for (uint32_t base = 0; base < nq; base += 4 * kBlock) {
-      uint4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t q = base + u * kBlock + threadIdx.x;
-        if (q < nq) v[u] = __ldg(src4 + q);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t q = base + u * kBlock + threadIdx.x;
-        const bool ok = q < nq;
-        int32_t c[4] = {0, 0, 0, 0};
-        if (ok) {
-          const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (f32) {
-              uint32_t reason = 0;
-              c[k] = quantize_f32(__uint_as_float(w[k]), qp, &reason);
-              if (reason) lerr = min(lerr, static_cast<unsigned long long>(err_key(e0 + 4ull * q + k, reason)));
-            } else {
-              c[k] = static_cast<int32_t>(w[k]);
-            }
-            if (huf) {
-              lmin = min(lmin, c[k]);
-              lmax = max(lmax, c[k]);
-            }
-          }
-        }
-        if (huf) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint32_t bin = 0xFFFFFFFFu;
-            if (ok) {
-              const uint32_t b = static_cast<uint32_t>(c[k] + static_cast<int32_t>(kWin / 2));
-              if (b < kWin) bin = b;
-              else lwide = true;
-            }
-            hist_add(shist, bin);
-          }
-        }
-        if (vlz) {
-          uint32_t h = 0, lit = 0;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            h += static_cast<uint32_t>(c[k]) * ck[k];
-            lit += varint_len(zigzag(c[k]));
-          }
-          for (uint32_t o = 1; o < qpr; o <<= 1) {
-            h += __shfl_xor_sync(0xffffffffu, h, o);
-            lit += __shfl_xor_sync(0xffffffffu, lit, o);
-          }
-          if (ok && (q & (qpr - 1)) == 0)
-            a.row_info[gbase + q / qpr] = (static_cast<uint64_t>(1 + lit) << 32) | h;
-        }
-      }
-    }
+    if (vlz) stats_vec<EMBC_CODEC_VLZ>(J, e0, ne, qpr, gbase, a.row_info, shist, lerr, lmin, lmax, lwide);
+    else if (huf) stats_vec<EMBC_CODEC_HUFFMAN>(J, e0, ne, qpr, gbase, a.row_info, shist, lerr, lmin, lmax, lwide);
+    else stats_vec<EMBC_CODEC_RAW>(J, e0, ne, qpr, gbase, a.row_info, shist, lerr, lmin, lmax, lwide);
   } else {
     // generic path: element loop, vlz codes staged at r * (dim|1) + col
     int32_t* codes = reinterpret_cast<int32_t*>(smem);
