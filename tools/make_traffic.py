@@ -10,10 +10,9 @@ out = {}
 for arg in sys.argv[1:]:
     wl, path = arg.split("=", 1)
     per, seen = {}, 0
+    names = {"void k_emit<0>": "k_sizes", "void k_emit<1>": "k_emit", "void k_emit<2>": "k_emit"}
     for name, us, rd, wr in launches(path):
-        if name == "k_emit":
-            name = "k_sizes" if seen % 2 == 0 else "k_emit"
-            seen += 1
+        name = names.get(name, name)
         per.setdefault(name, []).append((rd + wr) * 1e6)
     out[wl] = {"source": os.path.basename(path), "bytes_per_launch": {k: sum(v) / len(v) for k, v in per.items()}}
 json.dump(out, open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json"), "w"),
