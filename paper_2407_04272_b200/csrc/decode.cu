@@ -1557,12 +1557,24 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   // ---- coalesced stores of this block's symbols
   const uint32_t own = pk_cnt(BM[static_cast<uint32_t>(s_in >> 55) & 31]);
   const uint64_t nout = umin64(own, N - blk_base);
-  if (C.out_kind == EMBC_OUT_F64) {
+  // the decode LUT is dead now: its bytes hold the per-entry output values
+  const bool f64 = C.out_kind == EMBC_OUT_F64;
+  const bool vstage = nent <= (f64 ? (1u << kL0) / 2 : (1u << kL0));
+  if (vstage) {
+    if (f64)
+      for (uint32_t k = threadIdx.x; k < nent; k += blockDim.x) reinterpret_cast<uint64_t*>(lut)[k] = __ldcg(vals + k);
+    else
+      for (uint32_t k = threadIdx.x; k < nent; k += blockDim.x) lut[k] = static_cast<uint32_t>(__ldcg(vals + k));
+    __syncthreads();
+  }
+  if (f64) {
     uint64_t* o = static_cast<uint64_t*>(C.out) + blk_base;
-    for (uint32_t k = threadIdx.x; k < nout; k += blockDim.x) o[k] = __ldcg(vals + outs[k]);
+    const uint64_t* sv = reinterpret_cast<const uint64_t*>(lut);
+    for (uint32_t k = threadIdx.x; k < nout; k += blockDim.x) o[k] = vstage ? sv[outs[k]] : __ldcg(vals + outs[k]);
   } else {
     uint32_t* o = static_cast<uint32_t*>(C.out) + blk_base;
-    for (uint32_t k = threadIdx.x; k < nout; k += blockDim.x) o[k] = static_cast<uint32_t>(__ldcg(vals + outs[k]));
+    for (uint32_t k = threadIdx.x; k < nout; k += blockDim.x)
+      o[k] = vstage ? lut[outs[k]] : static_cast<uint32_t>(__ldcg(vals + outs[k]));
   }
 }
 
