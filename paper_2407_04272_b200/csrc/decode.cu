@@ -1251,11 +1251,9 @@ __device__ void vlz_roots(const DecArgs& a, uint32_t c, uint8_t* smem) {
 constexpr uint32_t kHSub = 256;                        // subsequences per block (one per thread)
 constexpr uint32_t kHBits = kSubBits * kHSub;          // 8192 bits
 constexpr uint32_t kHPre = 2;                          // words staged before the block (warm-up)
-constexpr uint32_t kHWords = kHPre + kHBits / 32 + 4;  // + look-ahead past the block
-constexpr uint32_t kHOut = kHBits;                     // at most one symbol per bit
-// smem: LUT | staged words | per-subsequence chain summaries | group states, later the symbols (u16)
+// smem: LUT | two-codeword LUT | staged words | per-subsequence chain summaries | group states, later the symbols (u16)
 __host__ __device__ constexpr uint32_t huff_smem(uint32_t hsub) {
-  return (1u << kL0) * 4 + (((kHPre + hsub * 2 + 4) * 4 + 15) & ~15u) + hsub * 20 +
+  return (1u << kL0) * 4 + (1u << kL0) * 2 + (((kHPre + hsub * 2 + 4) * 4 + 15) & ~15u) + hsub * 20 +
          (hsub * 33 * 4 > hsub * kSubBits * 2 ? hsub * 33 * 4 : hsub * kSubBits * 2);
 }
 constexpr uint32_t kHuffSmem = huff_smem(kHSub);
@@ -1292,7 +1290,8 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   const uint32_t b = gb - C.blk0;
   const uint32_t hsub = a.hsub, hbits = hsub * kSubBits, hwords = kHPre + hbits / 32 + 4;
   uint32_t* lut = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* W = lut + (1u << kL0);
+  uint16_t* luta = reinterpret_cast<uint16_t*>(lut + (1u << kL0));  // two-codeword steps (lengths only)
+  uint32_t* W = lut + (1u << kL0) + (1u << kL0) / 2;
   uint64_t* B0 = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(W) + ((hwords * 4 + 15) & ~15u));
   uint32_t* X0 = reinterpret_cast<uint32_t*>(B0 + hsub);
   uint32_t* Y0 = X0 + hsub;
@@ -1322,6 +1321,27 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   for (uint32_t i = threadIdx.x; i < sizeof(HTab) / 4; i += blockDim.x)
     reinterpret_cast<uint32_t*>(&t)[i] = __ldcg(reinterpret_cast<const unsigned int*>(hv.tab) + i);
   __syncthreads();
+  // two codewords per lookup when both fit the kL0-bit window:
+  // luta = len1 | len2 << 5 | n << 10  (n: 0 long code, 1 one codeword, 2 two, 3 invalid prefix)
+  for (uint32_t w = threadIdx.x; w < (1u << kL0); w += blockDim.x) {
+    const uint32_t e1 = lut[w];
+    uint32_t v;
+    if (e1 == 0) v = 3u << 10;
+    else if (e1 == kLong) v = 0;
+    else {
+      const uint32_t l1 = e1 & 63, rem = kL0 - l1;
+      uint32_t n = 1, l2 = 0;
+      if (rem) {
+        const uint32_t e2 = lut[(w << l1) & ((1u << kL0) - 1)];
+        if (e2 != 0 && e2 != kLong && (e2 & 63) <= rem) {
+          n = 2;
+          l2 = e2 & 63;
+        }
+      }
+      v = l1 | (l2 << 5) | (n << 10);
+    }
+    luta[w] = static_cast<uint16_t>(v);
+  }
   const uint64_t bit0 = static_cast<uint64_t>(b) * hbits;
   const uint8_t* bits = C.in + __ldcg(reinterpret_cast<const unsigned long long*>(&S.pay_off)) + t.bit_off;
   // W[kHPre + k] = word k of the block; the two words before hold the previous block's tail
@@ -1345,8 +1365,18 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
       if (q >= kSubBits) return pk(q - kSubBits, 0, n);
       if ((stop >> q) & 1) return pk(pk_off(xs), pk_term(xs), n + pk_cnt(xs) - popc_below(stop, q));
       if (gbase + q >= nbits) return pk(0, 2, n);
+      const uint32_t bits = speek(W, (kHPre * 32) + i * kSubBits + q);
+      const uint32_t la = luta[bits >> (32 - kL0)];
+      if ((la >> 10) == 2) {
+        const uint32_t l1 = la & 31, l12 = l1 + ((la >> 5) & 31);
+        if (q + l1 < kSubBits && !((stop >> (q + l1)) & 1) && gbase + q + l12 <= nbits) {
+          q += l12;
+          n += 2;
+          continue;
+        }
+      }
       uint32_t len = 0;
-      if (decode_one(lut, t, speek(W, (kHPre * 32) + i * kSubBits + q), &len) < 0) return pk(0, 1, n);
+      if (decode_one(lut, t, bits, &len) < 0) return pk(0, 1, n);
       if (gbase + q + len > nbits) return pk(0, 2, n);
       q += len;
       ++n;
@@ -1363,8 +1393,14 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     int p = gbase == 0 ? 0 : -64;
     for (;;) {
       if (p < 0) {
+        const uint32_t bits = speek(W, base + p);
+        const uint32_t la = luta[bits >> (32 - kL0)];
+        if ((la >> 10) == 2 && p + static_cast<int>(la & 31) < 0) {  // both start before the subsequence
+          p += static_cast<int>((la & 31) + ((la >> 5) & 31));
+          continue;
+        }
         uint32_t len = 0;
-        if (decode_one(lut, t, speek(W, base + p), &len) < 0) {
+        if (decode_one(lut, t, bits, &len) < 0) {
           p = 0;  // the early chain died: start at the subsequence itself
           continue;
         }
@@ -1383,8 +1419,19 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
         x0 = pk(0, 2, cnt);
         break;
       }
+      const uint32_t bits = speek(W, base + q);
+      const uint32_t la = luta[bits >> (32 - kL0)];
+      if ((la >> 10) == 2) {  // two codewords, the second starting inside the subsequence
+        const uint32_t l1 = la & 31, l12 = l1 + ((la >> 5) & 31);
+        if (q + l1 < kSubBits && gbase + q + l12 <= nbits) {
+          bm |= (1ull << q) | (1ull << (q + l1));
+          q += l12;
+          cnt += 2;
+          continue;
+        }
+      }
       uint32_t len = 0;
-      if (decode_one(lut, t, speek(W, base + q), &len) < 0) {
+      if (decode_one(lut, t, bits, &len) < 0) {
         x0 = pk(0, 1, cnt);
         break;
       }
@@ -1537,8 +1584,23 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     uint64_t gi = s_gc[g] + pk_cnt(q);  // index of this subsequence's first symbol
     uint32_t p = pk_off(q);
     while (p < kSubBits && gi < N && gbase + p < nbits) {
+      const uint32_t bits = speek(W, kHPre * 32 + i * kSubBits + p);
+      if (staged && gi + 1 < N) {
+        const uint32_t la = luta[bits >> (32 - kL0)];
+        if ((la >> 10) == 2) {
+          const uint32_t l1 = la & 31, l12 = l1 + ((la >> 5) & 31);
+          if (p + l1 < kSubBits && gbase + p + l12 <= nbits) {
+            const uint32_t w = bits >> (32 - kL0);
+            outs[gi - blk_base] = static_cast<uint16_t>(lut[w] >> 6);
+            outs[gi + 1 - blk_base] = static_cast<uint16_t>(lut[(w << l1) & ((1u << kL0) - 1)] >> 6);
+            p += l12;
+            gi += 2;
+            continue;
+          }
+        }
+      }
       uint32_t len = 0;
-      const int ent = decode_one(lut, t, speek(W, kHPre * 32 + i * kSubBits + p), &len);
+      const int ent = decode_one(lut, t, bits, &len);
       if (ent < 0 || gbase + p + len > nbits) break;
       if (staged) {
         outs[gi - blk_base] = static_cast<uint16_t>(ent);
