@@ -1249,7 +1249,6 @@ __device__ void vlz_roots(const DecArgs& a, uint32_t c, uint8_t* smem) {
 // Huffman blocks: 128 subsequences of 64 bits.
 // ===========================================================================
 constexpr uint32_t kHSub = 256;                        // subsequences per block (one per thread)
-constexpr uint32_t kHBits = kSubBits * kHSub;          // 8192 bits
 constexpr uint32_t kHPre = 2;                          // words staged before the block (warm-up)
 // smem: LUT | two-codeword LUT | staged words | per-subsequence chain summaries | group states, later the symbols (u16)
 __host__ __device__ constexpr uint32_t huff_smem(uint32_t hsub) {
