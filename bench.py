@@ -301,7 +301,7 @@ def run_single(args):
     # reads the decoded tensors back (D2H).  Three streams pipeline the steps
     # (H2D of step k+1 and D2H of step k-1 overlap step k's kernels), as an
     # exchange loop would; timed with events from the first copy to the last.
-    nslot = min(P, 3)
+    nslot = min(P, int(os.environ.get("EMBC_E2E_SLOTS", "3")))
     hx = [sets[k]["x"].cpu().pin_memory() for k in range(nslot)]  # slot j's input is set j's batch
     ys = [torch.empty((T, B, dim), dtype=torch.float32, device=dev) for _ in range(nslot)]
     hys = [torch.empty((T, B, dim), dtype=torch.float32).pin_memory() for _ in range(nslot)]
@@ -357,6 +357,31 @@ def run_single(args):
         e2e_step(k)
     torch.cuda.synchronize()
     e2e_steps = min(args.steps, 60)
+    if os.environ.get("EMBC_E2E_PROBE"):  # diagnostic: the pieces of the e2e pipeline alone
+        def probe(fn, n=e2e_steps):
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            for k in range(n):
+                fn(k)
+            a1.record()
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / n * 1e3
+        def h2d(k):
+            sets[k % nslot]["x"].copy_(hx[k % nslot], non_blocking=True)
+        def d2h(k):
+            hys[k % nslot].copy_(ys[k % nslot], non_blocking=True)
+        def both(k):
+            with torch.cuda.stream(s_h2d):
+                h2d(k)
+            with torch.cuda.stream(s_d2h):
+                d2h(k)
+            torch.cuda.current_stream().wait_stream(s_h2d)
+            torch.cuda.current_stream().wait_stream(s_d2h)
+        def comp(k):
+            slot_graphs[k % nslot].replay()
+        print("e2e probe us/step: h2d", round(probe(h2d), 1), "d2h", round(probe(d2h), 1),
+              "h2d||d2h", round(probe(both), 1), "graph", round(probe(comp), 1), file=sys.stderr)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s_h2d)
     th0 = time.perf_counter()

@@ -165,6 +165,27 @@ cudaError_t stage_commit(embc_ctx* ctx, int slot, cudaStream_t stream) {
   return cudaEventRecord(ctx->ring_evt[slot], stream);
 }
 
+cudaError_t stage_upload(embc_ctx* ctx, void* dst, const uint8_t* hs, size_t bytes, int slot, cudaStream_t stream) {
+  if (slot >= 0 || !ctx->darena || hs < ctx->arena || hs >= ctx->arena + ctx->arena_cap) {
+    cudaError_t e = cudaMemcpyAsync(dst, hs, bytes, cudaMemcpyHostToDevice, stream);
+    return e == cudaSuccess ? stage_commit(ctx, slot, stream) : e;
+  }
+  // capturing: the bytes go to the device mirror now, outside the graph (a
+  // relaxed-mode window for the synchronous side-stream copy); the graph
+  // copies device to device
+  uint8_t* dm = ctx->darena + (hs - ctx->arena);
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  cudaError_t e = cudaThreadExchangeStreamCaptureMode(&mode);
+  if (e != cudaSuccess) return e;
+  if (!ctx->side) e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dm, hs, bytes, cudaMemcpyHostToDevice, ctx->side);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->side);
+  cudaError_t e2 = cudaThreadExchangeStreamCaptureMode(&mode);
+  if (e != cudaSuccess) return e;
+  if (e2 != cudaSuccess) return e2;
+  return cudaMemcpyAsync(dst, dm, bytes, cudaMemcpyDeviceToDevice, stream);
+}
+
 static cudaEvent_t pool_event(embc_ctx* ctx) {
   if (!ctx->ev_pool.empty()) {
     cudaEvent_t e = ctx->ev_pool.back();
@@ -319,6 +340,8 @@ void embc_ctx_destroy(embc_ctx* ctx) {
     if (ctx->ring_evt[k]) cudaEventDestroy(ctx->ring_evt[k]);
   }
   if (ctx->arena) cudaFreeHost(ctx->arena);
+  if (ctx->darena) cudaFree(ctx->darena);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   for (auto& t : ctx->tev) {
     cudaEventDestroy(t.second.first);
     cudaEventDestroy(t.second.second);
@@ -452,11 +475,17 @@ embc_status embc_reserve_capture(embc_ctx* ctx, uint64_t bytes) {
   if (ctx->arena) {
     cudaDeviceSynchronize();
     cudaFreeHost(ctx->arena);
-    ctx->arena = nullptr;
+    cudaFree(ctx->darena);
+    ctx->arena = ctx->darena = nullptr;
     ctx->arena_cap = ctx->arena_used = 0;
   }
   cudaError_t e = cudaMallocHost(&ctx->arena, bytes);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "embc_reserve_capture");
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->darena, bytes);
+  if (e != cudaSuccess) {
+    if (ctx->arena) cudaFreeHost(ctx->arena);
+    ctx->arena = nullptr;
+    return cuda_fail(ctx, e, "embc_reserve_capture");
+  }
   ctx->arena_cap = bytes;
   return EMBC_OK;
 }

@@ -422,6 +422,9 @@ __device__ void huff_tables_small(const DChunk& C, DecState& S, const uint8_t* p
     }
   }
   __syncthreads();
+  DTS(8000 + c, 2);
+  DTS(8000 + c, 3);
+  DTS(8000 + c, 4);
   if (s_stop2) return;
   // left-aligned code starts ascending in canonical order -> prefix LUT
   for (uint32_t sl = threadIdx.x; sl < (1u << kL0); sl += blockDim.x) {
@@ -446,6 +449,8 @@ __device__ void huff_tables_small(const DChunk& C, DecState& S, const uint8_t* p
     if (!ent && f + 1 < static_cast<int>(nent) && (starts[f + 1] & 0xFFFFFFFFFFull) < Vend) ent = kLong;
     hv.lut[sl] = ent;
   }
+  DTS(8000 + c, 5);
+  DTS(8000 + c, 6);
   if (threadIdx.x == 0) {
     uint32_t max_len = 0;  // entries().back().length (huffman.hpp:257)
     for (uint32_t l = 1; l <= 32; ++l)
@@ -1298,6 +1303,28 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   uint32_t(*Gs)[33] = reinterpret_cast<uint32_t(*)[33]>(Ye + hsub);
   uint16_t* outs = reinterpret_cast<uint16_t*>(Ye + hsub);  // reuses Gs after phase B
   DROLE(blockIdx.x, 2);
+  // the bitstream is staged while the chunk CTA builds the tables: its place
+  // follows from the chunk's own bytes (header size, codebook entry count);
+  // the chunk CTA validates them and a disagreement restages below
+  const uint64_t bit0 = static_cast<uint64_t>(b) * hbits;
+  auto stage = [&](const uint8_t* bits, uint64_t nby) {
+    // W[kHPre + k] = word k of the block; the two words before hold the previous block's tail
+    if (b > 0) stage_bits(W, hwords, bits, nby, bit0 - 32 * kHPre);
+    else {
+      if (threadIdx.x < kHPre) W[threadIdx.x] = 0;
+      stage_bits(W + kHPre, hwords - kHPre, bits, nby, bit0);
+    }
+  };
+  const uint64_t poff = C.payload_only ? 0 : kHeader;
+  uint64_t boff = 0, nby = 0;
+  if (C.length >= poff + 12) {
+    const uint8_t* hp = C.in + poff + 8;
+    const uint32_t ne = (static_cast<uint32_t>(__ldg(hp)) << 24) | (static_cast<uint32_t>(__ldg(hp + 1)) << 16) |
+                        (static_cast<uint32_t>(__ldg(hp + 2)) << 8) | __ldg(hp + 3);
+    boff = 12 + 5ull * ne;
+    if (C.length - poff >= boff) nby = C.length - poff - boff;
+  }
+  stage(C.in + poff + boff, nby);
   if (threadIdx.x == 0) {  // the chunk CTA (an earlier ticket) publishes the tables
     uint32_t delay = 32;
     while (!*reinterpret_cast<volatile uint32_t*>(&a.ready[c])) {
@@ -1320,6 +1347,11 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   for (uint32_t i = threadIdx.x; i < sizeof(HTab) / 4; i += blockDim.x)
     reinterpret_cast<uint32_t*>(&t)[i] = __ldcg(reinterpret_cast<const unsigned int*>(hv.tab) + i);
   __syncthreads();
+  const uint64_t pay_off = __ldcg(reinterpret_cast<const unsigned long long*>(&S.pay_off));
+  if (pay_off != poff || t.bit_off != boff || t.nbits != 8 * nby) {  // uniform: shared / L2 values
+    stage(C.in + pay_off + t.bit_off, t.nbits / 8);
+    __syncthreads();
+  }
   // two codewords per lookup when both fit the kL0-bit window:
   // luta = len1 | len2 << 5 | n << 10  (n: 0 long code, 1 one codeword, 2 two, 3 invalid prefix)
   for (uint32_t w = threadIdx.x; w < (1u << kL0); w += blockDim.x) {
@@ -1340,14 +1372,6 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
       v = l1 | (l2 << 5) | (n << 10);
     }
     luta[w] = static_cast<uint16_t>(v);
-  }
-  const uint64_t bit0 = static_cast<uint64_t>(b) * hbits;
-  const uint8_t* bits = C.in + __ldcg(reinterpret_cast<const unsigned long long*>(&S.pay_off)) + t.bit_off;
-  // W[kHPre + k] = word k of the block; the two words before hold the previous block's tail
-  if (b > 0) stage_bits(W, hwords, bits, t.nbits / 8, bit0 - 32 * kHPre);
-  else {
-    if (threadIdx.x < kHPre) W[threadIdx.x] = 0;
-    stage_bits(W + kHPre, hwords - kHPre, bits, t.nbits / 8, bit0);
   }
   __syncthreads();
   DTS(blockIdx.x, 2);
@@ -1756,6 +1780,25 @@ __global__ void __launch_bounds__(kBlock) k_dec_fin(DecArgs a) {
       unsigned long long t0 = ~0ull;
       for (uint32_t k = 0; k < nb; ++k) t0 = min(t0, g_dts[k][1]);
       const char* names[4] = {"chunk", "vlzseg", "hufblk", "raw"};
+      {  // huffman table build phases (slots 8000 + chunk: 8 start, 2 keys, 3 sort, 4 codes, 5 lut, 6 dup sort)
+        unsigned long long n = 0, sm[6] = {0}, mx[6] = {0};
+        const int ord[6] = {8, 2, 3, 4, 5, 6};
+        for (uint32_t c = 0; c < a.nchunks && 8000 + c < 16384; ++c) {
+          if (!g_dts[8000 + c][8] || !g_dts[8000 + c][6]) continue;
+          ++n;
+          for (int q = 1; q < 6; ++q) {
+            const unsigned long long d = g_dts[8000 + c][ord[q]] - g_dts[8000 + c][ord[q - 1]];
+            sm[q] += d;
+            mx[q] = max(mx[q], d);
+          }
+          sm[0] += g_dts[8000 + c][8] - t0;
+          mx[0] = max(mx[0], g_dts[8000 + c][8] - t0);
+        }
+        if (n)
+          printf("D1 tables n %llu start %llu/%llu keys %llu/%llu sort %llu/%llu codes %llu/%llu lut %llu/%llu dup %llu/%llu\n", n,
+                 sm[0] / n, mx[0], sm[1] / n, mx[1], sm[2] / n, mx[2], sm[3] / n, mx[3], sm[4] / n, mx[4], sm[5] / n, mx[5]);
+        for (uint32_t c = 0; c < a.nchunks && 8000 + c < 16384; ++c) g_dts[8000 + c][8] = g_dts[8000 + c][6] = 0;
+      }
       for (uint32_t role = 0; role < 4; ++role) {
         unsigned long long n = 0, mn = ~0ull, mx = 0, sum[12] = {0}, mxs[12] = {0};
         for (uint32_t k = 0; k < nb; ++k) {
@@ -1913,8 +1956,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   std::memcpy(hs + o_hblk, hblk.data(), sizeof(uint32_t) * nhb);
   std::memcpy(hs + o_ct, ctiles.data(), sizeof(uint32_t) * ctiles.size());
   uint8_t* d = ctx->d_scratch;
-  ce = cudaMemcpyAsync(d, hs, host_bytes, cudaMemcpyHostToDevice, stream);
-  if (ce == cudaSuccess) ce = stage_commit(ctx, slot, stream);
+  ce = stage_upload(ctx, d, hs, host_bytes, slot, stream);
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "descriptor upload");
   DecArgs a{};
   a.ch = reinterpret_cast<const DChunk*>(d + o_ch);

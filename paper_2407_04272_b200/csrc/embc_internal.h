@@ -108,6 +108,11 @@ struct embc_ctx {
   int ring_next = 0;
   uint8_t* arena = nullptr;
   size_t arena_cap = 0, arena_used = 0;
+  // device mirror of the capture arena: a captured call's descriptors go up
+  // once at capture time, and the graph holds only a device-to-device copy
+  // (a small pinned host-to-device copy node costs ~9 us per replay)
+  uint8_t* darena = nullptr;
+  cudaStream_t side = nullptr;  // non-blocking stream for those capture-time uploads
   // per-kernel CUDA-event timing (embc_timing_*)
   bool timing = false;
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> tev;
@@ -126,6 +131,9 @@ cudaError_t ensure_scratch(embc_ctx* ctx, size_t bytes);
 // stage_commit after the cudaMemcpyAsync that reads it.
 cudaError_t stage_acquire(embc_ctx* ctx, size_t bytes, cudaStream_t stream, uint8_t** out, int* slot);
 cudaError_t stage_commit(embc_ctx* ctx, int slot, cudaStream_t stream);
+// Upload `bytes` staged at `hs` (from stage_acquire) to device `dst` on
+// `stream`, then commit the slot.
+cudaError_t stage_upload(embc_ctx* ctx, void* dst, const uint8_t* hs, size_t bytes, int slot, cudaStream_t stream);
 // Per-kernel timing hooks (no-ops unless embc_timing_enable(ctx, 1)).
 void tmark_begin(embc_ctx* ctx, const char* name, cudaStream_t stream);
 void tmark_end(embc_ctx* ctx, cudaStream_t stream);

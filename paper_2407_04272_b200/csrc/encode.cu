@@ -1348,7 +1348,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
   const uint64_t pay_end = start + hdr + book_bytes + (pre + my_bits + 7) / 8;  // end of this tile's bytes
   uint8_t* pay = a.out + start + hdr;
 #ifdef EMBC_DEBUG
-  if (threadIdx.x == 0 && atomicAdd(&g_dbg[2], 1ull) == a.ntiles - 1 && (g_dbg[2] = 0, a.ntiles > 1000) &&
+  if (threadIdx.x == 0 && atomicAdd(&g_dbg[2], 1ull) == a.ntiles - 1 && (g_dbg[2] = 0, a.ntiles > 100) &&
       atomicAdd(&g_dbg[3], 1ull) % 8 == 7) {
     unsigned long long t0 = ~0ull, mxe = 0, sl = 0, ml = 0, sb = 0, mb = 0, nb = 0;
     for (uint32_t t = 0; t < a.ntiles; ++t) t0 = min(t0, g_ts1[t][0]);
@@ -1754,8 +1754,7 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   uint32_t flags0[8] = {host_abort ? JF_ABORT : 0u, 0, 0, 0, 0, 0, 0, 0};
   std::memcpy(hs + o_flags, flags0, sizeof(flags0));
   uint8_t* d = ctx->d_scratch;
-  ce = cudaMemcpyAsync(d, hs, host_bytes, cudaMemcpyHostToDevice, stream);
-  if (ce == cudaSuccess) ce = stage_commit(ctx, slot, stream);
+  ce = stage_upload(ctx, d, hs, host_bytes, slot, stream);
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "descriptor upload");
 
   StatsArgs sa{};
@@ -1829,7 +1828,8 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   // small calls: one fused pass (sizes, decoupled look-back, bytes) -- the
   // look-back is cheap when every tile is resident at once; large calls: sizes
   // + layout, then bytes, with no waiting at all
-  if (!d_stats && ntiles <= 1024) {
+  static const uint32_t fused_max = getenv("EMBC_FUSED_MAX") ? atoi(getenv("EMBC_FUSED_MAX")) : 1024;
+  if (!d_stats && ntiles <= fused_max) {
     ea.phase = 2;
     EMBC_TIMED(ctx, "k_emit", stream, k_emit<2><<<ntiles, kBlock, emit_smem, stream>>>(ea));
   } else {
