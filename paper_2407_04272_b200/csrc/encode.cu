@@ -32,13 +32,74 @@ namespace embc_dev {
 
 #ifdef EMBC_DEBUG
 __device__ unsigned long long g_dbg[8];
-__device__ unsigned long long g_ts[16384][6];
+__device__ unsigned long long g_ts[16384][10];
+__device__ uint32_t g_tc[16384];  // codec of the tile
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 #define TS(k) do { if (threadIdx.x == 0 && tid < 16384) g_ts[tid][k] = gtime(); } while (0)
+// E2 (fused phase) timeline: every CTA stamps its exit; the last one prints
+// per-phase means / maxima (0 start, 1 codes, 2 sizes, 3 look-back, 4 staged, 5 exit)
+struct EmitEnd {
+  uint32_t tid, n;
+  __device__ ~EmitEnd() {
+    if (threadIdx.x != 0 || tid >= 16384 || n == 0xFFFFFFFFu) return;
+    g_ts[tid][5] = gtime();
+    __threadfence();
+    if (atomicAdd(&g_dbg[4], 1ull) != n - 1) return;
+    g_dbg[4] = 0;
+    if (n < 100 || (atomicAdd(&g_dbg[5], 1ull) % 8) != 7) return;
+    unsigned long long t0 = ~0ull, t1 = 0, sm[6] = {0}, mx[6] = {0};
+    for (uint32_t t = 0; t < n && t < 16384; ++t) {
+      t0 = min(t0, g_ts[t][0]);
+      t1 = max(t1, g_ts[t][5]);
+    }
+    for (uint32_t t = 0; t < n && t < 16384; ++t) {
+      unsigned long long prev = g_ts[t][0];
+      sm[0] += prev - t0;
+      mx[0] = max(mx[0], prev - t0);
+      for (int k = 1; k < 6; ++k) {
+        if (g_ts[t][k] < prev) continue;
+        const unsigned long long d = g_ts[t][k] - prev;
+        sm[k] += d;
+        mx[k] = max(mx[k], d);
+        prev = g_ts[t][k];
+      }
+    }
+    for (uint32_t cd = 0; cd < 3; ++cd) {  // codes + sizes by codec
+      unsigned long long c1 = 0, m1 = 0, c2 = 0, m2 = 0, nn = 0;
+      for (uint32_t t = 0; t < n && t < 16384; ++t) {
+        if (g_tc[t] != cd || g_ts[t][2] < g_ts[t][1] || g_ts[t][1] < g_ts[t][0]) continue;
+        ++nn;
+        c1 += g_ts[t][1] - g_ts[t][0];
+        m1 = max(m1, g_ts[t][1] - g_ts[t][0]);
+        c2 += g_ts[t][2] - g_ts[t][1];
+        m2 = max(m2, g_ts[t][2] - g_ts[t][1]);
+      }
+      if (nn) printf("  codec %u: %llu tiles codes %llu/%llu sizes %llu/%llu\n", cd, nn, c1 / nn, m1, c2 / nn, m2);
+      if (cd == 1 && nn) {
+        unsigned long long a6 = 0, a7 = 0, a8 = 0, m6 = 0, m7 = 0, m8 = 0, rr = 0, mr = 0;
+        for (uint32_t t = 0; t < n && t < 16384; ++t) {
+          if (g_tc[t] != 1 || !g_ts[t][6] || !g_ts[t][8]) continue;
+          a6 += g_ts[t][6] - g_ts[t][1]; m6 = max(m6, g_ts[t][6] - g_ts[t][1]);
+          a7 += g_ts[t][7] - g_ts[t][6]; m7 = max(m7, g_ts[t][7] - g_ts[t][6]);
+          a8 += g_ts[t][8] - g_ts[t][7]; m8 = max(m8, g_ts[t][8] - g_ts[t][7]);
+          rr += g_ts[t][9]; mr = max(mr, g_ts[t][9]);
+          g_ts[t][6] = g_ts[t][8] = 0;
+        }
+        printf("  vlz sizes: stage %llu/%llu search %llu/%llu verify %llu/%llu rounds %llu/%llu\n", a6 / nn, m6, a7 / nn,
+               m7, a8 / nn, m8, rr / nn, mr);
+      }
+    }
+    printf("k_emit: %u tiles span %llu ns; start %llu/%llu codes %llu/%llu sizes %llu/%llu lookback %llu/%llu bytes %llu/%llu exit %llu/%llu\n",
+           n, t1 - t0, sm[0] / n, mx[0], sm[1] / n, mx[1], sm[2] / n, mx[2], sm[3] / n, mx[3], sm[4] / n, mx[4],
+           sm[5] / n, mx[5]);
+    for (uint32_t t = 0; t < n && t < 16384; ++t)
+      for (int k = 0; k < 10; ++k) g_ts[t][k] = 0;
+  }
+};
 __device__ unsigned long long g_ts1[16384][12];
 #define TS1(k) do { if (threadIdx.x == 0 && blockIdx.x < 16384) g_ts1[blockIdx.x][k] = gtime(); } while (0)
 #else
@@ -62,7 +123,7 @@ __host__ __device__ constexpr uint32_t emit_codes_bytes(uint32_t vals, uint32_t 
 __host__ __device__ constexpr uint32_t emit_stage_bytes(uint32_t vals, uint32_t rows, bool vlz = true) {
   return ((vlz ? rows + 5 * vals : 4 * vals) + 128 + 15) & ~15u;
 }
-constexpr uint32_t kAuxBytes = kHashStage * 4 + kMaxTileRows * 20;  // hashes | dec, lits, cand, plist, miss
+constexpr uint32_t kAuxBytes = kHashStage * 4 + kMaxTileRows * 20 + 8 * kLutStage;  // LUT / hash stage | per-row arrays
 constexpr uint32_t kEmitSmemMax = emit_codes_bytes(kMaxRowVals, kMaxTileRows) +
                                   emit_stage_bytes(kMaxRowVals, kMaxTileRows) + kAuxBytes;
 // E1: codes staged for the generic (scalar) path + histogram window; the
@@ -70,14 +131,16 @@ constexpr uint32_t kEmitSmemMax = emit_codes_bytes(kMaxRowVals, kMaxTileRows) +
 __host__ __device__ constexpr uint32_t stats_codes_bytes(uint32_t vals, uint32_t rows) {
   return (vals + rows) * 4 > 16384 ? ((vals + rows) * 4 + 15) & ~15u : 16384u;
 }
-constexpr uint32_t kStatsSmemMax = stats_codes_bytes(kMaxRowVals, kMaxTileRows) + kWin * 4;
+constexpr uint32_t kStatsVlzAux = 4 * kHashStage + 16 * kMaxTileRows + 4 * 2048 + 2 * kHashStage;
+constexpr uint32_t kStatsSmemMax =
+    stats_codes_bytes(kMaxRowVals, kMaxTileRows) + (kWin * 4 > kStatsVlzAux ? kWin * 4 : kStatsVlzAux);
 
 // look-back status words: flag in bits 63:62, value in 61:0
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 constexpr uint32_t kJobStride = 16;  // job status words one 128-B line apart (polled by many CTAs)
 
 // call-level flags (device): [0] abort bits, [1] E2 tile ticket, [2..3] wide-pool cursor (u64)
-enum : uint32_t { CF_ABORT = 0, CF_TICKET = 1, CF_WIDE = 2 };
+enum : uint32_t { CF_ABORT = 0, CF_TICKET = 1, CF_WIDE = 2, CF_TICKET_S = 4 };
 
 // ---------------------------------------------------------------------------
 // element access (int32 code sources for the codec-stage entry points)
@@ -486,6 +549,213 @@ __device__ void build_book(const DJob& J, JobState* Sp, const BookArgs& a, uint8
 // ---------------------------------------------------------------------------
 // E1: quantize + per-tile statistics (+ codebook tail)
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// vlz matching of one tile (vlz.hpp:86-103): for every row the nearest
+// earlier row inside the window with identical codes.  Candidates come from
+// the row hashes nearest first and are verified exactly for all rows of the
+// tile at once (CodeRowEq, vlz.hpp:75-79); a hash collision resumes the search
+// past the disproved candidate.  `codes` holds the tile's codes (row r at
+// r * stride); the window's hashes are read through L2 (other CTAs of the
+// launch wrote them).  Writes row_dec; returns the tile's token bytes and
+// counts reference rows in *nref.
+// ---------------------------------------------------------------------------
+struct VlzSmem {
+  uint32_t* sh;       // staged window hashes (hash_cap)
+  uint32_t* dec;      // per row: match offset (0 = literal)
+  uint32_t* cand;     // per row: candidate offset under test
+  uint32_t* plist;    // rows with a pending candidate
+  uint32_t* miss;     // candidate disproved
+  uint32_t* bhead;    // bucket chains over the staged hashes
+  uint32_t chain_bytes;
+  uint32_t hash_cap;
+};
+
+__device__ uint64_t vlz_match_tile(const DJob& J, const DTile& T, const int32_t* codes, uint32_t stride,
+                                   const uint64_t* __restrict__ ri, uint32_t* __restrict__ row_dec, const VlzSmem& m,
+                                   uint32_t* s_tmp32, unsigned long long* s_tmp64, uint64_t* nref_out) {
+  const uint32_t dim = J.dim;
+  const uint32_t W = J.window;
+  const uint32_t lo = T.row0 > W ? T.row0 - W : 0;
+  const uint32_t nh = T.row0 + T.rows - lo;
+  const bool staged = nh <= m.hash_cap;
+  uint32_t* sh = m.sh;
+  uint32_t* dec = m.dec;
+  uint32_t* cand = m.cand;
+  uint32_t* plist = m.plist;
+  uint32_t* miss = m.miss;
+  if (staged)
+    for (uint32_t k = threadIdx.x; k < nh; k += kBlock) sh[k] = static_cast<uint32_t>(__ldcg(ri + lo + k));
+  // bucket chains (u16 links into sh): a row scans its 16 nearest offsets,
+  // then walks its bucket for the nearest farther candidate
+  uint32_t nbk = 0;
+  if (staged && nh < 65535 && m.chain_bytes > 2 * nh + 4 * 256) {
+    nbk = 4096;
+    while (4 * nbk + 2 * nh > m.chain_bytes) nbk >>= 1;
+    if (nbk < nh / 2) nbk = 0;
+  }
+  uint32_t* bhead = m.bhead;
+  uint16_t* bnext = reinterpret_cast<uint16_t*>(bhead + nbk);
+  const uint32_t bsh = 32 - (31 - __clz(nbk | 1));
+  for (uint32_t k = threadIdx.x; k < nbk; k += kBlock) bhead[k] = 0xFFFFu;
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < (nbk ? nh : 0); k += kBlock)
+    bnext[k] = static_cast<uint16_t>(atomicExch(&bhead[(sh[k] * 0x9E3779B1u) >> bsh], k));
+  __syncthreads();
+  // nearest earlier row with an equal hash at offset >= k0, or 0
+  auto search = [&](uint32_t r, uint32_t k0) -> uint32_t {
+    const uint32_t i = T.row0 + r;
+    const uint32_t kmax = min(W, i);
+    if (!staged) {
+      const uint32_t h = static_cast<uint32_t>(__ldcg(ri + i));
+      for (uint32_t k = k0; k <= kmax; ++k)
+        if (static_cast<uint32_t>(__ldcg(ri + i - k)) == h) return k;
+      return 0;
+    }
+    const uint32_t h = sh[i - lo];
+    const uint32_t knear = nbk ? min(kmax, k0 + 15) : kmax;
+    uint32_t k = k0;
+    for (; k + 3 <= knear; k += 4) {
+      const uint32_t j = i - k - lo;
+      const uint32_t h0 = sh[j], h1 = sh[j - 1], h2 = sh[j - 2], h3 = sh[j - 3];
+      if (h0 == h) return k;
+      if (h1 == h) return k + 1;
+      if (h2 == h) return k + 2;
+      if (h3 == h) return k + 3;
+    }
+    for (; k <= knear; ++k)
+      if (sh[i - k - lo] == h) return k;
+    if (knear >= kmax) return 0;
+    // farther: the largest staged index e with i - kmax <= lo + e <= i - knear - 1
+    const uint32_t ehi = i - knear - 1 - lo, elo = i - kmax - lo;
+    uint32_t best = 0xFFFFFFFFu;
+    for (uint32_t e = bhead[(h * 0x9E3779B1u) >> bsh]; e != 0xFFFFu; e = bnext[e])
+      if (e <= ehi && e >= elo && sh[e] == h && (best == 0xFFFFFFFFu || e > best)) best = e;
+    return best == 0xFFFFFFFFu ? 0 : i - lo - best;
+  };
+  for (uint32_t r = threadIdx.x; r < T.rows; r += kBlock) {
+    cand[r] = search(r, 1);
+    dec[r] = 0;
+  }
+  __syncthreads();
+  const bool vq = (dim & 3) == 0 && stride == dim && (reinterpret_cast<uintptr_t>(J.src) & 15) == 0;
+  for (;;) {
+    uint32_t np = 0;  // compact the rows with a candidate under test
+    for (uint32_t r0 = 0; r0 < T.rows; r0 += kBlock) {
+      const uint32_t r = r0 + threadIdx.x;
+      const bool p = r < T.rows && cand[r] != 0;
+      uint32_t tot;
+      const uint32_t at = block_excl_scan<uint32_t>(p, s_tmp32, &tot);
+      if (p) {
+        plist[np + at] = r;
+        miss[np + at] = 0;
+      }
+      np += tot;
+    }
+    if (np == 0) break;
+    __syncthreads();
+    const uint32_t work = vq ? np * (dim >> 2) : np * dim;
+    if (vq) {  // four codes per work item: 16-B smem / global loads
+      const uint32_t qpr = dim >> 2;
+      for (uint32_t e0w = 0; e0w < work; e0w += 2 * kBlock) {
+        int4 cj[2], ci[2];
+        uint32_t pp[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t e = e0w + u * kBlock + threadIdx.x;
+          pp[u] = 0xFFFFFFFFu;
+          if (e < work) {
+            const uint32_t pi = e / qpr;
+            const uint32_t qc = e - pi * qpr;
+            const uint32_t r = plist[pi];
+            const uint32_t i = T.row0 + r, j = i - cand[r];
+            pp[u] = pi;
+            ci[u] = reinterpret_cast<const int4*>(codes + r * dim)[qc];
+            if (j >= T.row0) {
+              cj[u] = reinterpret_cast<const int4*>(codes + (j - T.row0) * dim)[qc];
+            } else {
+              const uint4 g = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(J.src) +
+                                                                   static_cast<uint64_t>(j) * dim) + qc);
+              cj[u] = make_int4(static_cast<int32_t>(g.x), static_cast<int32_t>(g.y), static_cast<int32_t>(g.z),
+                                static_cast<int32_t>(g.w));
+              if (J.src_kind == EMBC_SRC_F32) pp[u] |= 0x80000000u;  // needs quantizing
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (pp[u] == 0xFFFFFFFFu) continue;
+          int4 c = cj[u];
+          if (pp[u] & 0x80000000u) {
+            uint32_t rr = 0;
+            c.x = quantize_f32(__int_as_float(c.x), J.qp, &rr);
+            c.y = quantize_f32(__int_as_float(c.y), J.qp, &rr);
+            c.z = quantize_f32(__int_as_float(c.z), J.qp, &rr);
+            c.w = quantize_f32(__int_as_float(c.w), J.qp, &rr);
+          }
+          if (c.x != ci[u].x || c.y != ci[u].y || c.z != ci[u].z || c.w != ci[u].w) miss[pp[u] & 0x7FFFFFFFu] = 1;
+        }
+      }
+    } else {
+      for (uint32_t e0w = 0; e0w < work; e0w += 4 * kBlock) {
+        int32_t cj[4], ci[4];
+        uint32_t pp[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // all loads first: four rows' elements in flight
+          const uint32_t e = e0w + u * kBlock + threadIdx.x;
+          pp[u] = 0xFFFFFFFFu;
+          if (e < work) {
+            const uint32_t pi = fdiv(e, J.fd);
+            const uint32_t col = e - pi * dim;
+            const uint32_t r = plist[pi];
+            const uint32_t i = T.row0 + r, j = i - cand[r];
+            pp[u] = pi;
+            ci[u] = codes[r * stride + col];
+            if (j >= T.row0) {
+              cj[u] = codes[(j - T.row0) * stride + col];
+            } else if (J.src_kind == EMBC_SRC_F32) {
+              cj[u] = __float_as_int(__ldg(static_cast<const float*>(J.src) + static_cast<uint64_t>(j) * dim + col));
+              pp[u] |= 0x80000000u;  // needs quantizing
+            } else {
+              cj[u] = __ldg(static_cast<const int32_t*>(J.src) + static_cast<uint64_t>(j) * dim + col);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (pp[u] == 0xFFFFFFFFu) continue;
+          int32_t c = cj[u];
+          if (pp[u] & 0x80000000u) {
+            uint32_t rr = 0;
+            c = quantize_f32(__int_as_float(c), J.qp, &rr);
+          }
+          if (c != ci[u]) miss[pp[u] & 0x7FFFFFFFu] = 1;
+        }
+      }
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < np; q += kBlock) {
+      const uint32_t r = plist[q];
+      if (!miss[q]) {
+        dec[r] = cand[r];
+        cand[r] = 0;
+      } else {  // hash collision: keep looking further back
+        cand[r] = search(r, cand[r] + 1);
+      }
+    }
+    __syncthreads();
+  }
+  unsigned long long local = 0, nref = 0;
+  for (uint32_t r = threadIdx.x; r < T.rows; r += kBlock) {
+    const uint32_t found = dec[r];
+    local += found ? 1u + varint_len(found) : static_cast<uint32_t>(__ldcg(ri + T.row0 + r) >> 32);
+    nref += found != 0;
+    row_dec[T.row0 + r] = found;
+  }
+  const unsigned long long both = block_sum<unsigned long long>(local | (nref << 40), s_tmp64);
+  *nref_out = both >> 40;
+  return both & ((1ull << 40) - 1);
+}
+
 struct StatsArgs {
   const DJob* jobs;
   const DTile* tiles;
@@ -495,15 +765,22 @@ struct StatsArgs {
   unsigned long long* job_status;
   uint32_t* edge_slot;
   BookArgs book;
-  uint32_t hist_off;  // dynamic smem offset of the histogram window
+  uint32_t hist_off;  // dynamic smem offset of the histogram window / vlz matching scratch
+  // vlz matching (vlz.hpp:86-103) runs in E1: a tile publishes its row hashes,
+  // waits for the tiles its window reaches into, then matches its rows
+  uint32_t* row_dec;                  // per row: match offset (0 = literal)
+  uint32_t* hready;                   // per tile: row hashes published (zeroed by the upload)
+  unsigned long long* d_stats;        // match_stats: (literal rows, reference rows)
+  uint32_t hash_cap, rows_cap, chain_bytes;
+  uint32_t match;                     // match here (fused E2 / match_stats); else E2's sizes pass does
 };
 
 // E1's vector loop, one instantiation per codec (no codec branches inside):
 // 128-bit loads, 4 quads in flight per thread; a vlz row is qpr consecutive lanes.
 template <int CODEC>
 __device__ __forceinline__ void stats_vec(const DJob& J, uint64_t e0, uint32_t ne, uint32_t qpr, uint64_t gbase,
-                                          uint64_t* __restrict__ row_info, uint32_t* shist, unsigned long long& lerr,
-                                          int& lmin, int& lmax, bool& lwide) {
+                                          uint64_t* __restrict__ row_info, uint32_t* shist, int32_t* codes,
+                                          unsigned long long& lerr, int& lmin, int& lmax, bool& lwide) {
   constexpr bool vlz = CODEC == EMBC_CODEC_VLZ, huf = CODEC == EMBC_CODEC_HUFFMAN;
   const uint32_t nq = ne >> 2;
   const QParams qp = J.qp;
@@ -566,6 +843,7 @@ __device__ __forceinline__ void stats_vec(const DJob& J, uint64_t e0, uint32_t n
           lit += __shfl_xor_sync(0xffffffffu, lit, o);
         }
         if (ok && (q & (qpr - 1)) == 0) row_info[gbase + q / qpr] = (static_cast<uint64_t>(1 + lit) << 32) | h;
+        if (ok) reinterpret_cast<int4*>(codes)[q] = make_int4(c[0], c[1], c[2], c[3]);  // row-major, for matching
       }
     }
   }
@@ -575,7 +853,11 @@ __global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ unsigned long long s_err;
   __shared__ int s_min, s_max, s_last;
-  const uint32_t tid = blockIdx.x;
+  __shared__ uint32_t s_tk;
+  // tiles in ticket order: a vlz tile only ever waits on earlier tickets
+  if (threadIdx.x == 0) s_tk = atomicAdd(&a.book.flags[CF_TICKET_S], 1u);
+  __syncthreads();
+  const uint32_t tid = s_tk;
   TS1(0);
   const DTile T = a.tiles[tid];
   const DJob& J = a.jobs[T.job];
@@ -611,9 +893,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
                    (!vlz || (qpr <= 32 && (qpr & (qpr - 1)) == 0));
   const uint64_t gbase = J.row_base + T.row0;
   if (vec) {
-    if (vlz) stats_vec<EMBC_CODEC_VLZ>(J, e0, ne, qpr, gbase, a.row_info, shist, lerr, lmin, lmax, lwide);
-    else if (huf) stats_vec<EMBC_CODEC_HUFFMAN>(J, e0, ne, qpr, gbase, a.row_info, shist, lerr, lmin, lmax, lwide);
-    else stats_vec<EMBC_CODEC_RAW>(J, e0, ne, qpr, gbase, a.row_info, shist, lerr, lmin, lmax, lwide);
+    int32_t* codes = reinterpret_cast<int32_t*>(smem);
+    if (vlz) stats_vec<EMBC_CODEC_VLZ>(J, e0, ne, qpr, gbase, a.row_info, shist, codes, lerr, lmin, lmax, lwide);
+    else if (huf) stats_vec<EMBC_CODEC_HUFFMAN>(J, e0, ne, qpr, gbase, a.row_info, shist, codes, lerr, lmin, lmax, lwide);
+    else stats_vec<EMBC_CODEC_RAW>(J, e0, ne, qpr, gbase, a.row_info, shist, codes, lerr, lmin, lmax, lwide);
   } else {
     // generic path: element loop, vlz codes staged at r * (dim|1) + col
     int32_t* codes = reinterpret_cast<int32_t*>(smem);
@@ -696,6 +979,44 @@ __global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
     }
   }
   TS1(2);
+  if (vlz && a.match) {
+    // publish this tile's row hashes, wait for the tiles the window reaches
+    // into (earlier tickets of the same job), then match
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t*>(&a.hready[tid]) = 1;
+    if (!J.window_ok || T.rows == 0) return;
+    const uint32_t lo = T.row0 > J.window ? T.row0 - J.window : 0;
+    for (uint32_t t = J.tile0 + lo / J.tile_rows + threadIdx.x; t < tid; t += blockDim.x) {
+      uint32_t delay = 32;
+      while (!*reinterpret_cast<volatile uint32_t*>(&a.hready[t])) {
+        __nanosleep(delay);
+        delay = min(delay * 2, 256u);
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ uint32_t s_tmp32[33];
+    __shared__ unsigned long long s_tmp64[33];
+    uint32_t* aux = reinterpret_cast<uint32_t*>(smem + a.hist_off);
+    VlzSmem m;
+    m.sh = aux;
+    m.dec = aux + a.hash_cap;
+    m.cand = m.dec + a.rows_cap;
+    m.plist = m.cand + a.rows_cap;
+    m.miss = m.plist + a.rows_cap;
+    m.bhead = m.miss + a.rows_cap;
+    m.chain_bytes = a.chain_bytes;
+    m.hash_cap = a.hash_cap;
+    uint64_t nref = 0;
+    vlz_match_tile(J, T, reinterpret_cast<const int32_t*>(smem), vec ? dim : (dim | 1u), a.row_info + J.row_base,
+                   a.row_dec + J.row_base, m, s_tmp32, s_tmp64, &nref);
+    if (a.d_stats && threadIdx.x == 0) {  // match_stats (vlz.hpp:162-168)
+      atomicAdd(&a.d_stats[0], static_cast<unsigned long long>(T.rows) - nref);
+      atomicAdd(&a.d_stats[1], static_cast<unsigned long long>(nref));
+    }
+    return;
+  }
   if (!huf) return;
   // the job's last tile to finish builds the codebook
   __threadfence();
@@ -986,6 +1307,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
   __syncthreads();
   const uint32_t tid = s_t;
   TS(0);
+#ifdef EMBC_DEBUG
+  EmitEnd dbg_end{tid, PHASE == 2 ? a.ntiles : 0xFFFFFFFFu};
+#endif
   if (*reinterpret_cast<volatile uint32_t*>(&a.flags[CF_ABORT]) & JF_ABORT) {
     if (tid == 0 && PHASE != 1 && !a.d_stats) fold_failure(a);
     return;
@@ -1004,13 +1328,15 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
   uint8_t* aux = smem + a.aux_off;
   const uint32_t codec = J.codec;
   const uint32_t stride = codec == EMBC_CODEC_VLZ ? dim : 0;  // vlz rows unpadded: warps read rows along lanes
+#ifdef EMBC_DEBUG
+  if (threadIdx.x == 0 && tid < 16384) g_tc[tid] = codec;
+#endif
 
   uint32_t* dec = reinterpret_cast<uint32_t*>(aux + a.hash_cap * 4);  // vlz: match offset per row
   uint32_t* lits = dec + a.rows_cap;                                   // vlz: token bytes per row
-  uint32_t* cand = lits + a.rows_cap;                                  // vlz: candidate offset under test
-  uint32_t* plist = cand + a.rows_cap;                                 // vlz: rows with a pending candidate
-  uint32_t* miss = plist + a.rows_cap;                                 // vlz: candidate disproved
-  const bool vlz_lit_only = phase == 1 && codec == EMBC_CODEC_VLZ;     // phase 1 needs literal rows only
+  // vlz rows are matched in E1 (fused calls) or in phase 0: the byte passes
+  // need the literal rows only
+  const bool vlz_lit_only = codec == EMBC_CODEC_VLZ && phase != 0;
   if (vlz_lit_only) {
     const uint64_t* ri = a.row_info + J.row_base + T.row0;
     for (uint32_t r = threadIdx.x; r < T.rows; r += kBlock) {
@@ -1085,186 +1411,26 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
   uint64_t* sl = reinterpret_cast<uint64_t*>(aux);
   const int32_t cmin = S.cmin;
   const uint32_t span = codec == EMBC_CODEC_HUFFMAN ? static_cast<uint32_t>(S.cmax - cmin + 1) : 0;
-  const bool lut_staged = span <= kLutStage && 8 * span <= a.hash_cap * 4 + a.rows_cap * 20;
+  const bool lut_staged = span <= kLutStage && 8 * span <= a.hash_cap * 4 + a.rows_cap * 8;
   if (codec == EMBC_CODEC_RAW) {
     my_bits = 32ull * ne;
-  } else if (codec == EMBC_CODEC_VLZ && phase == 1) {
+  } else if (codec == EMBC_CODEC_VLZ && phase != 0) {  // matched before
     uint64_t local = 0;
     for (uint32_t r = threadIdx.x; r < T.rows; r += kBlock) local += lits[r];
     my_bits = 8ull * block_sum<unsigned long long>(local, s_tmp64);
-  } else if (codec == EMBC_CODEC_VLZ) {
-    const uint32_t W = J.window;
-    const uint32_t lo = T.row0 > W ? T.row0 - W : 0;
-    const uint32_t nh = T.row0 + T.rows - lo;
-    const bool staged = nh <= a.hash_cap;
-    uint32_t* sh = reinterpret_cast<uint32_t*>(aux);
-    const uint64_t* ri = a.row_info + J.row_base;
-    if (staged)
-      for (uint32_t k = threadIdx.x; k < nh; k += kBlock) sh[k] = static_cast<uint32_t>(__ldg(ri + lo + k));
-    __syncthreads();
-    // nearest earlier row with an equal hash at offset >= k0, or 0
-    auto search = [&](uint32_t r, uint32_t k0) -> uint32_t {
-      const uint32_t i = T.row0 + r;
-      const uint32_t h = staged ? sh[i - lo] : static_cast<uint32_t>(__ldg(ri + i));
-      const uint32_t kmax = min(W, i);
-      uint32_t k = k0;
-      for (; k + 3 <= kmax; k += 4) {
-        const uint32_t j = i - k;
-        uint32_t h0, h1, h2, h3;
-        if (staged) {
-          h0 = sh[j - lo];
-          h1 = sh[j - 1 - lo];
-          h2 = sh[j - 2 - lo];
-          h3 = sh[j - 3 - lo];
-        } else {
-          h0 = static_cast<uint32_t>(__ldg(ri + j));
-          h1 = static_cast<uint32_t>(__ldg(ri + j - 1));
-          h2 = static_cast<uint32_t>(__ldg(ri + j - 2));
-          h3 = static_cast<uint32_t>(__ldg(ri + j - 3));
-        }
-        if (h0 == h) return k;
-        if (h1 == h) return k + 1;
-        if (h2 == h) return k + 2;
-        if (h3 == h) return k + 3;
-      }
-      for (; k <= kmax; ++k) {
-        const uint32_t j = i - k;
-        if ((staged ? sh[j - lo] : static_cast<uint32_t>(__ldg(ri + j))) == h) return k;
-      }
-      return 0;
-    };
-    // nearest identical row (vlz.hpp:86-103): hash candidates, nearest first,
-    // verified exactly for all rows of the tile at once (CodeRowEq, vlz.hpp:75-79)
-    for (uint32_t r = threadIdx.x; r < T.rows; r += kBlock) {
-      cand[r] = search(r, 1);
-      dec[r] = 0;
-    }
-    __syncthreads();
-    for (;;) {
-      uint32_t np = 0;  // compact the rows with a candidate under test
-      for (uint32_t r0 = 0; r0 < T.rows; r0 += kBlock) {
-        const uint32_t r = r0 + threadIdx.x;
-        const bool p = r < T.rows && cand[r] != 0;
-        uint32_t tot;
-        const uint32_t at = block_excl_scan<uint32_t>(p, s_tmp32, &tot);
-        if (p) {
-          plist[np + at] = r;
-          miss[np + at] = 0;
-        }
-        np += tot;
-      }
-      if (np == 0) break;
-      __syncthreads();
-      const bool vq = (dim & 3) == 0 && (reinterpret_cast<uintptr_t>(J.src) & 15) == 0;
-      const uint32_t work = vq ? np * (dim >> 2) : np * dim;
-      if (vq) {  // four codes per work item: 16-B smem / global loads
-        const uint32_t qpr = dim >> 2;
-        for (uint32_t e0w = 0; e0w < work; e0w += 2 * kBlock) {
-          int4 cj[2], ci[2];
-          uint32_t pp[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const uint32_t e = e0w + u * kBlock + threadIdx.x;
-            pp[u] = 0xFFFFFFFFu;
-            if (e < work) {
-              const uint32_t pi = e / qpr;
-              const uint32_t qc = e - pi * qpr;
-              const uint32_t r = plist[pi];
-              const uint32_t i = T.row0 + r, j = i - cand[r];
-              pp[u] = pi;
-              ci[u] = reinterpret_cast<const int4*>(codes + r * dim)[qc];
-              if (j >= T.row0) {
-                cj[u] = reinterpret_cast<const int4*>(codes + (j - T.row0) * dim)[qc];
-              } else {
-                const uint4 g = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(J.src) +
-                                                                     static_cast<uint64_t>(j) * dim) + qc);
-                cj[u] = make_int4(static_cast<int32_t>(g.x), static_cast<int32_t>(g.y), static_cast<int32_t>(g.z),
-                                  static_cast<int32_t>(g.w));
-                if (J.src_kind == EMBC_SRC_F32) pp[u] |= 0x80000000u;  // needs quantizing
-              }
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (pp[u] == 0xFFFFFFFFu) continue;
-            int4 c = cj[u];
-            if (pp[u] & 0x80000000u) {
-              uint32_t rr = 0;
-              c.x = quantize_f32(__int_as_float(c.x), J.qp, &rr);
-              c.y = quantize_f32(__int_as_float(c.y), J.qp, &rr);
-              c.z = quantize_f32(__int_as_float(c.z), J.qp, &rr);
-              c.w = quantize_f32(__int_as_float(c.w), J.qp, &rr);
-            }
-            if (c.x != ci[u].x || c.y != ci[u].y || c.z != ci[u].z || c.w != ci[u].w)
-              miss[pp[u] & 0x7FFFFFFFu] = 1;
-          }
-        }
-      } else
-      for (uint32_t e0w = 0; e0w < work; e0w += 4 * kBlock) {
-        int32_t cj[4], ci[4];
-        uint32_t pp[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {  // all loads first: four rows' elements in flight
-          const uint32_t e = e0w + u * kBlock + threadIdx.x;
-          pp[u] = 0xFFFFFFFFu;
-          if (e < work) {
-            const uint32_t pi = fdiv(e, J.fd);
-            const uint32_t col = e - pi * dim;
-            const uint32_t r = plist[pi];
-            const uint32_t i = T.row0 + r, j = i - cand[r];
-            pp[u] = pi;
-            ci[u] = codes[r * stride + col];
-            if (j >= T.row0) {
-              cj[u] = codes[(j - T.row0) * stride + col];
-            } else if (J.src_kind == EMBC_SRC_F32) {
-              cj[u] = __float_as_int(__ldg(static_cast<const float*>(J.src) + static_cast<uint64_t>(j) * dim + col));
-              pp[u] |= 0x80000000u;  // needs quantizing
-            } else {
-              cj[u] = __ldg(static_cast<const int32_t*>(J.src) + static_cast<uint64_t>(j) * dim + col);
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (pp[u] == 0xFFFFFFFFu) continue;
-          int32_t c = cj[u];
-          if (pp[u] & 0x80000000u) {
-            uint32_t rr = 0;
-            c = quantize_f32(__int_as_float(c), J.qp, &rr);
-          }
-          if (c != ci[u]) miss[pp[u] & 0x7FFFFFFFu] = 1;
-        }
-      }
-      __syncthreads();
-      for (uint32_t q = threadIdx.x; q < np; q += kBlock) {
-        const uint32_t r = plist[q];
-        if (!miss[q]) {
-          dec[r] = cand[r];
-          cand[r] = 0;
-        } else {  // hash collision: keep looking further back
-          cand[r] = search(r, cand[r] + 1);
-        }
-      }
-      __syncthreads();
-    }
-    uint64_t local = 0, nref = 0;
-    for (uint32_t r = threadIdx.x; r < T.rows; r += kBlock) {
-      const uint32_t found = dec[r];
-      const uint32_t sz = found ? 1u + varint_len(found) : static_cast<uint32_t>(__ldg(ri + T.row0 + r) >> 32);
-      lits[r] = sz;
-      local += sz;
-      nref += found != 0;
-      a.row_dec[J.row_base + T.row0 + r] = found;
-    }
-    if (a.d_stats) {  // match_stats (vlz.hpp:162-168)
-      nref = block_sum<unsigned long long>(nref, s_tmp64);
-      if (threadIdx.x == 0) {
-        atomicAdd(&a.d_stats[0], static_cast<unsigned long long>(T.rows) - nref);
-        atomicAdd(&a.d_stats[1], nref);
-      }
-      return;
-    }
-    my_bits = 8ull * block_sum<unsigned long long>(local, s_tmp64);
+  } else if (codec == EMBC_CODEC_VLZ) {  // phase 0 of a large call: match here
+    VlzSmem m;
+    m.sh = reinterpret_cast<uint32_t*>(aux);
+    m.dec = dec;
+    m.cand = lits + a.rows_cap;
+    m.plist = m.cand + a.rows_cap;
+    m.miss = m.plist + a.rows_cap;
+    m.bhead = reinterpret_cast<uint32_t*>(stage);  // the output stage idles until the bytes pass
+    m.chain_bytes = a.aux_off - a.stage_off;
+    m.hash_cap = a.hash_cap;
+    uint64_t nref = 0;
+    my_bits = 8ull * vlz_match_tile(J, T, codes, stride, a.row_info + J.row_base, a.row_dec + J.row_base, m, s_tmp32,
+                                    s_tmp64, &nref);
   } else {  // huffman
     if (lut_staged)
       for (uint32_t k = threadIdx.x; k < span; k += kBlock) sl[k] = __ldg(L + k);
@@ -1319,6 +1485,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
       }
     }
     __syncthreads();
+    TS(3);
     pre = s_pre;
     start = s_start;
     if (last && threadIdx.x == 0) {  // the job's records (header, pack table, metadata)
@@ -1454,6 +1621,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
       }
     }
     __syncthreads();
+    TS(4);
     copy_out_staged(dst, stage, tot);
     return;
   }
@@ -1501,6 +1669,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
   const uint32_t nbytes_stage = (endbit + 7) / 8;
   for (uint32_t w = threadIdx.x; w < (nbytes_stage + 3) / 4; w += kBlock) words[w] = __byte_perm(words[w], 0, 0x0123);
   __syncthreads();
+  TS(4);
   const uint32_t nbytes = nbytes_stage - mis;  // output bytes touched by this tile
   const bool head_shared = b0 != 0;
   const bool tail_shared = !last && (endbit & 7) != 0;
@@ -1710,6 +1879,7 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   const size_t o_tiles = cv.take<DTile>(ntiles);
   const size_t o_st = cv.take<JobState>(njobs);
   const size_t o_flags = cv.take<uint32_t>(8);
+  const size_t o_hready = cv.take<uint32_t>(ntiles + 1);
   const size_t host_bytes = cv.off;  // everything above is uploaded from the host
   const size_t o_info = cv.take<uint64_t>(total_rows + 1);
   const size_t o_tstat = cv.take<unsigned long long>(ntiles + 1);
@@ -1753,6 +1923,7 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   }
   uint32_t flags0[8] = {host_abort ? JF_ABORT : 0u, 0, 0, 0, 0, 0, 0, 0};
   std::memcpy(hs + o_flags, flags0, sizeof(flags0));
+  std::memset(hs + o_hready, 0, sizeof(uint32_t) * (ntiles + 1));
   uint8_t* d = ctx->d_scratch;
   ce = stage_upload(ctx, d, hs, host_bytes, slot, stream);
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "descriptor upload");
@@ -1777,8 +1948,34 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   sa.book.gs_stride = p2cap;
   sa.book.nhuff = nhuff;
   sa.book.flags = reinterpret_cast<uint32_t*>(d + o_flags);
+  static const uint32_t fused_max = getenv("EMBC_FUSED_MAX") ? atoi(getenv("EMBC_FUSED_MAX")) : 1024;
+  // small calls: one fused E2 pass (sizes, decoupled look-back, bytes) -- the
+  // look-back is cheap when every tile is resident at once -- with the vlz
+  // matching in E1; large calls: E2 sizes (matching included) + layout, then
+  // bytes, with no waiting at all
+  const bool fused = !d_stats && ntiles <= fused_max;
+  sa.match = fused || d_stats ? 1u : 0u;
   sa.hist_off = stats_codes_bytes(vals_max, rows_max);
-  const uint32_t stats_smem = sa.hist_off + (nhuff ? kWin * 4 : 0);
+  sa.row_dec = reinterpret_cast<uint32_t*>(d + o_rdec);
+  sa.hready = reinterpret_cast<uint32_t*>(d + o_hready);
+  sa.d_stats = d_stats;
+  uint32_t stats_aux = nhuff ? kWin * 4 : 0;
+  {
+    uint32_t wmax = 0;
+    bool any_vlz = false;
+    for (uint32_t j = 0; j < njobs; ++j)
+      if (jobs[j].codec == EMBC_CODEC_VLZ && jobs[j].window_ok) {
+        any_vlz = true;
+        wmax = std::max(wmax, jobs[j].window);
+      }
+    if (any_vlz && sa.match) {
+      sa.rows_cap = rows_max;
+      sa.hash_cap = static_cast<uint32_t>(std::min<uint64_t>(kHashStage, static_cast<uint64_t>(wmax) + rows_max));
+      sa.chain_bytes = 4 * 2048 + 2 * sa.hash_cap;
+      stats_aux = std::max<uint32_t>(stats_aux, 4 * sa.hash_cap + 16 * sa.rows_cap + sa.chain_bytes);
+    }
+  }
+  const uint32_t stats_smem = sa.hist_off + stats_aux;
 
   EMBC_TIMED(ctx, "k_stats", stream, k_stats<<<ntiles, kBlock, stats_smem, stream>>>(sa));
 
@@ -1806,19 +2003,23 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   ea.err = ctx->d_err;
   ea.d_stats = d_stats;
   bool has_vlz = false, has_huf = false;
-  uint32_t wmax = 0;
   for (uint32_t j = 0; j < njobs; ++j) {
     has_vlz |= jobs[j].codec == EMBC_CODEC_VLZ;
     has_huf |= jobs[j].codec == EMBC_CODEC_HUFFMAN;
-    if (jobs[j].codec == EMBC_CODEC_VLZ) wmax = std::max(wmax, jobs[j].window);
   }
   ea.stage_off = emit_codes_bytes(vals_max, rows_max);
   ea.aux_off = ea.stage_off + emit_stage_bytes(vals_max, rows_max, has_vlz);
   ea.rows_cap = rows_max;
-  ea.hash_cap = has_vlz ? static_cast<uint32_t>(std::min<uint64_t>(kHashStage, static_cast<uint64_t>(wmax) + rows_max)) : 0;
-  uint32_t aux_bytes = ea.hash_cap * 4 + ea.rows_cap * 20;
-  if (has_huf) aux_bytes = std::max<uint32_t>(aux_bytes, 8 * kLutStage);
-  ea.hash_cap = (aux_bytes - ea.rows_cap * 20) / 4;  // any slack widens the hash stage
+  // aux: [huffman LUT stage | vlz: hash stage (phase 0) ][vlz: match offset,
+  // token bytes, (phase 0:) candidate, pending list, miss per row]
+  uint32_t wmax = 0;
+  for (uint32_t j = 0; j < njobs; ++j)
+    if (jobs[j].codec == EMBC_CODEC_VLZ) wmax = std::max(wmax, jobs[j].window);
+  const uint32_t per_row = fused ? 8 : 20;
+  ea.hash_cap = has_vlz && !fused ? static_cast<uint32_t>(std::min<uint64_t>(kHashStage, static_cast<uint64_t>(wmax) + rows_max)) : 0;
+  uint32_t aux_bytes = ea.hash_cap * 4 + ea.rows_cap * per_row;
+  if (has_huf) aux_bytes = std::max<uint32_t>(aux_bytes, 8 * kLutStage + ea.rows_cap * 8);
+  ea.hash_cap = (aux_bytes - ea.rows_cap * per_row) / 4;  // any slack widens the hash stage
   const uint32_t emit_smem = ea.aux_off + aux_bytes;
   ea.row_dec = reinterpret_cast<uint32_t*>(d + o_rdec);
   ea.tile_bits = reinterpret_cast<uint64_t*>(d + o_tbits);
@@ -1828,17 +2029,16 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   // small calls: one fused pass (sizes, decoupled look-back, bytes) -- the
   // look-back is cheap when every tile is resident at once; large calls: sizes
   // + layout, then bytes, with no waiting at all
-  static const uint32_t fused_max = getenv("EMBC_FUSED_MAX") ? atoi(getenv("EMBC_FUSED_MAX")) : 1024;
-  if (!d_stats && ntiles <= fused_max) {
+  if (d_stats) {
+    // match_stats: the counts come from E1
+  } else if (fused) {
     ea.phase = 2;
     EMBC_TIMED(ctx, "k_emit", stream, k_emit<2><<<ntiles, kBlock, emit_smem, stream>>>(ea));
   } else {
     ea.phase = 0;
     EMBC_TIMED(ctx, "k_sizes", stream, k_emit<0><<<ntiles, kBlock, emit_smem, stream>>>(ea));
-    if (!d_stats) {
-      ea.phase = 1;
-      EMBC_TIMED(ctx, "k_emit", stream, k_emit<1><<<ntiles, kBlock, emit_smem, stream>>>(ea));
-    }
+    ea.phase = 1;
+    EMBC_TIMED(ctx, "k_emit", stream, k_emit<1><<<ntiles, kBlock, emit_smem, stream>>>(ea));
   }
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "encode launch");
