@@ -1,4 +1,4 @@
-// decode.cu -- sm_100a decompression in two launches: chunk parse/validation,
+// decode.cu -- sm_100a decompression in one launch: chunk parse/validation,
 // raw / vlz / huffman decoding and dequantization straight into the consumer
 // tensor.
 //
@@ -24,10 +24,15 @@
 //                   decoupled look-back for the block's true entry, then the
 //                   symbols, staged in shared memory and stored coalesced.
 //     raw tiles     u32le -> values.
-//   D2 k_dec_fin    reference rows copied from their roots; chunks the
-//                   parallel path flagged are re-walked by the exact
-//                   sequential decoders (the reference's first error and
-//                   message); the lowest failing chunk is folded.
+//     copy tiles    once a vlz chunk's segments are done: reference rows
+//                   copied from their roots.
+//     finishers     one per chunk, once its parallel decode is done: chunks
+//                   the parallel path flagged (or planned sequential) are
+//                   re-walked by the exact sequential decoders (the
+//                   reference's first error and message); the last finisher
+//                   folds the lowest failing chunk.
+//   Later roles only ever wait on earlier tickets, so every wait is on a CTA
+//   that is already resident or finished.
 //
 // Every malformed-input check of the reference is reproduced, in the
 // reference's order, so the first failure (and its message) is identical.
@@ -209,7 +214,7 @@ __device__ __forceinline__ bool rd_varint(const uint8_t* p, uint64_t L, uint64_t
 }
 
 __device__ __forceinline__ void k_dec_vlz_seq_cta(uint32_t bid, const DChunk* __restrict__ ch, DecState* __restrict__ st,
-                              const uint32_t* __restrict__ list, const uint32_t* __restrict__ vflag) {
+                              const uint32_t* list, const volatile uint32_t* vflag) {
   if (threadIdx.x != 0) return;
   const uint32_t c = bid;
   const DChunk C = ch[c];
@@ -738,8 +743,7 @@ __device__ __forceinline__ uint32_t popc_below(uint64_t bm, uint32_t p) {
 // Exact sequential walk (huffman.hpp:274-290) for flagged chunks: reproduces
 // the reference's first error (exhaustion / invalid prefix / count).
 __device__ __forceinline__ void k_dec_huff_seq_cta(uint32_t bid, const DChunk* __restrict__ ch, DecState* __restrict__ st,
-                               const uint32_t* __restrict__ list, uint8_t* __restrict__ tabs,
-                               const uint32_t* __restrict__ hflag) {
+                               const uint32_t* list, uint8_t* tabs, const volatile uint32_t* hflag) {
   if (threadIdx.x != 0) return;
   const uint32_t c = bid;
   const DChunk C = ch[c];
@@ -900,7 +904,9 @@ struct DecArgs {
   uint32_t* hflag;
   uint32_t* ready;
   uint32_t* cnt;               // per-chunk tail tickets
-  uint32_t* tickets;           // [0] D1 ticket, [1] D2 fold ticket
+  uint32_t* vdone;             // per chunk: vlz segments finished (the last one after the roots)
+  uint32_t* hdone;             // per chunk: huffman blocks finished
+  uint32_t* tickets;           // [0] role ticket, [1] fold ticket, [2] fallback count
   unsigned long long* seg_status;
   unsigned long long* blk_status;
   uint32_t* maps;              // vlz: per segment (dim + 1) entry maps
@@ -1668,57 +1674,39 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
 // ===========================================================================
 constexpr uint32_t kDecSmem = kVlzSmem > kHuffSmem ? kVlzSmem : kHuffSmem;
 
-__global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_t;
-  if (threadIdx.x == 0) s_t = atomicAdd(&a.tickets[0], 1u);
+// Completion counters of the decode roles: every thread fences its writes,
+// then one thread counts the CTA in; waiters spin on the count.
+__device__ __forceinline__ void done_signal(uint32_t* cnt) {
+  __threadfence();
   __syncthreads();
-  uint32_t t = s_t;  // roles in ticket order: look-back only ever waits on earlier tickets
-  DROLE(blockIdx.x, 0);
-  DTS(blockIdx.x, 1);
-  if (t < a.nchunks) {  // chunk CTA: header + (huffman) decode tables, then the ready flag
-    __shared__ DecState sS;
-    const DChunk& C = a.ch[t];
-    if (threadIdx.x == 0) sS = parse_chunk(C);
-    __syncthreads();
-    if (C.codec == EMBC_CODEC_HUFFMAN)
-      huff_tables(t, a.ch, sS, a.keys, a.tabs, a.hflag, reinterpret_cast<uint64_t*>(smem), a.smem_bytes / 8);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      a.st[t] = sS;
-      __threadfence();
-      *reinterpret_cast<volatile uint32_t*>(&a.ready[t]) = 1;
-    }
-    DTS(blockIdx.x, 7);
-    return;
+  if (threadIdx.x == 0) atomicAdd(cnt, 1u);
+}
+__device__ __forceinline__ void wait_count(const uint32_t* cnt, uint32_t n) {
+  uint32_t delay = 32;
+  while (*reinterpret_cast<const volatile uint32_t*>(cnt) < n) {
+    __nanosleep(delay);
+    delay = min(delay * 2, 256u);
   }
-  t -= a.nchunks;
-  if (t < a.nseg) {
-    vlz_segment(a, t, smem);
-    DTS(blockIdx.x, 7);
-    return;
-  }
-  t -= a.nseg;
-  if (t < a.nhblk) {
-    huff_block(a, t, smem);
-    DTS(blockIdx.x, 7);
-    return;
-  }
-  t -= a.nhblk;
-  DROLE(blockIdx.x, 3);
-  DTS(blockIdx.x, 1);
-  const RawTile T = a.raw[t];
-  const DChunk& C = a.ch[T.chunk];
-  raw_tile(C, parse_chunk(C), T);
-  DTS(blockIdx.x, 7);
+  __threadfence();
 }
 
-__global__ void __launch_bounds__(kBlock) k_dec_fin(DecArgs a) {
-  uint32_t b = blockIdx.x;
-  if (b < a.nctile) {  // reference rows <- their root rows
+// Reference rows <- their root rows, for one tile of a vlz chunk's rows, once
+// every segment of the chunk (and the roots tail) has finished.
+__device__ void copy_tile(const DecArgs& a, uint32_t b) {
+  {
+    __shared__ int s_skip;
+    const uint32_t c = a.ctile[3 * b];
+    if (threadIdx.x == 0) {
+      wait_count(&a.vdone[c], a.ch[c].nseg);
+      s_skip = *reinterpret_cast<volatile unsigned long long*>(&a.st[c].err) != ~0ull ||
+               *reinterpret_cast<volatile uint32_t*>(&a.vflag[c]);
+    }
+    __syncthreads();
+    if (s_skip) return;
+  }
+  {
     const uint32_t c = a.ctile[3 * b], r0 = a.ctile[3 * b + 1], nr = a.ctile[3 * b + 2];
     const DChunk& C = a.ch[c];
-    if (a.st[c].err != ~0ull || a.vflag[c]) return;
     const uint32_t* src = a.row_src + C.row_base;
     const uint32_t D = C.dim;
     // 16-B units per row when rows are 16-B aligned, else 4-B (8-B for fp64) elements
@@ -1736,7 +1724,7 @@ __global__ void __launch_bounds__(kBlock) k_dec_fin(DecArgs a) {
           const uint32_t rl = k / upr;
           cc[u] = k - rl * upr;
           rr[u] = r0 + rl;
-          ss[u] = src[rr[u]];
+          ss[u] = __ldcg(src + rr[u]);
         }
       }
 #pragma unroll
@@ -1745,24 +1733,34 @@ __global__ void __launch_bounds__(kBlock) k_dec_fin(DecArgs a) {
         if (vec) {
           const uint4* in = reinterpret_cast<const uint4*>(C.out) + static_cast<uint64_t>(ss[u]) * upr + cc[u];
           uint4* o = reinterpret_cast<uint4*>(C.out) + static_cast<uint64_t>(rr[u]) * upr + cc[u];
-          *o = *in;
+          *o = __ldcg(in);
         } else if (esz == 8) {
           static_cast<uint64_t*>(C.out)[static_cast<uint64_t>(rr[u]) * D + cc[u]] =
-              static_cast<const uint64_t*>(C.out)[static_cast<uint64_t>(ss[u]) * D + cc[u]];
+              __ldcg(static_cast<const unsigned long long*>(C.out) + static_cast<uint64_t>(ss[u]) * D + cc[u]);
         } else {
           static_cast<uint32_t*>(C.out)[static_cast<uint64_t>(rr[u]) * D + cc[u]] =
-              static_cast<const uint32_t*>(C.out)[static_cast<uint64_t>(ss[u]) * D + cc[u]];
+              __ldcg(static_cast<const unsigned int*>(C.out) + static_cast<uint64_t>(ss[u]) * D + cc[u]);
         }
       }
     }
-    return;
-  }
-  // exact sequential walkers for chunks the parallel path flagged, then the fold
-  const uint32_t c = b - a.nctile;
+    }
+}
+
+// Per chunk, once its parallel decode has finished: the exact sequential
+// walker when the chunk was planned sequential or the parallel path flagged
+// it; the last chunk to finish folds the first failure into the error record.
+__device__ void finish_chunk(const DecArgs& a, uint32_t c) {
   const uint8_t codec = a.ch[c].codec;
-  if (threadIdx.x == 0 && a.st[c].err == ~0ull &&
-      ((codec == EMBC_CODEC_VLZ && (a.ch[c].seq || a.vflag[c])) || (codec == EMBC_CODEC_HUFFMAN && a.hflag[c])))
-    atomicAdd(a.diag, 1u);
+  if (threadIdx.x == 0) {
+    wait_count(&a.ready[c], 1);
+    if (codec == EMBC_CODEC_VLZ && !a.ch[c].seq) wait_count(&a.vdone[c], a.ch[c].nseg);
+    if (codec == EMBC_CODEC_HUFFMAN) wait_count(&a.hdone[c], a.ch[c].nblk);
+    const bool ok = *reinterpret_cast<volatile unsigned long long*>(&a.st[c].err) == ~0ull;
+    if (ok && ((codec == EMBC_CODEC_VLZ && (a.ch[c].seq || *reinterpret_cast<volatile uint32_t*>(&a.vflag[c]))) ||
+               (codec == EMBC_CODEC_HUFFMAN && *reinterpret_cast<volatile uint32_t*>(&a.hflag[c]))))
+      atomicAdd(&a.tickets[2], 1u);
+  }
+  __syncthreads();
   if (codec == EMBC_CODEC_VLZ) k_dec_vlz_seq_cta(c, a.ch, a.st, nullptr, a.vflag);
   else if (codec == EMBC_CODEC_HUFFMAN) k_dec_huff_seq_cta(c, a.ch, a.st, nullptr, a.tabs, a.hflag);
   __shared__ int s_last;
@@ -1773,6 +1771,7 @@ __global__ void __launch_bounds__(kBlock) k_dec_fin(DecArgs a) {
   if (s_last) {
     __threadfence();
     dec_fold(a.st, a.nchunks, a.err);
+    if (threadIdx.x == 0) *a.diag = atomicAdd(&a.tickets[2], 0u);  // decode fallbacks of this call
 #ifdef EMBC_DEBUG
     if (threadIdx.x != 0) return;
     const uint32_t nb = a.nchunks + a.nseg + a.nhblk + a.nraw;
@@ -1832,6 +1831,62 @@ __global__ void __launch_bounds__(kBlock) k_dec_fin(DecArgs a) {
     }
 #endif
   }
+}
+
+__global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_t;
+  if (threadIdx.x == 0) s_t = atomicAdd(&a.tickets[0], 1u);
+  __syncthreads();
+  uint32_t t = s_t;  // roles in ticket order: look-back only ever waits on earlier tickets
+  DROLE(blockIdx.x, 0);
+  DTS(blockIdx.x, 1);
+  if (t < a.nchunks) {  // chunk CTA: header + (huffman) decode tables, then the ready flag
+    __shared__ DecState sS;
+    const DChunk& C = a.ch[t];
+    if (threadIdx.x == 0) sS = parse_chunk(C);
+    __syncthreads();
+    if (C.codec == EMBC_CODEC_HUFFMAN)
+      huff_tables(t, a.ch, sS, a.keys, a.tabs, a.hflag, reinterpret_cast<uint64_t*>(smem), a.smem_bytes / 8);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a.st[t] = sS;
+      __threadfence();
+      *reinterpret_cast<volatile uint32_t*>(&a.ready[t]) = 1;
+    }
+    DTS(blockIdx.x, 7);
+    return;
+  }
+  t -= a.nchunks;
+  if (t < a.nseg) {
+    vlz_segment(a, t, smem);
+    DTS(blockIdx.x, 7);
+    done_signal(&a.vdone[a.segs[t].chunk]);
+    return;
+  }
+  t -= a.nseg;
+  if (t < a.nhblk) {
+    huff_block(a, t, smem);
+    DTS(blockIdx.x, 7);
+    done_signal(&a.hdone[a.hblk_chunk[t]]);
+    return;
+  }
+  t -= a.nhblk;
+  if (t < a.nraw) {
+    DROLE(blockIdx.x, 3);
+    DTS(blockIdx.x, 1);
+    const RawTile T = a.raw[t];
+    const DChunk& C = a.ch[T.chunk];
+    raw_tile(C, parse_chunk(C), T);
+    DTS(blockIdx.x, 7);
+    return;
+  }
+  t -= a.nraw;
+  if (t < a.nctile) {
+    copy_tile(a, t);
+    return;
+  }
+  finish_chunk(a, t - a.nctile);
 }
 
 }  // namespace embc_dev
@@ -1933,7 +1988,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   const size_t o_segs = take(sizeof(SegPair) * (nseg + 1));
   const size_t o_hblk = take(sizeof(uint32_t) * (nhb + 1));
   const size_t o_ct = take(sizeof(uint32_t) * (ctiles.size() + 1));
-  const size_t o_flags = take(sizeof(uint32_t) * (4 * n + 4));  // vflag | hflag | ready | cnt | tickets
+  const size_t o_flags = take(sizeof(uint32_t) * (6 * n + 4));  // vflag | hflag | ready | cnt | vdone | hdone | tickets
   const size_t o_sst = take(sizeof(unsigned long long) * (nseg + 1));
   const size_t o_bst = take(sizeof(unsigned long long) * (nhb + 1));
   const size_t host_bytes = off;  // uploaded (status words and flags start at zero)
@@ -1970,7 +2025,9 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   a.hflag = flags + n;
   a.ready = flags + 2 * n;
   a.cnt = flags + 3 * n;
-  a.tickets = flags + 4 * n;
+  a.vdone = flags + 4 * n;
+  a.hdone = flags + 5 * n;
+  a.tickets = flags + 6 * n;
   a.seg_status = reinterpret_cast<unsigned long long*>(d + o_sst);
   a.blk_status = reinterpret_cast<unsigned long long*>(d + o_bst);
   a.maps = reinterpret_cast<uint32_t*>(d + o_maps);
@@ -1985,8 +2042,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   a.nhblk = nhb;
   a.nraw = static_cast<uint32_t>(raw_tiles.size());
   a.nctile = nct;
-  cudaMemsetAsync(ctx->d_diag, 0, sizeof(uint32_t), stream);
-  const uint32_t g1 = n + nseg + nhb + a.nraw;
+  const uint32_t g1 = n + nseg + nhb + a.nraw + nct + n;
   uint32_t dmax = 1;
   for (uint32_t c = 0; c < n; ++c)
     if (ch[c].codec == EMBC_CODEC_VLZ && !ch[c].seq) dmax = std::max(dmax, ch[c].dim);
@@ -1999,7 +2055,6 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   if (nseg) smem = std::max<uint32_t>(smem, std::min<uint32_t>(4 * rmax + 64, 48 * 1024));
   a.smem_bytes = smem;
   EMBC_TIMED(ctx, "k_dec_main", stream, k_dec_main<<<g1, kBlock, smem, stream>>>(a));
-  EMBC_TIMED(ctx, "k_dec_fin", stream, k_dec_fin<<<nct + n, kBlock, 0, stream>>>(a));
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "decode launch");
   return EMBC_OK;
