@@ -50,6 +50,7 @@ namespace embc_dev {
 #ifdef EMBC_DEBUG
 __device__ unsigned long long g_dts[16384][12];  // role, t1..t11 (t7 = end)
 __device__ unsigned long long g_dcalls;
+__device__ unsigned long long g_dloc[8];  // huffman blocks: local tables ok / not; ns in local build, in stage
 __device__ __forceinline__ unsigned long long dtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -114,7 +115,7 @@ __device__ DecState parse_chunk(const DChunk& C) {
     uint8_t hb[kHeader];
     const uint8_t* src = C.in;
 #pragma unroll
-    for (uint32_t k = 0; k < kHeader; ++k) hb[k] = k < C.length ? __ldg(src + k) : 0;
+    for (uint32_t k = 0; k < kHeader; ++k) hb[k] = k < C.length ? src[k] : 0;  // generic: global or a smem copy
     const uint8_t* p = hb;
     const uint64_t L = C.length;
     // field layout: magic[4] ver codec eb:8 dim:4 count:4 paylen:8
@@ -329,6 +330,90 @@ __device__ __forceinline__ uint64_t value_bits(int32_t code, double w, int kind)
   return static_cast<uint32_t>(code);
 }
 
+// Codebook of <= 64 entries by one warp (two entries per lane): entry checks
+// in entry order (huffman.hpp:137-141), Kraft (:143-148), canonical order
+// (length, symbol) by rank counting over the staged keys, canonical codes
+// (closed form of finalize, :165-181), duplicate symbols (:183-185).  Fills
+// tb.first/base/count (zeroed by the caller), vals / syms (if given) and the
+// left-aligned code starts.  Returns 0, or 1 length out of range (*bad =
+// entry << 8 | length), 2 Kraft, 3 duplicate symbol.
+__device__ int small_book_warp(const uint8_t* p, uint32_t nent, double w, int out_kind, HTab& tb, uint64_t* vals,
+                               int32_t* syms, uint64_t* starts, uint64_t* kk, unsigned long long* bad_out) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t k[2];
+  unsigned long long bad = ~0ull, kraft = 0;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const uint32_t i = r * 32 + lane;
+    k[r] = ~0ull;
+    if (i < nent) {
+      const uint32_t sym = static_cast<uint32_t>(ld_be(p + 12 + 5 * i, 4));
+      const uint32_t len = p[12 + 5 * i + 4];
+      if (len == 0 || len > 32) bad = min(bad, (static_cast<unsigned long long>(i) << 8) | len);
+      else kraft += 1ull << (32 - len);
+      k[r] = (static_cast<uint64_t>(len) << 32) | (sym ^ 0x80000000u);
+      kk[i] = k[r];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+    kraft += __shfl_xor_sync(0xffffffffu, kraft, o);
+  }
+  if (bad != ~0ull) {
+    *bad_out = bad;
+    return 1;
+  }
+  if (kraft > (1ull << 32)) return 2;
+  __syncwarp();
+  uint32_t rank[2] = {0, 0};
+  bool dup = false;
+  for (uint32_t j = 0; j < nent; ++j) {
+    const uint64_t kj = kk[j];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint32_t i = r * 32 + lane;
+      rank[r] += (kj < k[r] || (kj == k[r] && j < i)) ? 1u : 0u;
+      dup |= i < nent && j != i && static_cast<uint32_t>(kj) == static_cast<uint32_t>(k[r]);
+    }
+  }
+  if (__any_sync(0xffffffffu, dup)) return 3;
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+    if (r * 32 + lane < nent) kk[rank[r]] = k[r];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 2; ++r) k[r] = r * 32 + lane < nent ? kk[r * 32 + lane] : ~0ull;
+  unsigned long long carry = 0;
+  uint32_t prev_last = 0;  // length of the previous register's last element
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const uint32_t i = r * 32 + lane;
+    const bool v = i < nent;
+    const uint32_t ln = v ? static_cast<uint32_t>(k[r] >> 32) : 0;
+    const unsigned long long kr = v ? (1ull << (32 - ln)) : 0;
+    const unsigned long long inc = warp_incl_scan<unsigned long long>(kr);
+    const uint32_t lp = __shfl_up_sync(0xffffffffu, ln, 1);
+    const uint32_t lprev = lane ? lp : prev_last;
+    if (v) {
+      const uint32_t code = static_cast<uint32_t>((carry + inc - kr) >> (32 - ln));
+      const uint32_t sy = static_cast<uint32_t>(k[r]) ^ 0x80000000u;
+      if (i == 0 || lprev != ln) {
+        tb.first[ln] = code;
+        tb.base[ln] = i;
+      }
+      atomicAdd(&tb.count[ln], 1u);
+      if (syms) syms[i] = static_cast<int32_t>(sy);
+      vals[i] = value_bits(static_cast<int32_t>(sy), w, out_kind);
+      starts[i] = (static_cast<uint64_t>(code) << (32 - ln)) | (static_cast<uint64_t>(ln) << 56);
+    }
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+    prev_last = __shfl_sync(0xffffffffu, ln, 31);
+  }
+  return 0;
+}
+
 // Codebook of <= 64 entries: validation (huffman.hpp:132-148, entry order),
 // canonical codes (finalize, :165-186), duplicate check (:183-185) by one warp
 // in registers (two entries per lane); the prefix LUT by the whole CTA.
@@ -345,85 +430,13 @@ __device__ void huff_tables_small(const DChunk& C, DecState& S, const uint8_t* p
   if (threadIdx.x == 0) s_stop2 = 0;
   __syncthreads();
   if (threadIdx.x < 32) {
-    uint32_t sym[2], len[2];
-    unsigned long long bad = ~0ull, kraft = 0;
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const uint32_t i = r * 32 + lane;
-      sym[r] = 0;
-      len[r] = 0;
-      if (i < nent) {
-        sym[r] = static_cast<uint32_t>(ld_be(p + 12 + 5ull * i, 4));
-        len[r] = p[12 + 5ull * i + 4];
-        if (len[r] == 0 || len[r] > 32) bad = min(bad, (static_cast<unsigned long long>(i) << 8) | len[r]);
-        else kraft += 1ull << (32 - len[r]);
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
-      kraft += __shfl_xor_sync(0xffffffffu, kraft, o);
-    }
-    if (bad != ~0ull || kraft > (1ull << 32)) {  // length range in entry order, then Kraft
-      if (lane == 0) {
-        if (bad != ~0ull) dec_fail(S, bad >> 8, EMBC_R_HUF_LEN_RANGE, bad & 0xFF, 0);
-        else dec_fail(S, 0, EMBC_R_HUF_KRAFT, 0, 0);
-        s_stop2 = 1;
-      }
-    } else {
-      // canonical order (length, symbol)
-      uint64_t k[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-        k[r] = r * 32 + lane < nent ? (static_cast<uint64_t>(len[r]) << 32) | (sym[r] ^ 0x80000000u) : ~0ull;
-      warp_sort_regs<2>(k);
-      const double w = 2.0 * S.eb;
-      unsigned long long carry = 0;
-      uint32_t prev_last = 0;  // length of the previous register's last element
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const uint32_t i = r * 32 + lane;
-        const bool v = i < nent;
-        const uint32_t ln = v ? static_cast<uint32_t>(k[r] >> 32) : 0;
-        const unsigned long long kr = v ? (1ull << (32 - ln)) : 0;
-        const unsigned long long inc = warp_incl_scan<unsigned long long>(kr);
-        const uint32_t lp = __shfl_up_sync(0xffffffffu, ln, 1);
-        const uint32_t lprev = lane ? lp : prev_last;
-        if (v) {
-          const uint32_t code = static_cast<uint32_t>((carry + inc - kr) >> (32 - ln));
-          const uint32_t sy = static_cast<uint32_t>(k[r]) ^ 0x80000000u;
-          if (i == 0 || lprev != ln) {
-            tb.first[ln] = code;
-            tb.base[ln] = i;
-          }
-          atomicAdd(&tb.count[ln], 1u);
-          hv.syms[i] = static_cast<int32_t>(sy);
-          hv.vals[i] = value_bits(static_cast<int32_t>(sy), w, C.out_kind);
-          starts[i] = (static_cast<uint64_t>(code) << (32 - ln)) | (static_cast<uint64_t>(ln) << 56);
-        }
-        carry += __shfl_sync(0xffffffffu, inc, 31);
-        prev_last = __shfl_sync(0xffffffffu, ln, 31);
-      }
-      // duplicate symbols (huffman.hpp:183-185): sort by symbol, compare neighbours
-      uint64_t d[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-        d[r] = r * 32 + lane < nent ? (static_cast<uint64_t>(static_cast<uint32_t>(k[r]) ) << 32) | (r * 32 + lane) : ~0ull;
-      warp_sort_regs<2>(d);
-      bool dup = false;
-      uint64_t prevd = 0;
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const uint32_t i = r * 32 + lane;
-        const uint64_t up = __shfl_up_sync(0xffffffffu, d[r], 1);
-        const uint64_t before = lane ? up : prevd;
-        if (i > 0 && i < nent && (before >> 32) == (d[r] >> 32)) dup = true;
-        prevd = __shfl_sync(0xffffffffu, d[r], 31);
-      }
-      if (__any_sync(0xffffffffu, dup) && lane == 0) {
-        dec_fail(S, 0, EMBC_R_HUF_DUP, 0, 0);
-        s_stop2 = 1;
-      }
+    unsigned long long bad = 0;
+    const int r = small_book_warp(p, nent, 2.0 * S.eb, C.out_kind, tb, hv.vals, hv.syms, starts, starts + 64, &bad);
+    if (r && (threadIdx.x & 31) == 0) {
+      if (r == 1) dec_fail(S, bad >> 8, EMBC_R_HUF_LEN_RANGE, bad & 0xFF, 0);
+      else if (r == 2) dec_fail(S, 0, EMBC_R_HUF_KRAFT, 0, 0);
+      else dec_fail(S, 0, EMBC_R_HUF_DUP, 0, 0);
+      s_stop2 = 1;
     }
   }
   __syncthreads();
@@ -470,6 +483,105 @@ __device__ void huff_tables_small(const DChunk& C, DecState& S, const uint8_t* p
     S.bit_off = tb.bit_off;
     if (S.nsym != C.N) hflag[c] = 1;  // decoded count != dim*count (container.hpp:169-172)
   }
+}
+
+
+// Block-local decode tables for a small codebook (<= 64 entries): a huffman
+// block repeats the chunk CTA's checks and table build (huff_tables +
+// huff_tables_small) on a shared-memory copy of the chunk's first bytes, so it
+// need not wait for the chunk CTA.  Returns false when anything would differ
+// from the plain path (any failure, a larger codebook, a count mismatch): the
+// block then waits for the chunk CTA's verdict and tables.  Called by all
+// threads; `hb` holds min(length, kLocalHdr) bytes of the chunk.
+constexpr uint32_t kLocalHdr = kHeader + 12 + 5 * 64;
+__device__ bool huff_tables_local(const DChunk& C, const uint8_t* hb, HTab& tb, uint32_t* lut, uint64_t* vals,
+                                  uint64_t* starts) {
+  __shared__ int s_ok;
+  __shared__ uint32_t s_nent;
+  __shared__ double s_w;
+  if (threadIdx.x < 33) {
+    tb.count[threadIdx.x] = 0;
+    tb.first[threadIdx.x] = 0;
+    tb.base[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) {
+    DChunk Cl = C;
+    Cl.in = hb;
+    Cl.length = C.length;
+    const DecState S = parse_chunk(Cl);  // reads only the header bytes
+    bool ok = S.err == ~0ull;
+    const uint64_t L = S.pay_len;
+    const uint8_t* p = hb + S.pay_off;
+    uint64_t nent = 0;
+    if (ok) ok = L >= 12 && S.pay_off + 12 <= kLocalHdr;
+    if (ok) {
+      nent = ld_be(p + 8, 4);
+      ok = ld_be(p, 8) == C.N && nent >= 1 && nent <= 64 && nent <= (L - 12) / 5 && nent <= C.book_cap &&
+           S.pay_off + 12 + 5 * nent <= kLocalHdr;
+    }
+    s_ok = ok;
+    s_nent = static_cast<uint32_t>(nent);
+    s_w = 2.0 * S.eb;
+    if (ok) {
+      tb.nent = static_cast<uint32_t>(nent);
+      tb.nsym = C.N;
+      tb.bit_off = 12 + 5ull * nent;
+      tb.nbits = 8 * (L - tb.bit_off);
+    }
+  }
+  __syncthreads();
+#ifdef EMBC_DEBUG
+  const unsigned long long lt0 = dtime();
+#endif
+  if (!s_ok) return false;
+  const uint32_t nent = s_nent;
+  const uint8_t* p = hb + (C.payload_only ? 0 : kHeader);
+  if (threadIdx.x < 32) {
+    unsigned long long bad = 0;
+    if (small_book_warp(p, nent, s_w, C.out_kind, tb, vals, nullptr, starts, starts + 64, &bad) && threadIdx.x == 0)
+      s_ok = 0;
+  }
+  __syncthreads();
+#ifdef EMBC_DEBUG
+  const unsigned long long lt1 = dtime();
+#endif
+  if (!s_ok) return false;
+  for (uint32_t sl = threadIdx.x; sl < (1u << kL0); sl += blockDim.x) {
+    const uint64_t V = static_cast<uint64_t>(sl) << (32 - kL0);
+    const uint64_t Vend = V + (1ull << (32 - kL0));
+    int lo = 0, hi = static_cast<int>(nent) - 1, f = -1;
+    while (lo <= hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((starts[mid] & 0xFFFFFFFFFFull) <= V) {
+        f = mid;
+        lo = mid + 1;
+      } else {
+        hi = mid - 1;
+      }
+    }
+    uint32_t ent = 0;
+    if (f >= 0) {
+      const uint32_t ln = static_cast<uint32_t>(starts[f] >> 56);
+      const uint64_t a0 = starts[f] & 0xFFFFFFFFFFull;
+      if (V < a0 + (1ull << (32 - ln))) ent = ln <= kL0 ? (static_cast<uint32_t>(f) << 6) | ln : kLong;
+    }
+    if (!ent && f + 1 < static_cast<int>(nent) && (starts[f + 1] & 0xFFFFFFFFFFull) < Vend) ent = kLong;
+    lut[sl] = ent;
+  }
+  if (threadIdx.x == 0) {
+    uint32_t max_len = 0;
+    for (uint32_t l = 1; l <= 32; ++l)
+      if (tb.count[l]) max_len = l;
+    tb.max_len = max_len;
+  }
+  __syncthreads();
+#ifdef EMBC_DEBUG
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_dloc[4], lt1 - lt0);
+    atomicAdd(&g_dloc[5], dtime() - lt1);
+  }
+#endif
+  return true;
 }
 
 __device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState& S,
@@ -519,7 +631,7 @@ __device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState&
   __syncthreads();
   if (s_stop) return;
   const uint32_t nent = S.nent;
-  if (nent <= 64 && skey_cap >= 64) {  // small codebooks: one warp in registers, the LUT by the CTA
+  if (nent <= 64 && skey_cap >= 128) {  // small codebooks: one warp, the LUT by the CTA
     huff_tables_small(C, S, p, L, hv, tb, reinterpret_cast<uint64_t*>(skey), c, hflag);
     return;
   }
@@ -1321,42 +1433,64 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
       stage_bits(W + kHPre, hwords - kHPre, bits, nby, bit0);
     }
   };
+  // the chunk's first bytes (header, codebook of up to 64 entries) in one round
+  __shared__ __align__(8) uint8_t s_hb[kLocalHdr + 8];
+  __shared__ uint64_t s_vals[64], s_starts[128];
+  for (uint32_t k = threadIdx.x; k < kLocalHdr; k += blockDim.x) s_hb[k] = k < C.length ? __ldg(C.in + k) : 0;
+  __syncthreads();
   const uint64_t poff = C.payload_only ? 0 : kHeader;
   uint64_t boff = 0, nby = 0;
   if (C.length >= poff + 12) {
-    const uint8_t* hp = C.in + poff + 8;
-    const uint32_t ne = (static_cast<uint32_t>(__ldg(hp)) << 24) | (static_cast<uint32_t>(__ldg(hp + 1)) << 16) |
-                        (static_cast<uint32_t>(__ldg(hp + 2)) << 8) | __ldg(hp + 3);
-    boff = 12 + 5ull * ne;
+    boff = 12 + 5 * ld_be(s_hb + poff + 8, 4);
     if (C.length - poff >= boff) nby = C.length - poff - boff;
   }
+#ifdef EMBC_DEBUG
+  const unsigned long long dt0 = dtime();
+#endif
   stage(C.in + poff + boff, nby);
-  if (threadIdx.x == 0) {  // the chunk CTA (an earlier ticket) publishes the tables
-    uint32_t delay = 32;
-    while (!*reinterpret_cast<volatile uint32_t*>(&a.ready[c])) {
-      __nanosleep(delay);
-      delay = min(delay * 2, 256u);
+#ifdef EMBC_DEBUG
+  __syncthreads();
+  const unsigned long long dt1 = dtime();
+#endif
+  // small calls (128-subsequence blocks) build block-local tables: there the
+  // blocks start with the chunk CTAs and would otherwise wait on them
+  const bool local = hsub == 128 && huff_tables_local(C, s_hb, t, lut, s_vals, s_starts);
+#ifdef EMBC_DEBUG
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_dloc[local ? 0 : 1], 1ull);
+    atomicAdd(&g_dloc[2], dtime() - dt1);
+    atomicAdd(&g_dloc[3], dt1 - dt0);
+  }
+#endif
+  const uint64_t* vals = s_vals;
+  if (!local) {
+    if (threadIdx.x == 0) {  // the chunk CTA (an earlier ticket) publishes the verdict and the tables
+      uint32_t delay = 32;
+      while (!*reinterpret_cast<volatile uint32_t*>(&a.ready[c])) {
+        __nanosleep(delay);
+        delay = min(delay * 2, 256u);
+      }
+      __threadfence();
+      const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&a.st[c].err);
+      s_use = e == ~0ull && !*reinterpret_cast<volatile uint32_t*>(&a.hflag[c]);
     }
-    __threadfence();
-    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&a.st[c].err);
-    s_use = e == ~0ull && !*reinterpret_cast<volatile uint32_t*>(&a.hflag[c]);
-  }
-  __syncthreads();
-  if (!s_use) {  // nothing to decode: still publish, so later blocks never wait
-    if (threadIdx.x == 0) st_vol(a.blk_status + gb, kStInc | huf_state(1, 0, 0));
-    return;
-  }
-  const DecState& S = a.st[c];
-  HView hv = hview(a.tabs, C);
-  // tables written by another CTA of this launch: read through L2
-  for (uint32_t i = threadIdx.x; i < (1u << kL0); i += blockDim.x) lut[i] = __ldcg(hv.lut + i);
-  for (uint32_t i = threadIdx.x; i < sizeof(HTab) / 4; i += blockDim.x)
-    reinterpret_cast<uint32_t*>(&t)[i] = __ldcg(reinterpret_cast<const unsigned int*>(hv.tab) + i);
-  __syncthreads();
-  const uint64_t pay_off = __ldcg(reinterpret_cast<const unsigned long long*>(&S.pay_off));
-  if (pay_off != poff || t.bit_off != boff || t.nbits != 8 * nby) {  // uniform: shared / L2 values
-    stage(C.in + pay_off + t.bit_off, t.nbits / 8);
     __syncthreads();
+    if (!s_use) {  // nothing to decode: still publish, so later blocks never wait
+      if (threadIdx.x == 0) st_vol(a.blk_status + gb, kStInc | huf_state(1, 0, 0));
+      return;
+    }
+    HView hv = hview(a.tabs, C);
+    // tables written by another CTA of this launch: read through L2
+    for (uint32_t i = threadIdx.x; i < (1u << kL0); i += blockDim.x) lut[i] = __ldcg(hv.lut + i);
+    for (uint32_t i = threadIdx.x; i < sizeof(HTab) / 4; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(&t)[i] = __ldcg(reinterpret_cast<const unsigned int*>(hv.tab) + i);
+    __syncthreads();
+    vals = hv.vals;
+    const uint64_t pay_off = __ldcg(reinterpret_cast<const unsigned long long*>(&a.st[c].pay_off));
+    if (pay_off != poff || t.bit_off != boff || t.nbits != 8 * nby) {  // uniform: shared / L2 values
+      stage(C.in + pay_off + t.bit_off, t.nbits / 8);
+      __syncthreads();
+    }
   }
   // two codewords per lookup when both fit the kL0-bit window:
   // luta = len1 | len2 << 5 | n << 10  (n: 0 long code, 1 one codeword, 2 two, 3 invalid prefix)
@@ -1606,7 +1740,8 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   }
   __syncthreads();  // Gs is dead: its bytes take the symbols
   const bool staged = nent <= 65536;
-  const uint64_t* vals = hv.vals;
+  // per-entry output values: block-local (shared) or the chunk CTA's (global, L2)
+  auto ldv = [&](uint32_t k) -> uint64_t { return local ? vals[k] : __ldcg(vals + k); };
   if (threadIdx.x < nloc && !pk_term(q)) {
     const uint32_t i = threadIdx.x, g = i / 32;
     const uint64_t gbase = bit0 + static_cast<uint64_t>(i) * kSubBits;
@@ -1634,7 +1769,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
       if (staged) {
         outs[gi - blk_base] = static_cast<uint16_t>(ent);
       } else {
-        const uint64_t v = __ldcg(vals + ent);
+        const uint64_t v = ldv(ent);
         if (C.out_kind == EMBC_OUT_F64) static_cast<uint64_t*>(C.out)[gi] = v;
         else static_cast<uint32_t*>(C.out)[gi] = static_cast<uint32_t>(v);
       }
@@ -1653,19 +1788,19 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   const bool vstage = nent <= (f64 ? (1u << kL0) / 2 : (1u << kL0));
   if (vstage) {
     if (f64)
-      for (uint32_t k = threadIdx.x; k < nent; k += blockDim.x) reinterpret_cast<uint64_t*>(lut)[k] = __ldcg(vals + k);
+      for (uint32_t k = threadIdx.x; k < nent; k += blockDim.x) reinterpret_cast<uint64_t*>(lut)[k] = ldv(k);
     else
-      for (uint32_t k = threadIdx.x; k < nent; k += blockDim.x) lut[k] = static_cast<uint32_t>(__ldcg(vals + k));
+      for (uint32_t k = threadIdx.x; k < nent; k += blockDim.x) lut[k] = static_cast<uint32_t>(ldv(k));
     __syncthreads();
   }
   if (f64) {
     uint64_t* o = static_cast<uint64_t*>(C.out) + blk_base;
     const uint64_t* sv = reinterpret_cast<const uint64_t*>(lut);
-    for (uint32_t k = threadIdx.x; k < nout; k += blockDim.x) o[k] = vstage ? sv[outs[k]] : __ldcg(vals + outs[k]);
+    for (uint32_t k = threadIdx.x; k < nout; k += blockDim.x) o[k] = vstage ? sv[outs[k]] : ldv(outs[k]);
   } else {
     uint32_t* o = static_cast<uint32_t*>(C.out) + blk_base;
     for (uint32_t k = threadIdx.x; k < nout; k += blockDim.x)
-      o[k] = vstage ? lut[outs[k]] : static_cast<uint32_t>(__ldcg(vals + outs[k]));
+      o[k] = vstage ? lut[outs[k]] : static_cast<uint32_t>(ldv(outs[k]));
   }
 }
 
@@ -1776,6 +1911,10 @@ __device__ void finish_chunk(const DecArgs& a, uint32_t c) {
     if (threadIdx.x != 0) return;
     const uint32_t nb = a.nchunks + a.nseg + a.nhblk + a.nraw;
     if (a.nchunks >= 26 && (++g_dcalls) % 8 == 7 && nb <= 16384) {
+      printf("D1 huffman blocks: local tables %llu, waited %llu; mean ns local build %llu (warp %llu, lut %llu), stage %llu\n",
+             g_dloc[0], g_dloc[1], g_dloc[2] / max(1ull, g_dloc[0] + g_dloc[1]), g_dloc[4] / max(1ull, g_dloc[0]),
+             g_dloc[5] / max(1ull, g_dloc[0]), g_dloc[3] / max(1ull, g_dloc[0] + g_dloc[1]));
+      for (int q = 0; q < 8; ++q) g_dloc[q] = 0;
       unsigned long long t0 = ~0ull;
       for (uint32_t k = 0; k < nb; ++k) t0 = min(t0, g_dts[k][1]);
       const char* names[4] = {"chunk", "vlzseg", "hufblk", "raw"};
