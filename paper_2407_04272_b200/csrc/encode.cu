@@ -132,6 +132,7 @@ __host__ __device__ constexpr uint32_t stats_codes_bytes(uint32_t vals, uint32_t
   return (vals + rows) * 4 > 16384 ? ((vals + rows) * 4 + 15) & ~15u : 16384u;
 }
 constexpr uint32_t kStatsVlzAux = 4 * kHashStage + 16 * kMaxTileRows + 4 * 2048 + 2 * kHashStage;
+constexpr uint32_t kEncodeSmemMax = 200 * 1024;  // k_encode (merged E1 + E2): picked per call when it fits
 constexpr uint32_t kStatsSmemMax =
     stats_codes_bytes(kMaxRowVals, kMaxTileRows) + (kWin * 4 > kStatsVlzAux ? kWin * 4 : kStatsVlzAux);
 
@@ -777,7 +778,7 @@ struct StatsArgs {
 
 // E1's vector loop, one instantiation per codec (no codec branches inside):
 // 128-bit loads, 4 quads in flight per thread; a vlz row is qpr consecutive lanes.
-template <int CODEC>
+template <int CODEC, bool STAGE_HUF>
 __device__ __forceinline__ void stats_vec(const DJob& J, uint64_t e0, uint32_t ne, uint32_t qpr, uint64_t gbase,
                                           uint64_t* __restrict__ row_info, uint32_t* shist, int32_t* codes,
                                           unsigned long long& lerr, int& lmin, int& lmax, bool& lwide) {
@@ -816,6 +817,10 @@ __device__ __forceinline__ void stats_vec(const DJob& J, uint64_t e0, uint32_t n
           if (huf) {
             lmin = min(lmin, c[k]);
             lmax = max(lmax, c[k]);
+            if (STAGE_HUF) {
+              const uint32_t l = 4 * q + k;
+              codes[l + (l >> 5)] = c[k];
+            }
           }
         }
       }
@@ -849,28 +854,18 @@ __device__ __forceinline__ void stats_vec(const DJob& J, uint64_t e0, uint32_t n
   }
 }
 
-__global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+// E1 on one tile.  MERGED (the single-launch encode of small calls): the
+// tile's codes stay in shared memory for E2 (huffman padded l + l/32, vlz
+// row-major), the codebook scratch lives past them (smem + hist_off), and the
+// job's codebook is published through JobState::flags.
+template <bool MERGED>
+__device__ __forceinline__ void stats_tile(const StatsArgs& a, const uint32_t tid, uint8_t* smem) {
   __shared__ unsigned long long s_err;
   __shared__ int s_min, s_max, s_last;
-  __shared__ uint32_t s_tk;
-  // tiles in ticket order: a vlz tile only ever waits on earlier tickets
-  if (threadIdx.x == 0) s_tk = atomicAdd(&a.book.flags[CF_TICKET_S], 1u);
-  __syncthreads();
-  const uint32_t tid = s_tk;
   TS1(0);
   const DTile T = a.tiles[tid];
   const DJob& J = a.jobs[T.job];
-  // E2 scratch of this call starts clean
   if (threadIdx.x == 0) {
-    a.tile_status[tid] = 0;
-    a.edge_slot[tid] = 0;
-    if (tid == J.tile0) {  // job status word, payload-bit sum, sized-tile count
-      a.job_status[T.job * kJobStride] = 0;
-      a.job_status[T.job * kJobStride + 1] = 0;
-      a.job_status[T.job * kJobStride + 2] = 0;
-    }
-    if (tid == 0) a.book.flags[CF_TICKET] = 0;
     s_err = ~0ull;
     s_min = INT_MAX;
     s_max = INT_MIN;
@@ -894,13 +889,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
   const uint64_t gbase = J.row_base + T.row0;
   if (vec) {
     int32_t* codes = reinterpret_cast<int32_t*>(smem);
-    if (vlz) stats_vec<EMBC_CODEC_VLZ>(J, e0, ne, qpr, gbase, a.row_info, shist, codes, lerr, lmin, lmax, lwide);
-    else if (huf) stats_vec<EMBC_CODEC_HUFFMAN>(J, e0, ne, qpr, gbase, a.row_info, shist, codes, lerr, lmin, lmax, lwide);
-    else stats_vec<EMBC_CODEC_RAW>(J, e0, ne, qpr, gbase, a.row_info, shist, codes, lerr, lmin, lmax, lwide);
+    if (vlz) stats_vec<EMBC_CODEC_VLZ, false>(J, e0, ne, qpr, gbase, a.row_info, shist, codes, lerr, lmin, lmax, lwide);
+    else if (huf)
+      stats_vec<EMBC_CODEC_HUFFMAN, MERGED>(J, e0, ne, qpr, gbase, a.row_info, shist, codes, lerr, lmin, lmax, lwide);
+    else stats_vec<EMBC_CODEC_RAW, false>(J, e0, ne, qpr, gbase, a.row_info, shist, codes, lerr, lmin, lmax, lwide);
   } else {
     // generic path: element loop, vlz codes staged at r * (dim|1) + col
     int32_t* codes = reinterpret_cast<int32_t*>(smem);
-    const uint32_t stride = dim | 1u;
+    const uint32_t stride = MERGED ? dim : (dim | 1u);  // MERGED: E2's row-major layout
     for (uint32_t l0 = 0; l0 < ne; l0 += kBlock) {
       const uint32_t l = l0 + threadIdx.x;
       const bool ok = l < ne;
@@ -925,6 +921,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
         const uint32_t r = fdiv(l, J.fd);
         codes[r * stride + (l - r * dim)] = c;
       }
+      if (MERGED && huf && ok) codes[l + (l >> 5)] = c;
     }
     if (vlz) {
       __syncthreads();
@@ -1009,7 +1006,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
     m.chain_bytes = a.chain_bytes;
     m.hash_cap = a.hash_cap;
     uint64_t nref = 0;
-    vlz_match_tile(J, T, reinterpret_cast<const int32_t*>(smem), vec ? dim : (dim | 1u), a.row_info + J.row_base,
+    vlz_match_tile(J, T, reinterpret_cast<const int32_t*>(smem), vec || MERGED ? dim : (dim | 1u), a.row_info + J.row_base,
                    a.row_dec + J.row_base, m, s_tmp32, s_tmp64, &nref);
     if (a.d_stats && threadIdx.x == 0) {  // match_stats (vlz.hpp:162-168)
       atomicAdd(&a.d_stats[0], static_cast<unsigned long long>(T.rows) - nref);
@@ -1026,8 +1023,22 @@ __global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
   if (!s_last) return;
   __threadfence();
   TS1(3);
-  build_book(J, Sp, a.book, smem);
+  build_book(J, Sp, a.book, MERGED ? smem + a.hist_off : smem);
+  if (MERGED) {  // the job's codebook (or its failure) is final
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t*>(&Sp->flags) = 1;
+  }
   TS1(4);
+}
+
+__global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_tk;
+  // tiles in ticket order: a vlz tile only ever waits on earlier tickets
+  if (threadIdx.x == 0) s_tk = atomicAdd(&a.book.flags[CF_TICKET_S], 1u);
+  __syncthreads();
+  stats_tile<false>(a, s_tk, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1293,24 +1304,22 @@ __device__ void layout_tail(const EmitArgs& a) {
   }
 }
 
-// PHASE 0: sizes + layout (last CTA); 1: bytes; 2: fused (sizes, look-back, bytes)
-template <int PHASE>
-__global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+// E2 on one tile.  PHASE 0: sizes + layout (last CTA); 1: bytes; 2: fused
+// (sizes, look-back, bytes).  MERGED (phase 2 after E1 in the same CTA): the
+// codes are already in shared memory; the quantization verdict is final only
+// once the look-back has passed, so a failed call still publishes every
+// size (nothing ever waits forever), skips the bytes, and the last ticket folds
+// the failure.
+template <int PHASE, bool MERGED>
+__device__ __forceinline__ void emit_tile(const EmitArgs& a, const uint32_t tid, uint8_t* smem) {
   __shared__ uint32_t s_tmp32[33];
   __shared__ unsigned long long s_tmp64[33];
-  __shared__ uint32_t s_t;
-  __shared__ unsigned long long s_pre, s_start;
-  // phase 2 (fused, small calls): tiles in ticket order, so the look-back only
-  // ever waits on CTAs that are already running
-  if (threadIdx.x == 0) s_t = PHASE == 2 ? atomicAdd(&a.flags[CF_TICKET], 1u) : blockIdx.x;
-  __syncthreads();
-  const uint32_t tid = s_t;
+  __shared__ unsigned long long s_pre, s_start, s_total;
   TS(0);
 #ifdef EMBC_DEBUG
   EmitEnd dbg_end{tid, PHASE == 2 ? a.ntiles : 0xFFFFFFFFu};
 #endif
-  if (*reinterpret_cast<volatile uint32_t*>(&a.flags[CF_ABORT]) & JF_ABORT) {
+  if (!MERGED && (*reinterpret_cast<volatile uint32_t*>(&a.flags[CF_ABORT]) & JF_ABORT)) {
     if (tid == 0 && PHASE != 1 && !a.d_stats) fold_failure(a);
     return;
   }
@@ -1342,13 +1351,13 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
     for (uint32_t r = threadIdx.x; r < T.rows; r += kBlock) {
       const uint32_t o = a.row_dec[J.row_base + T.row0 + r];
       dec[r] = o;
-      lits[r] = o ? 1u + varint_len(o) : static_cast<uint32_t>(__ldg(ri + r) >> 32);
+      lits[r] = o ? 1u + varint_len(o) : static_cast<uint32_t>((MERGED ? __ldcg(ri + r) : __ldg(ri + r)) >> 32);
     }
     __syncthreads();
   }
   // ---- 1. codes of the tile into shared memory (vlz: row stride dim|1;
   //         huffman: l + l/32, conflict-free thread-contiguous reads)
-  if (codec != EMBC_CODEC_RAW && ne) {
+  if (!MERGED && codec != EMBC_CODEC_RAW && ne) {
     const bool vec = (dim & 3) == 0 && (reinterpret_cast<uintptr_t>(J.src) & 15) == 0;
     if (vec) {
       const uint4* src4 = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(J.src) + e0);
@@ -1412,6 +1421,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
   const int32_t cmin = S.cmin;
   const uint32_t span = codec == EMBC_CODEC_HUFFMAN ? static_cast<uint32_t>(S.cmax - cmin + 1) : 0;
   const bool lut_staged = span <= kLutStage && 8 * span <= a.hash_cap * 4 + a.rows_cap * 8;
+  // MERGED: the LUT was written in this launch (L2 reads); a failed job has none
+  auto ldL = [&](uint32_t k) -> uint64_t { return MERGED ? __ldcg(L + k) : __ldg(L + k); };
+  const bool no_book = MERGED && codec == EMBC_CODEC_HUFFMAN &&
+                       *reinterpret_cast<const volatile unsigned long long*>(&S.err) != ~0ull;
   if (codec == EMBC_CODEC_RAW) {
     my_bits = 32ull * ne;
   } else if (codec == EMBC_CODEC_VLZ && phase != 0) {  // matched before
@@ -1431,15 +1444,17 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
     uint64_t nref = 0;
     my_bits = 8ull * vlz_match_tile(J, T, codes, stride, a.row_info + J.row_base, a.row_dec + J.row_base, m, s_tmp32,
                                     s_tmp64, &nref);
+  } else if (no_book) {  // MERGED, quantization failed: sized empty, never emitted
+    my_bits = 0;
   } else {  // huffman
     if (lut_staged)
-      for (uint32_t k = threadIdx.x; k < span; k += kBlock) sl[k] = __ldg(L + k);
+      for (uint32_t k = threadIdx.x; k < span; k += kBlock) sl[k] = ldL(k);
     __syncthreads();
     const uint32_t l0 = threadIdx.x * per_h, l1 = min(l0 + per_h, ne);
     uint32_t nb = 0;
     for (uint32_t l = l0; l < l1; ++l) {
       const uint32_t s = static_cast<uint32_t>(codes[l + (l >> 5)] - cmin);
-      nb += static_cast<uint32_t>((lut_staged ? sl[s] : __ldg(L + s)) & 0xFF);
+      nb += static_cast<uint32_t>((lut_staged ? sl[s] : ldL(s)) & 0xFF);
     }
     uint32_t tot;
     pos_thread = block_excl_scan<uint32_t>(nb, s_tmp32, &tot);
@@ -1491,9 +1506,25 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
     if (last && threadIdx.x == 0) {  // the job's records (header, pack table, metadata)
       const uint64_t P = book_bytes + (pre + my_bits + 7) / 8;
       write_job_records(a, jid, start, P);
-      if (tid == a.ntiles - 1) finish_call(a, start + hdr + P);
+      if (tid == a.ntiles - 1) {
+        if (!MERGED) finish_call(a, start + hdr + P);
+        else s_total = start + hdr + P;
+      }
     }
     if (tid == 0 && threadIdx.x == 0 && a.layout == EMBC_LAYOUT_PACKED && a.cap >= 4) st_le(a.out, a.njobs, 4);
+    if (MERGED) {
+      // the last ticket is past every other tile's E1: the abort flag is final
+      // there (earlier tiles may still emit bytes of a call that then fails)
+      __shared__ int s_abort;
+      __syncthreads();
+      if (threadIdx.x == 0) s_abort = (*reinterpret_cast<volatile uint32_t*>(&a.flags[CF_ABORT]) & JF_ABORT) != 0;
+      __syncthreads();
+      if (tid == a.ntiles - 1) {
+        if (s_abort) fold_failure(a);
+        else if (threadIdx.x == 0) finish_call(a, s_total);
+      }
+      if (s_abort) return;
+    }
   } else if (phase == 0) {
     // ---- 3a. sizes out; the last CTA to finish lays the call out
     __shared__ int s_last;
@@ -1649,7 +1680,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
     bool shared_word = true;  // the first word may be shared with the previous thread
     for (uint32_t l = l0; l < l1; ++l) {
       const uint32_t s = static_cast<uint32_t>(codes[l + (l >> 5)] - cmin);
-      const uint64_t e = lut_staged ? sl[s] : __ldg(L + s);
+      const uint64_t e = lut_staged ? sl[s] : ldL(s);
       const uint32_t len = static_cast<uint32_t>(e & 0xFF);
       buf |= (e >> 8) << (64 - used - len);
       used += len;
@@ -1694,6 +1725,51 @@ __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
       }
     }
   }
+}
+
+template <int PHASE>
+__global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_t;
+  // phase 2 (fused, small calls): tiles in ticket order, so the look-back only
+  // ever waits on CTAs that are already running
+  if (threadIdx.x == 0) s_t = PHASE == 2 ? atomicAdd(&a.flags[CF_TICKET], 1u) : blockIdx.x;
+  __syncthreads();
+  emit_tile<PHASE, false>(a, s_t, smem);
+}
+
+// Single-launch encode of small calls: E1 then E2 (phase 2) in the same CTA,
+// the tile's codes kept in shared memory.  Waits, all on earlier tickets
+// except one: vlz tiles on the window's hashes, E2 on earlier tiles' sizes,
+// and huffman tiles on their job's codebook, built by whichever tile of the
+// job finishes E1 last -- tickets are dealt in job order, so a job's tiles
+// hold consecutive tickets and the host only picks this kernel when every
+// job's tiles fit on the GPU at once.
+struct FusedArgs {
+  StatsArgs s;
+  EmitArgs e;
+};
+
+__global__ void __launch_bounds__(kBlock, 4) k_encode(FusedArgs f) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_t;
+  if (threadIdx.x == 0) s_t = atomicAdd(&f.s.book.flags[CF_TICKET_S], 1u);
+  __syncthreads();
+  const uint32_t tid = s_t;
+  stats_tile<true>(f.s, tid, smem);
+  const uint32_t jid = f.e.tiles[tid].job;
+  if (f.e.jobs[jid].codec == EMBC_CODEC_HUFFMAN) {
+    if (threadIdx.x == 0) {
+      uint32_t delay = 32;
+      while (!*reinterpret_cast<volatile uint32_t*>(&f.e.st[jid].flags)) {
+        __nanosleep(delay);
+        delay = min(delay * 2, 256u);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+  emit_tile<2, true>(f.e, tid, smem);
 }
 
 }  // namespace embc_dev
@@ -1880,11 +1956,12 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   const size_t o_st = cv.take<JobState>(njobs);
   const size_t o_flags = cv.take<uint32_t>(8);
   const size_t o_hready = cv.take<uint32_t>(ntiles + 1);
-  const size_t host_bytes = cv.off;  // everything above is uploaded from the host
-  const size_t o_info = cv.take<uint64_t>(total_rows + 1);
   const size_t o_tstat = cv.take<unsigned long long>(ntiles + 1);
   const size_t o_jstat = cv.take<unsigned long long>(kJobStride * (njobs + 1), 128);
   const size_t o_slot = cv.take<uint32_t>(ntiles + 1);
+  const size_t o_zero = o_hready;    // [hready .. edge slots] start at zero every call
+  const size_t host_bytes = cv.off;  // everything above is uploaded from the host
+  const size_t o_info = cv.take<uint64_t>(total_rows + 1);
   const size_t o_rdec = cv.take<uint32_t>(total_rows + 1);
   const size_t o_tbits = cv.take<uint64_t>(ntiles + 1);
   const size_t o_toff = cv.take<uint64_t>(ntiles + 1);
@@ -1923,7 +2000,7 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   }
   uint32_t flags0[8] = {host_abort ? JF_ABORT : 0u, 0, 0, 0, 0, 0, 0, 0};
   std::memcpy(hs + o_flags, flags0, sizeof(flags0));
-  std::memset(hs + o_hready, 0, sizeof(uint32_t) * (ntiles + 1));
+  std::memset(hs + o_zero, 0, host_bytes - o_zero);
   uint8_t* d = ctx->d_scratch;
   ce = stage_upload(ctx, d, hs, host_bytes, slot, stream);
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "descriptor upload");
@@ -1977,8 +2054,6 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   }
   const uint32_t stats_smem = sa.hist_off + stats_aux;
 
-  EMBC_TIMED(ctx, "k_stats", stream, k_stats<<<ntiles, kBlock, stats_smem, stream>>>(sa));
-
   EmitArgs ea{};
   ea.jobs = sa.jobs;
   ea.tiles = sa.tiles;
@@ -2025,7 +2100,38 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   ea.tile_bits = reinterpret_cast<uint64_t*>(d + o_tbits);
   ea.tile_off = reinterpret_cast<uint64_t*>(d + o_toff);
   ea.job_start = reinterpret_cast<uint64_t*>(d + o_jstart);
-  ea.done = sa.book.flags + CF_TICKET;  // zeroed by k_stats
+  ea.done = sa.book.flags + CF_TICKET;  // zeroed by the upload
+  ea.phase = 2;
+  // small calls whose tiles all fit on the GPU at once: E1 + E2 in one launch
+  // (k_encode), the codes kept in shared memory.  Layout: codes | E1 scratch
+  // (histogram window, vlz matching, codebook build) overlapping E2's stage + aux
+  if (fused) {
+    uint32_t e1 = nhuff ? std::max<uint32_t>(kWin * 4, kSmemBook * 32) : 0;
+    if (sa.match && sa.hash_cap) e1 = std::max<uint32_t>(e1, 4 * sa.hash_cap + 16 * sa.rows_cap + sa.chain_bytes);
+    const uint32_t merged_smem = ea.stage_off + std::max<uint32_t>(e1, emit_smem - ea.stage_off);
+    bool merged = merged_smem <= kEncodeSmemMax;
+    if (merged) {
+      int per_sm = 0, nsm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_encode, kBlock, merged_smem) != cudaSuccess ||
+          cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess) {
+        cudaGetLastError();
+        per_sm = 0;
+      }
+      merged = static_cast<uint64_t>(ntiles) <= static_cast<uint64_t>(per_sm) * nsm;
+    }
+    static const bool no_merge = getenv("EMBC_NO_MERGE") != nullptr;
+    if (merged && !no_merge) {
+      FusedArgs f;
+      sa.hist_off = ea.stage_off;
+      f.s = sa;
+      f.e = ea;
+      EMBC_TIMED(ctx, "k_encode", stream, k_encode<<<ntiles, kBlock, merged_smem, stream>>>(f));
+      ce = cudaGetLastError();
+      if (ce != cudaSuccess) return cuda_fail(ctx, ce, "encode launch");
+      return EMBC_OK;
+    }
+  }
+  EMBC_TIMED(ctx, "k_stats", stream, k_stats<<<ntiles, kBlock, stats_smem, stream>>>(sa));
   // small calls: one fused pass (sizes, decoupled look-back, bytes) -- the
   // look-back is cheap when every tile is resident at once; large calls: sizes
   // + layout, then bytes, with no waiting at all
@@ -2049,6 +2155,7 @@ cudaError_t encode_set_attributes() {
   cudaError_t e = cudaFuncSetAttribute(k_emit<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmemMax);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_emit<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmemMax);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_emit<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmitSmemMax);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, kEncodeSmemMax);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, kStatsSmemMax);
 }
