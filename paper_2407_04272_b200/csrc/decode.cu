@@ -50,7 +50,7 @@ namespace embc_dev {
 #ifdef EMBC_DEBUG
 __device__ unsigned long long g_dts[16384][12];  // role, t1..t11 (t7 = end)
 __device__ unsigned long long g_dcalls;
-__device__ unsigned long long g_dloc[8];  // huffman blocks: local tables ok / not; ns in local build, in stage
+__device__ unsigned long long g_dloc[12];  // huffman blocks: local tables ok / not; ns in local build, in stage
 __device__ __forceinline__ unsigned long long dtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -416,12 +416,11 @@ __device__ int small_book_warp(const uint8_t* p, uint32_t nent, double w, int ou
 
 // Codebook of <= 64 entries: validation (huffman.hpp:132-148, entry order),
 // canonical codes (finalize, :165-186), duplicate check (:183-185) by one warp
-// in registers (two entries per lane); the prefix LUT by the whole CTA.
+// (small_book_warp); the prefix LUT by the whole CTA.
 __device__ void huff_tables_small(const DChunk& C, DecState& S, const uint8_t* p, uint64_t L, HView hv, HTab& tb,
                                   uint64_t* starts, uint32_t c, uint32_t* __restrict__ hflag) {
   __shared__ int s_stop2;
   const uint32_t nent = S.nent;
-  const uint32_t lane = threadIdx.x & 31;
   if (threadIdx.x < 33) {
     tb.count[threadIdx.x] = 0;
     tb.first[threadIdx.x] = 0;
@@ -994,7 +993,6 @@ __host__ __device__ constexpr uint32_t vlz_smem(uint32_t dmax) {
   return vlz_bytes_cap(dmax) + ((vlz_unit_cap(dmax) * 2 + 15) & ~15u) + kLift * kSeg * 2 + 8 * (kSeg / 2);
 }
 constexpr uint32_t kVlzSmem = vlz_smem(kVlzMaxDim);
-constexpr uint32_t kRootBlock = 1024;   // rows resolved per pass of the root tail
 
 struct SegPair {
   uint32_t chunk, seg;
@@ -1042,7 +1040,7 @@ __device__ __forceinline__ uint64_t stage_varint(const uint8_t* B, uint32_t star
   return v;
 }
 
-__device__ void vlz_roots(const DecArgs& a, uint32_t c, uint8_t* smem);
+__device__ void vlz_end_check(const DecArgs& a, uint32_t c);
 
 __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   __shared__ uint32_t s_tmp32[33];
@@ -1294,7 +1292,7 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   __syncthreads();
   DTS(blockIdx.x, 9);
   if (threadIdx.x == 0 && (bad || s_bad)) atomicOr(&a.vflag[c], 1u);
-  // the chunk's last segment to finish checks the end state and resolves roots
+  // the chunk's last segment to finish checks the end state
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&a.cnt[c], 1u) == C.nseg - 1;
@@ -1302,70 +1300,19 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   DTS(blockIdx.x, 10);
   if (!s_last) return;
   __threadfence();
-  vlz_roots(a, c, smem);
+  vlz_end_check(a, c);
   DTS(blockIdx.x, 11);
 }
 
-// Reference chains -> root rows, in row blocks of kRootBlock: every source of
-// a row is an earlier row, so sources before the block are already final and
-// sources inside it resolve by pointer jumping.
-__device__ void vlz_roots(const DecArgs& a, uint32_t c, uint8_t* smem) {
-  __shared__ int s_ok;
+// The chunk's end state after its last segment (vlz.hpp:154-157): the token
+// chain must end exactly at the payload end with one vector per row.
+__device__ void vlz_end_check(const DecArgs& a, uint32_t c) {
+  if (threadIdx.x != 0) return;
   const DChunk& C = a.ch[c];
-  if (threadIdx.x == 0) {
-    const unsigned long long w = ld_vol(a.seg_status + C.seg0 + C.nseg - 1);
-    const bool dead = (w >> 61) & 1;
-    const uint32_t e = static_cast<uint32_t>(w >> 32) & 0x7FF, rows = static_cast<uint32_t>(w);
-    s_ok = !dead && rows == C.count && e == 0 && !*reinterpret_cast<volatile uint32_t*>(&a.vflag[c]);
-    if (!s_ok) a.vflag[c] = 1;
-  }
-  __syncthreads();
-  if (!s_ok) return;
-  uint32_t* src = a.row_src + C.row_base;
-  const bool in_smem = C.count <= a.smem_bytes / 4;
-  uint32_t* A = in_smem ? reinterpret_cast<uint32_t*>(smem) : src;  // whole chunk in smem when it fits
-  if (in_smem) {
-    for (uint32_t k0 = 0; k0 < C.count; k0 += 8 * blockDim.x) {
-      uint32_t v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t k = k0 + u * blockDim.x + threadIdx.x;
-        if (k < C.count) v[u] = __ldcg(src + k);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t k = k0 + u * blockDim.x + threadIdx.x;
-        if (k < C.count) A[k] = v[u];
-      }
-    }
-  }
-  __syncthreads();
-  for (uint32_t b0 = 0; b0 < C.count; b0 += kRootBlock) {
-    const uint32_t n = min(kRootBlock, C.count - b0);
-    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {  // sources before the block hold their root
-      const uint32_t s = in_smem ? A[b0 + k] : __ldcg(A + b0 + k);
-      if (s < b0) A[b0 + k] = in_smem ? A[s] : __ldcg(A + s);
-    }
-    if (!in_smem) __threadfence();
-    __syncthreads();
-    for (;;) {  // pointer jumping inside the block
-      bool changed = false;
-      for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
-        const uint32_t v = in_smem ? A[b0 + k] : __ldcg(A + b0 + k);
-        if (v >= b0 && v != b0 + k) {
-          const uint32_t vv = in_smem ? A[v] : __ldcg(A + v);
-          if (vv != v) {
-            A[b0 + k] = vv;
-            changed = true;
-          }
-        }
-      }
-      if (!in_smem) __threadfence();
-      if (!__syncthreads_or(changed)) break;
-    }
-  }
-  if (in_smem)
-    for (uint32_t k = threadIdx.x; k < C.count; k += blockDim.x) src[k] = A[k];
+  const unsigned long long w = ld_vol(a.seg_status + C.seg0 + C.nseg - 1);
+  const bool dead = (w >> 61) & 1;
+  const uint32_t e = static_cast<uint32_t>(w >> 32) & 0x7FF, rows = static_cast<uint32_t>(w);
+  if (dead || rows != C.count || e != 0) a.vflag[c] = 1;
 }
 
 // ===========================================================================
@@ -1827,7 +1774,7 @@ __device__ __forceinline__ void wait_count(const uint32_t* cnt, uint32_t n) {
 
 // Reference rows <- their root rows, for one tile of a vlz chunk's rows, once
 // every segment of the chunk (and the roots tail) has finished.
-__device__ void copy_tile(const DecArgs& a, uint32_t b) {
+__device__ void copy_tile(const DecArgs& a, uint32_t b, uint8_t* smem) {
   {
     __shared__ int s_skip;
     const uint32_t c = a.ctile[3 * b];
@@ -1842,8 +1789,36 @@ __device__ void copy_tile(const DecArgs& a, uint32_t b) {
   {
     const uint32_t c = a.ctile[3 * b], r0 = a.ctile[3 * b + 1], nr = a.ctile[3 * b + 2];
     const DChunk& C = a.ch[c];
-    const uint32_t* src = a.row_src + C.row_base;
+    uint32_t* src = a.row_src + C.row_base;
     const uint32_t D = C.dim;
+    // roots of the tile's rows: pointer jumping through row_src in L2.  Every
+    // copy tile of the chunk jumps its own rows at the same time, so each
+    // round also sees the other tiles' progress; a row's pointer only ever
+    // moves toward its root (the first occurrence, src == itself)
+    uint32_t* V = reinterpret_cast<uint32_t*>(smem);
+    for (uint32_t r = threadIdx.x; r < nr; r += blockDim.x) V[r] = __ldcg(src + r0 + r);
+    for (;;) {
+      bool changed = false;
+      for (uint32_t q0 = 0; q0 < nr; q0 += 4 * blockDim.x) {
+        uint32_t v[4], vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t r = q0 + u * blockDim.x + threadIdx.x;
+          v[u] = r < nr ? V[r] : 0;
+          vv[u] = (r < nr && v[u] != r0 + r) ? __ldcg(src + v[u]) : v[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t r = q0 + u * blockDim.x + threadIdx.x;
+          if (r < nr && vv[u] != v[u]) {
+            V[r] = vv[u];
+            __stcg(src + r0 + r, vv[u]);
+            changed = true;
+          }
+        }
+      }
+      if (!__syncthreads_or(changed)) break;
+    }
     // 16-B units per row when rows are 16-B aligned, else 4-B (8-B for fp64) elements
     const uint32_t esz = C.out_kind == EMBC_OUT_F64 ? 8 : 4;
     const bool vec = ((D * esz) & 15) == 0 && (reinterpret_cast<uintptr_t>(C.out) & 15) == 0;
@@ -1859,7 +1834,7 @@ __device__ void copy_tile(const DecArgs& a, uint32_t b) {
           const uint32_t rl = k / upr;
           cc[u] = k - rl * upr;
           rr[u] = r0 + rl;
-          ss[u] = __ldcg(src + rr[u]);
+          ss[u] = V[rl];
         }
       }
 #pragma unroll
@@ -1911,10 +1886,13 @@ __device__ void finish_chunk(const DecArgs& a, uint32_t c) {
     if (threadIdx.x != 0) return;
     const uint32_t nb = a.nchunks + a.nseg + a.nhblk + a.nraw;
     if (a.nchunks >= 26 && (++g_dcalls) % 8 == 7 && nb <= 16384) {
+      printf("D1 vlz roots: %llu chunks, mean %llu ns (rounds 2+: %llu ns, %llu rounds, %llu active after round 1)\n", g_dloc[7],
+             g_dloc[6] / max(1ull, g_dloc[7]), g_dloc[8] / max(1ull, g_dloc[7]), g_dloc[9] / max(1ull, g_dloc[7]),
+             g_dloc[10] / max(1ull, g_dloc[7]));
       printf("D1 huffman blocks: local tables %llu, waited %llu; mean ns local build %llu (warp %llu, lut %llu), stage %llu\n",
              g_dloc[0], g_dloc[1], g_dloc[2] / max(1ull, g_dloc[0] + g_dloc[1]), g_dloc[4] / max(1ull, g_dloc[0]),
              g_dloc[5] / max(1ull, g_dloc[0]), g_dloc[3] / max(1ull, g_dloc[0] + g_dloc[1]));
-      for (int q = 0; q < 8; ++q) g_dloc[q] = 0;
+      for (int q = 0; q < 12; ++q) g_dloc[q] = 0;
       unsigned long long t0 = ~0ull;
       for (uint32_t k = 0; k < nb; ++k) t0 = min(t0, g_dts[k][1]);
       const char* names[4] = {"chunk", "vlzseg", "hufblk", "raw"};
@@ -2022,7 +2000,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
   }
   t -= a.nraw;
   if (t < a.nctile) {
-    copy_tile(a, t);
+    copy_tile(a, t, smem);
     return;
   }
   finish_chunk(a, t - a.nctile);
@@ -2086,7 +2064,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
         C.row_base = row_total;
         row_total += r.count;
         for (uint32_t s = 0; s < C.nseg; ++s) segs.push_back(SegPair{c, s});
-        const uint32_t per = std::max<uint32_t>(8, 8192 / std::max<uint32_t>(r.dim, 1));
+        const uint32_t per = std::max<uint32_t>(8, std::min<uint32_t>(4096, 8192 / std::max<uint32_t>(r.dim, 1)));
         for (uint32_t r0 = 0; r0 < r.count; r0 += per) {
           ctiles.push_back(c);
           ctiles.push_back(r0);
@@ -2187,11 +2165,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
     if (ch[c].codec == EMBC_CODEC_VLZ && !ch[c].seq) dmax = std::max(dmax, ch[c].dim);
   a.vlz_dmax = dmax;
   a.hsub = hsub;
-  uint32_t rmax = 0;  // rows of the largest vlz chunk: the root tail keeps them in smem
-  for (uint32_t c = 0; c < n; ++c)
-    if (ch[c].codec == EMBC_CODEC_VLZ && !ch[c].seq) rmax = std::max(rmax, ch[c].count);
   uint32_t smem = std::max<uint32_t>(std::max<uint32_t>(nseg ? vlz_smem(dmax) : 0, nhb ? huff_smem(hsub) : 0), 16384);
-  if (nseg) smem = std::max<uint32_t>(smem, std::min<uint32_t>(4 * rmax + 64, 48 * 1024));
   a.smem_bytes = smem;
   EMBC_TIMED(ctx, "k_dec_main", stream, k_dec_main<<<g1, kBlock, smem, stream>>>(a));
   ce = cudaGetLastError();
