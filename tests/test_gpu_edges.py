@@ -157,3 +157,13 @@ def test_two_pass_encode_large_call(ctx, oracle):
     buf = K.pack_encode(jobs)
     table = K.unpack_table(buf)
     assert [buf[o:o + ln] for o, ln in table] == want
+
+
+@pytest.mark.parametrize("dim,n,classes", [(16, 8192, 1), (64, 8192, 3), (4, 30000, 2), (1, 20000, 5)])
+def test_long_reference_chains(ctx, oracle, dim, n, classes):
+    # every row a repeat of a handful of rows: reference chains thousands of
+    # rows deep, resolved by the copy tiles' pointer jumping
+    rng = np.random.default_rng(dim * 7 + classes)
+    rows = (rng.standard_normal((classes, dim)) * 0.05).astype(np.float32)
+    x = rows[rng.integers(0, classes, n)]
+    roundtrip(oracle, x.ravel(), dim, 0.01, 1)
