@@ -1,5 +1,5 @@
 # Evidence run: GPU tests, smoke, bench lines (KG default with CPU baseline, TB), reference arm,
-# ncu launch lists (KG, TB) and --set full captures of every kernel of one TB step.
+# ncu launch lists (KG, TB) and --set full captures of every kernel of one TB step and one KG step.
 TAG=${1:-r1}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
@@ -14,5 +14,7 @@ for WL in kg tb; do
 done
 timeout 1500 ncu --nvtx --nvtx-include "embc_step/" --set full --clock-control none --import-source on -c 5 -f \
   -o gpurun_out/ev_${TAG}_full_tb python bench.py --workload tb --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --nvtx --nvtx-include "embc_step/" --set full --clock-control none --import-source on -c 2 -f \
+  -o gpurun_out/ev_${TAG}_full_kg python bench.py --workload kg --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 tail -3 gpurun_out/ev_${TAG}_pytest_gpu.log; tail -1 gpurun_out/ev_${TAG}_smoke.log
 python tools/show_bench.py gpurun_out/ev_${TAG}_bench_kg.log gpurun_out/ev_${TAG}_bench_tb.log gpurun_out/ev_${TAG}_bench_ref.log
