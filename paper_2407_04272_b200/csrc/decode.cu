@@ -50,6 +50,7 @@ namespace embc_dev {
 #ifdef EMBC_DEBUG
 __device__ unsigned long long g_dts[16384][12];  // role, t1..t11 (t7 = end)
 __device__ unsigned long long g_dcalls;
+__device__ unsigned long long g_kspan[4] = {~0ull, 0, 0, 0};  // k_dec_main: first start, last end, CTAs done, calls
 __device__ unsigned long long g_dloc[12];  // huffman blocks: local tables ok / not; ns in local build, in stage
 __device__ __forceinline__ unsigned long long dtime() {
   unsigned long long t;
@@ -1956,6 +1957,24 @@ __global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
   if (threadIdx.x == 0) s_t = atomicAdd(&a.tickets[0], 1u);
   __syncthreads();
   uint32_t t = s_t;  // roles in ticket order: look-back only ever waits on earlier tickets
+#ifdef EMBC_DEBUG
+  struct SpanEnd {
+    uint32_t n;
+    __device__ ~SpanEnd() {
+      if (threadIdx.x != 0) return;
+      atomicMax(&g_kspan[1], dtime());
+      __threadfence();
+      if (atomicAdd(&g_kspan[2], 1ull) == n - 1) {
+        const unsigned long long k = atomicAdd(&g_kspan[3], 1ull);
+        if (k < 400) printf("KSPAN dec %llu %llu\n", g_kspan[0], atomicMax(&g_kspan[1], 0ull));
+        g_kspan[0] = ~0ull;
+        g_kspan[1] = 0;
+        g_kspan[2] = 0;
+      }
+    }
+  } span_end{gridDim.x};
+  if (threadIdx.x == 0) atomicMin(&g_kspan[0], dtime());
+#endif
   DROLE(blockIdx.x, 0);
   DTS(blockIdx.x, 1);
   if (t < a.nchunks) {  // chunk CTA: header + (huffman) decode tables, then the ready flag

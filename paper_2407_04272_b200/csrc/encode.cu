@@ -34,6 +34,7 @@ namespace embc_dev {
 __device__ unsigned long long g_dbg[8];
 __device__ unsigned long long g_ts[16384][10];
 __device__ uint32_t g_tc[16384];  // codec of the tile
+__device__ unsigned long long g_kspan[4] = {~0ull, 0, 0, 0};  // k_encode: first CTA start, last CTA end, CTAs done, calls
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -255,33 +256,38 @@ __device__ void book_warp(const DJob& J, JobState* Sp, const BookArgs& a, uint64
   // 2. leaves sorted by (count, symbol) (huffman.hpp:74-77)
   if (nsym > 1) warp_sort_smem(key, p2);
   TS1(8);
-  // 3. two-queue merge, leaf queue preferred on ties (huffman.hpp:91-109)
-  for (uint32_t i = lane; i < nsym; i += 32) wgt[i] = key[i] >> 32;
+  // 3. two-queue merge, leaf queue preferred on ties (huffman.hpp:91-109);
+  //    weights are symbol counts and their sums (< 2^32 values per chunk)
+  uint32_t* w32 = reinterpret_cast<uint32_t*>(wgt);
+  for (uint32_t i = lane; i < nsym; i += 32) w32[i] = static_cast<uint32_t>(key[i] >> 32);
   __syncwarp();
   if (nsym > 1 && lane == 0) {
-    // the merged queue's weights are created in non-decreasing order; its head
-    // and the leaf head are kept in registers, the next leaf prefetched
+    // the merged queue's weights are created in non-decreasing order; the two
+    // heads of each queue live in registers (wm == w32[mh] while mh < size,
+    // wm1 == w32[mh + 1] while mh + 1 < size), so no load is on the chain
     const uint32_t n = nsym, total = 2 * n - 1;
     uint32_t size = n, lh = 0, mh = n;
-    uint64_t wl = wgt[0], wl_next = n > 1 ? wgt[1] : 0, wm = 0;
+    uint32_t wl = w32[0], wl_next = n > 1 ? w32[1] : 0, wm = 0, wm1 = 0;
     while (size < total) {
       uint32_t ab[2];
-      uint64_t w2 = 0;
+      uint32_t w2 = 0;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        if (lh < n && (mh >= size || wl <= wm)) {
-          ab[k] = lh++;
-          w2 += wl;
-          wl = wl_next;
-          wl_next = lh + 1 < n ? wgt[lh + 1] : 0;
-        } else {
-          ab[k] = mh++;
-          w2 += wm;
-          wm = mh < size ? wgt[mh] : 0;
-        }
+      for (int k = 0; k < 2; ++k) {  // branch-free pick: selects, loads issued unconditionally
+        const bool tl = lh < n && (mh >= size || wl <= wm);
+        ab[k] = tl ? lh : mh;
+        w2 += tl ? wl : wm;
+        lh += tl ? 1u : 0u;
+        mh += tl ? 0u : 1u;
+        const uint32_t ln = w32[min(lh + 1, n - 1)];
+        const uint32_t mn = w32[min(mh + 1, total - 1)];
+        wl = tl ? wl_next : wl;
+        wl_next = tl ? ln : wl_next;
+        wm = tl ? wm : wm1;
+        wm1 = tl ? wm1 : mn;
       }
-      wgt[size] = w2;
+      w32[size] = w2;
       if (mh == size) wm = w2;  // the new node is the merged head
+      else if (mh + 1 == size) wm1 = w2;
       parent[ab[0]] = static_cast<int32_t>(size);
       parent[ab[1]] = static_cast<int32_t>(size);
       ++size;
@@ -1756,6 +1762,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_encode(FusedArgs f) {
   if (threadIdx.x == 0) s_t = atomicAdd(&f.s.book.flags[CF_TICKET_S], 1u);
   __syncthreads();
   const uint32_t tid = s_t;
+#ifdef EMBC_DEBUG
+  if (threadIdx.x == 0) atomicMin(&g_kspan[0], gtime());
+#endif
   stats_tile<true>(f.s, tid, smem);
   const uint32_t jid = f.e.tiles[tid].job;
   if (f.e.jobs[jid].codec == EMBC_CODEC_HUFFMAN) {
@@ -1770,6 +1779,19 @@ __global__ void __launch_bounds__(kBlock, 4) k_encode(FusedArgs f) {
     __syncthreads();
   }
   emit_tile<2, true>(f.e, tid, smem);
+#ifdef EMBC_DEBUG
+  if (threadIdx.x == 0) {
+    atomicMax(&g_kspan[1], gtime());
+    __threadfence();
+    if (atomicAdd(&g_kspan[2], 1ull) == f.e.ntiles - 1) {
+      const unsigned long long k = atomicAdd(&g_kspan[3], 1ull);
+      if (k < 400) printf("KSPAN enc %llu %llu\n", g_kspan[0], atomicMax(&g_kspan[1], 0ull));
+      g_kspan[0] = ~0ull;
+      g_kspan[1] = 0;
+      g_kspan[2] = 0;
+    }
+  }
+#endif
 }
 
 }  // namespace embc_dev
