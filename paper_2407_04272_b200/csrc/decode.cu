@@ -1571,13 +1571,15 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   }
   __syncthreads();
   DTS(blockIdx.x, 3);
-  // ---- B: group walks (Gs[i][r] = state at the entry of subsequence i for group entry r)
+  // ---- B: group walks (Gs[i][r] = state at the entry of subsequence i for group entry r);
+  //      hsub / 8 subsequences per group, so all eight warps walk
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t ng = (nloc + 31) / 32;
+  const uint32_t gs = hsub / 8, gsh = 31 - __clz(gs);
+  const uint32_t ng = (nloc + gs - 1) >> gsh;
   if (warp < ng) {
     uint32_t e = lane, term = lane < R ? 0 : 3, cnt = 0;  // entries >= max_len are unreachable
-    for (uint32_t j = 0; j < 32; ++j) {
-      const uint32_t i = warp * 32 + j;
+    for (uint32_t j = 0; j < gs; ++j) {
+      const uint32_t i = warp * gs + j;
       if (i >= nloc) break;
       Gs[i][lane] = pk(e, term, cnt);
       // lanes that reached the same entry share one result
@@ -1683,7 +1685,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   // ---- C: decode every subsequence from its true entry
   uint32_t q = pk(0, 1, 0);
   if (threadIdx.x < nloc) {
-    const uint32_t g = threadIdx.x / 32;
+    const uint32_t g = threadIdx.x >> gsh;
     if (!s_gt[g]) q = Gs[threadIdx.x][s_ge[g]];
   }
   __syncthreads();  // Gs is dead: its bytes take the symbols
@@ -1691,7 +1693,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   // per-entry output values: block-local (shared) or the chunk CTA's (global, L2)
   auto ldv = [&](uint32_t k) -> uint64_t { return local ? vals[k] : __ldcg(vals + k); };
   if (threadIdx.x < nloc && !pk_term(q)) {
-    const uint32_t i = threadIdx.x, g = i / 32;
+    const uint32_t i = threadIdx.x, g = i >> gsh;
     const uint64_t gbase = bit0 + static_cast<uint64_t>(i) * kSubBits;
     uint64_t gi = s_gc[g] + pk_cnt(q);  // index of this subsequence's first symbol
     uint32_t p = pk_off(q);
