@@ -116,7 +116,7 @@ __device__ DecState parse_chunk(const DChunk& C) {
     uint8_t hb[kHeader];
     const uint8_t* src = C.in;
 #pragma unroll
-    for (uint32_t k = 0; k < kHeader; ++k) hb[k] = k < C.length ? src[k] : 0;  // generic: global or a smem copy
+    for (uint32_t k = 0; k < kHeader; ++k) hb[k] = k < C.length ? __ldg(src + k) : 0;
     const uint8_t* p = hb;
     const uint64_t L = C.length;
     // field layout: magic[4] ver codec eb:8 dim:4 count:4 paylen:8
@@ -388,11 +388,13 @@ __device__ int small_book_warp(const uint8_t* p, uint32_t nent, double w, int ou
   for (int r = 0; r < 2; ++r) k[r] = r * 32 + lane < nent ? kk[r * 32 + lane] : ~0ull;
   unsigned long long carry = 0;
   uint32_t prev_last = 0;  // length of the previous register's last element
+  uint32_t maxl = 0;
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const uint32_t i = r * 32 + lane;
     const bool v = i < nent;
     const uint32_t ln = v ? static_cast<uint32_t>(k[r] >> 32) : 0;
+    maxl = max(maxl, ln);
     const unsigned long long kr = v ? (1ull << (32 - ln)) : 0;
     const unsigned long long inc = warp_incl_scan<unsigned long long>(kr);
     const uint32_t lp = __shfl_up_sync(0xffffffffu, ln, 1);
@@ -412,6 +414,8 @@ __device__ int small_book_warp(const uint8_t* p, uint32_t nent, double w, int ou
     carry += __shfl_sync(0xffffffffu, inc, 31);
     prev_last = __shfl_sync(0xffffffffu, ln, 31);
   }
+  maxl = __reduce_max_sync(0xffffffffu, maxl);
+  if (lane == 0) tb.max_len = maxl;
   return 0;
 }
 
@@ -505,23 +509,30 @@ __device__ bool huff_tables_local(const DChunk& C, const uint8_t* hb, HTab& tb, 
     tb.base[threadIdx.x] = 0;
   }
   if (threadIdx.x == 0) {
-    DChunk Cl = C;
-    Cl.in = hb;
-    Cl.length = C.length;
-    const DecState S = parse_chunk(Cl);  // reads only the header bytes
-    bool ok = S.err == ~0ull;
-    const uint64_t L = S.pay_len;
-    const uint8_t* p = hb + S.pay_off;
+    // parse_chunk's checks, all passing (any failure: the chunk CTA decides)
+    const uint64_t len = C.length;
+    const uint32_t poff = C.payload_only ? 0 : kHeader;
+    double eb = C.eb;
+    bool ok = len >= poff;
+    if (ok && !C.payload_only) {
+      const uint64_t ebits = ld_le(hb + 6, 8);
+      memcpy(&eb, &ebits, 8);
+      ok = hb[0] == 'E' && hb[1] == 'M' && hb[2] == 'B' && hb[3] == 'C' && hb[4] == 1 && hb[5] == C.codec &&
+           ld_le(hb + 22, 8) == len - kHeader && ld_le(hb + 14, 4) == C.dim && ld_le(hb + 18, 4) == C.count;
+    }
+    ok = ok && isfinite(eb) && eb > 0.0;
+    const uint64_t L = len - poff;
+    const uint8_t* p = hb + poff;
     uint64_t nent = 0;
-    if (ok) ok = L >= 12 && S.pay_off + 12 <= kLocalHdr;
+    if (ok) ok = L >= 12 && poff + 12 <= kLocalHdr;
     if (ok) {
       nent = ld_be(p + 8, 4);
       ok = ld_be(p, 8) == C.N && nent >= 1 && nent <= 64 && nent <= (L - 12) / 5 && nent <= C.book_cap &&
-           S.pay_off + 12 + 5 * nent <= kLocalHdr;
+           poff + 12 + 5 * nent <= kLocalHdr;
     }
     s_ok = ok;
     s_nent = static_cast<uint32_t>(nent);
-    s_w = 2.0 * S.eb;
+    s_w = 2.0 * eb;
     if (ok) {
       tb.nent = static_cast<uint32_t>(nent);
       tb.nsym = C.N;
@@ -546,33 +557,22 @@ __device__ bool huff_tables_local(const DChunk& C, const uint8_t* hb, HTab& tb, 
   const unsigned long long lt1 = dtime();
 #endif
   if (!s_ok) return false;
+  // the prefix LUT straight from the canonical tables: a slot is the codeword
+  // of length l <= kL0 whose code is its top l bits, else a prefix of a longer
+  // codeword (kLong), else no codeword (0)
+  const uint32_t ml = tb.max_len;
   for (uint32_t sl = threadIdx.x; sl < (1u << kL0); sl += blockDim.x) {
-    const uint64_t V = static_cast<uint64_t>(sl) << (32 - kL0);
-    const uint64_t Vend = V + (1ull << (32 - kL0));
-    int lo = 0, hi = static_cast<int>(nent) - 1, f = -1;
-    while (lo <= hi) {
-      const int mid = (lo + hi) >> 1;
-      if ((starts[mid] & 0xFFFFFFFFFFull) <= V) {
-        f = mid;
-        lo = mid + 1;
-      } else {
-        hi = mid - 1;
-      }
-    }
     uint32_t ent = 0;
-    if (f >= 0) {
-      const uint32_t ln = static_cast<uint32_t>(starts[f] >> 56);
-      const uint64_t a0 = starts[f] & 0xFFFFFFFFFFull;
-      if (V < a0 + (1ull << (32 - ln))) ent = ln <= kL0 ? (static_cast<uint32_t>(f) << 6) | ln : kLong;
+    for (uint32_t l = 1; l <= min(ml, kL0) && !ent; ++l) {
+      const uint32_t d = (sl >> (kL0 - l)) - tb.first[l];
+      if (d < tb.count[l]) ent = ((tb.base[l] + d) << 6) | l;
     }
-    if (!ent && f + 1 < static_cast<int>(nent) && (starts[f + 1] & 0xFFFFFFFFFFull) < Vend) ent = kLong;
+    for (uint32_t l = kL0 + 1; l <= ml && !ent; ++l) {
+      if (!tb.count[l]) continue;
+      const uint64_t f = tb.first[l];
+      if (sl >= (f >> (l - kL0)) && sl <= ((f + tb.count[l] - 1) >> (l - kL0))) ent = kLong;
+    }
     lut[sl] = ent;
-  }
-  if (threadIdx.x == 0) {
-    uint32_t max_len = 0;
-    for (uint32_t l = 1; l <= 32; ++l)
-      if (tb.count[l]) max_len = l;
-    tb.max_len = max_len;
   }
   __syncthreads();
 #ifdef EMBC_DEBUG
