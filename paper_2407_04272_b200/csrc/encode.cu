@@ -132,6 +132,7 @@ constexpr uint32_t kEmitSmemMax = emit_codes_bytes(kMaxRowVals, kMaxTileRows) +
 __host__ __device__ constexpr uint32_t stats_codes_bytes(uint32_t vals, uint32_t rows) {
   return (vals + rows) * 4 > 16384 ? ((vals + rows) * 4 + 15) & ~15u : 16384u;
 }
+constexpr uint32_t kTileHist = 256;  // bins of a huffman tile's kept histogram (two-pass calls)
 constexpr uint32_t kStatsVlzAux = 4 * kHashStage + 16 * kMaxTileRows + 4 * 2048 + 2 * kHashStage;
 constexpr uint32_t kEncodeSmemMax = 200 * 1024;  // k_encode (merged E1 + E2): picked per call when it fits
 constexpr uint32_t kStatsSmemMax =
@@ -780,6 +781,10 @@ struct StatsArgs {
   unsigned long long* d_stats;        // match_stats: (literal rows, reference rows)
   uint32_t hash_cap, rows_cap, chain_bytes;
   uint32_t match;                     // match here (fused E2 / match_stats); else E2's sizes pass does
+  // two-pass calls: a huffman tile's histogram (codes tile_hr.x .. + tile_hr.y),
+  // so E2's sizes pass prices the tile without re-reading it (y == 0: re-read)
+  uint32_t* tile_hist;
+  int2* tile_hr;
 };
 
 // E1's vector loop, one instantiation per codec (no codec branches inside):
@@ -976,10 +981,15 @@ __device__ __forceinline__ void stats_tile(const StatsArgs& a, const uint32_t ti
     uint32_t* gh = a.book.hist + static_cast<uint64_t>(J.hjob) * kWin;
     const uint32_t b0 = static_cast<uint32_t>(s_min + static_cast<int32_t>(kWin / 2));
     const uint32_t b1 = static_cast<uint32_t>(s_max + static_cast<int32_t>(kWin / 2));
+    const bool keep = !MERGED && a.tile_hist && b1 - b0 < kTileHist;
     for (uint32_t b = b0 + threadIdx.x; b <= b1; b += blockDim.x) {
       const uint32_t v = shist[b];
       if (v) atomicAdd(&gh[b], v);
+      if (keep) a.tile_hist[static_cast<uint64_t>(tid) * kTileHist + (b - b0)] = v;
     }
+    if (keep && threadIdx.x == 0) a.tile_hr[tid] = make_int2(s_min, static_cast<int>(b1 - b0 + 1));
+  } else if (!MERGED && a.tile_hr && threadIdx.x == 0) {
+    a.tile_hr[tid] = make_int2(0, 0);
   }
   TS1(2);
   if (vlz && a.match) {
@@ -1080,6 +1090,8 @@ struct EmitArgs {
   uint64_t* job_start;          // chunk offset of each job (layout)
   uint32_t* done;               // phase-0 completion ticket
   int phase;                    // 0: sizes + layout (last CTA), 1: bytes
+  const uint32_t* tile_hist;    // huffman tiles priced from E1's histograms (phase 0)
+  const int2* tile_hr;
 };
 
 __device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
@@ -1361,9 +1373,11 @@ __device__ __forceinline__ void emit_tile(const EmitArgs& a, const uint32_t tid,
     }
     __syncthreads();
   }
+  // phase 0 prices a huffman tile from its E1 histogram when it was kept
+  const int2 thr = (PHASE == 0 && codec == EMBC_CODEC_HUFFMAN && a.tile_hr) ? a.tile_hr[tid] : make_int2(0, 0);
   // ---- 1. codes of the tile into shared memory (vlz: row stride dim|1;
   //         huffman: l + l/32, conflict-free thread-contiguous reads)
-  if (!MERGED && codec != EMBC_CODEC_RAW && ne) {
+  if (!MERGED && codec != EMBC_CODEC_RAW && ne && thr.y == 0) {
     const bool vec = (dim & 3) == 0 && (reinterpret_cast<uintptr_t>(J.src) & 15) == 0;
     if (vec) {
       const uint4* src4 = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(J.src) + e0);
@@ -1452,6 +1466,13 @@ __device__ __forceinline__ void emit_tile(const EmitArgs& a, const uint32_t tid,
                                     s_tmp64, &nref);
   } else if (no_book) {  // MERGED, quantization failed: sized empty, never emitted
     my_bits = 0;
+  } else if (thr.y > 0) {  // phase 0: sum over the tile's histogram of count * code length
+    uint64_t nb = 0;
+    for (uint32_t b = threadIdx.x; b < static_cast<uint32_t>(thr.y); b += kBlock) {
+      const uint32_t cnt = a.tile_hist[static_cast<uint64_t>(tid) * kTileHist + b];
+      if (cnt) nb += static_cast<uint64_t>(cnt) * (ldL(static_cast<uint32_t>(thr.x + static_cast<int32_t>(b) - cmin)) & 0xFF);
+    }
+    my_bits = block_sum<unsigned long long>(nb, s_tmp64);
   } else {  // huffman
     if (lut_staged)
       for (uint32_t k = threadIdx.x; k < span; k += kBlock) sl[k] = ldL(k);
@@ -1991,6 +2012,11 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   hist_entries += kWidePool;  // [nhuff windows | wide pool], LUT mirrors the layout
   const size_t o_lut = cv.take<uint64_t>(hist_entries + 1);
   const size_t o_books = cv.take<uint8_t>(book_stride * std::max<uint32_t>(nhuff, 1));
+  static const uint32_t fused_max = getenv("EMBC_FUSED_MAX") ? atoi(getenv("EMBC_FUSED_MAX")) : 1024;
+  const bool two_pass = !d_stats && ntiles > fused_max;
+  const bool keep_hist = two_pass && nhuff > 0;  // E1 keeps huffman tile histograms for E2's sizes pass
+  const size_t o_thist = keep_hist ? cv.take<uint32_t>(static_cast<uint64_t>(ntiles) * kTileHist) : 0;
+  const size_t o_thr = keep_hist ? cv.take<int2>(ntiles) : 0;
   size_t o_gkey = 0, o_gwgt = 0, o_gpar = 0;
   if (big_books) {
     o_gkey = cv.take<uint64_t>(p2cap * nhuff);
@@ -2047,7 +2073,6 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   sa.book.gs_stride = p2cap;
   sa.book.nhuff = nhuff;
   sa.book.flags = reinterpret_cast<uint32_t*>(d + o_flags);
-  static const uint32_t fused_max = getenv("EMBC_FUSED_MAX") ? atoi(getenv("EMBC_FUSED_MAX")) : 1024;
   // small calls: one fused E2 pass (sizes, decoupled look-back, bytes) -- the
   // look-back is cheap when every tile is resident at once -- with the vlz
   // matching in E1; large calls: E2 sizes (matching included) + layout, then
@@ -2055,6 +2080,8 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   const bool fused = !d_stats && ntiles <= fused_max;
   sa.match = fused || d_stats ? 1u : 0u;
   sa.hist_off = stats_codes_bytes(vals_max, rows_max);
+  sa.tile_hist = keep_hist ? reinterpret_cast<uint32_t*>(d + o_thist) : nullptr;
+  sa.tile_hr = keep_hist ? reinterpret_cast<int2*>(d + o_thr) : nullptr;
   sa.row_dec = reinterpret_cast<uint32_t*>(d + o_rdec);
   sa.hready = reinterpret_cast<uint32_t*>(d + o_hready);
   sa.d_stats = d_stats;
@@ -2123,6 +2150,8 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   ea.tile_off = reinterpret_cast<uint64_t*>(d + o_toff);
   ea.job_start = reinterpret_cast<uint64_t*>(d + o_jstart);
   ea.done = sa.book.flags + CF_TICKET;  // zeroed by the upload
+  ea.tile_hist = sa.tile_hist;
+  ea.tile_hr = sa.tile_hr;
   ea.phase = 2;
   // small calls whose tiles all fit on the GPU at once: E1 + E2 in one launch
   // (k_encode), the codes kept in shared memory.  Layout: codes | E1 scratch
