@@ -250,12 +250,33 @@ __device__ __forceinline__ void warp_bitonic(uint64_t* key, uint32_t p2) {
 
 // Codebook of an alphabet of <= 256 symbols by one warp: the same steps as the
 // block version below (huffman.hpp:49-120 lengths, :165-186 canonical codes).
+// Ascending sort of n <= 64 distinct keys in shared memory by one warp: each
+// lane ranks its (up to) two keys against all n, then scatters.
+__device__ __forceinline__ void warp_rank_sort64(uint64_t* key, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t k0 = lane < n ? key[lane] : 0, k1 = lane + 32 < n ? key[lane + 32] : 0;
+  uint32_t r0 = 0, r1 = 0;
+#pragma unroll 4
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint64_t kj = key[j];
+    r0 += kj < k0 ? 1u : 0u;
+    r1 += kj < k1 ? 1u : 0u;
+  }
+  __syncwarp();
+  if (lane < n) key[r0] = k0;
+  if (lane + 32 < n) key[r1] = k1;
+  __syncwarp();
+}
+
 __device__ void book_warp(const DJob& J, JobState* Sp, const BookArgs& a, uint64_t* key, uint64_t* wgt,
                           int32_t* parent, uint32_t nsym, uint32_t p2, uint32_t* gh, uint64_t span, int32_t cmin,
                           uint64_t* L, uint8_t* book, uint64_t lut_off) {
   const uint32_t lane = threadIdx.x & 31;
-  // 2. leaves sorted by (count, symbol) (huffman.hpp:74-77)
-  if (nsym > 1) warp_sort_smem(key, p2);
+  // 2. leaves sorted by (count, symbol) (huffman.hpp:74-77); keys are distinct
+  if (nsym > 1) {
+    if (nsym <= 64) warp_rank_sort64(key, nsym);
+    else warp_sort_smem(key, p2);
+  }
   TS1(8);
   // 3. two-queue merge, leaf queue preferred on ties (huffman.hpp:91-109);
   //    weights are symbol counts and their sums (< 2^32 values per chunk)
@@ -319,8 +340,11 @@ __device__ void book_warp(const DJob& J, JobState* Sp, const BookArgs& a, uint64
   }
   __syncwarp();
   TS1(10);
-  // 5. canonical order (length asc, symbol asc)
-  if (nsym > 1) warp_sort_smem(key, p2);
+  // 5. canonical order (length asc, symbol asc); keys are distinct
+  if (nsym > 1) {
+    if (nsym <= 64) warp_rank_sort64(key, nsym);
+    else warp_sort_smem(key, p2);
+  }
   TS1(11);
   // 6. canonical codes: code_i = sum_{j<i} 2^(len_i - len_j) (finalize, huffman.hpp:170-181)
   unsigned long long carry = 0, bits = 0;
