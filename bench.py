@@ -421,7 +421,9 @@ def run_single(args):
             for k in range(nrep * E):
                 e2e_step(k)
 
-    e2e_run(4)
+    # warm-up: the PCIe link and host paths take a few ms of sustained traffic
+    # to reach their steady rate (the first replays run up to 2x slower)
+    e2e_run(30)
     torch.cuda.synchronize()
     if os.environ.get("EMBC_E2E_PROBE"):  # diagnostic: per-replay times, copies alone
         ts = []
