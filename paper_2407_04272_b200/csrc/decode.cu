@@ -1051,7 +1051,8 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   const SegPair sp = a.segs[gseg];
   const uint32_t c = sp.chunk;
   const DChunk& C = a.ch[c];
-  const DecState S = parse_chunk(C);
+  __shared__ unsigned long long s_err;
+  __shared__ double s_eb;
   DROLE(blockIdx.x, 1);
   const uint32_t D = C.dim;
   const uint32_t kUnitCap = vlz_unit_cap(a.vlz_dmax);
@@ -1059,9 +1060,11 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   uint16_t* uend = reinterpret_cast<uint16_t*>(smem + vlz_bytes_cap(a.vlz_dmax));  // unit terminal byte
   uint16_t(*J)[kSeg] = reinterpret_cast<uint16_t(*)[kSeg]>(reinterpret_cast<uint8_t*>(uend) + ((kUnitCap * 2 + 15) & ~15u));
   uint32_t* lit = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(J) + kLift * kSeg * 2);  // literal tokens (<= kSeg/2)
-  if (S.err != ~0ull) return;  // every CTA of the chunk sees it: nobody waits on this segment
-  const uint8_t* p = C.in + S.pay_off;
-  const uint64_t L = S.pay_len;
+  // the payload's place follows from the plan (the host cut the segments from
+  // length - header); the header is validated by thread 0 while the bytes load
+  const uint64_t poff = C.payload_only ? 0 : kHeader;
+  const uint8_t* p = C.in + poff;
+  const uint64_t L = C.length - poff;
   const uint32_t b0 = sp.seg * kSeg;
   const uint32_t nb = static_cast<uint32_t>(umin64(kSeg, L - b0));
   const uint32_t sb = b0 >= kSegBack ? b0 - kSegBack : 0;
@@ -1091,8 +1094,12 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   if (threadIdx.x == 0) {
     s_bad = 0;
     s_nlit = 0;
+    const DecState S = parse_chunk(C);
+    s_err = S.err;
+    s_eb = S.eb;
   }
   __syncthreads();
+  if (s_err != ~0ull) return;  // every CTA of the chunk sees it: nobody waits on this segment
   DTS(blockIdx.x, 2);
   // unit table: terminal bytes at payload offsets [b0, b0 + nb + la)
   uint32_t nu = 0, U = 0;
@@ -1235,7 +1242,7 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   if (!bad && row0 + T > C.count) bad = true;
   // every token of the segment: reference offsets validated (vlz.hpp:141-145),
   // literal tokens queued for the warp decoder
-  const double w = 2.0 * S.eb;
+  const double w = 2.0 * s_eb;
   uint32_t* row_src = a.row_src + C.row_base;
   if (!bad) {
     for (uint32_t t = threadIdx.x; t < T; t += blockDim.x) {
