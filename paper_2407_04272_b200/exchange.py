@@ -385,7 +385,9 @@ class CompressedAllToAll:
 
     def backward(self, iteration: int, grads: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
         """grads[t] for every table: [B, dim] local gradient slice.  Returns
-        {t: [R*B, dim]} for owned tables (rows s*B.. from rank s)."""
+        {t: [R*B, dim]} for owned tables (rows s*B.. from rank s).  With
+        groups > 1 the same pipeline as forward, over the destinations' owned
+        tables."""
         R, B = self.R, self.B
         jobs, job_dst = [], []
         for d in range(R):
@@ -395,6 +397,25 @@ class CompressedAllToAll:
                 job_dst.append(d)
         own = self.owned(self.rank)
         out = {t: torch.empty((R * B, self.dim), dtype=self.out_dtype, device=self.device) for t in own}
+        if self.groups > 1:  # group k = the k-th run of every destination's owned tables
+            G = min(self.groups, max(len(self.owned(r)) for r in range(R)))  # identical on every rank
+            mine = [self._split_of(len(own), G, k) for k in range(G)]
+            jobs_by, dst_by, plan_by, outs_by = [], [], [], []
+            for k in range(G):
+                jg, dg = [], []
+                for d in range(R):
+                    theirs = self.owned(d)
+                    for i in self._split_of(len(theirs), G, k):
+                        t = theirs[i]
+                        eb = P.eb_at(t, iteration, self.grad_profiles, self.grad_cfg)
+                        jg.append(K.EncodeJob(grads[t], eb, self._codec(self.grad_profiles, t), self.window))
+                        dg.append(d)
+                jobs_by.append(jg)
+                dst_by.append(dg)
+                plan_by.append([[(B, self.dim) for _ in mine[k]] for s in range(R)])
+                outs_by.append([[out[own[i]][s * B:(s + 1) * B] for i in mine[k]] for s in range(R)])
+            self._exchange_pipelined(jobs_by, dst_by, plan_by, outs_by)
+            return out
         recv_plan = [[(B, self.dim) for _ in own] for s in range(R)]
         outs = [[out[t][s * B:(s + 1) * B] for t in own] for s in range(R)]
         self._exchange(jobs, job_dst, recv_plan, outs)

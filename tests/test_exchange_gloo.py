@@ -136,6 +136,15 @@ def _worker(rank, world, port, q, mode):
                     if (s1.payload_bytes, s1.metadata_bytes, s1.uncompressed_bytes) != \
                             (sg.payload_bytes, sg.metadata_bytes, sg.uncompressed_bytes):
                         res["ok"] = False
+                    # backward through the same pipeline: gradients of every table -> owner
+                    grads = {t: (a1[t] * 0.5 + 0.01 * (t + 1)).contiguous() for t in range(T)}
+                    b1 = ex1.backward(it, grads)
+                    bg = exg.backward(it, grads)
+                    for t in ex1.owned(rank):
+                        if not torch.equal(b1[t], bg[t]):
+                            res["ok"] = False
+                    if ex1.stats.payload_bytes != exg.stats.payload_bytes:
+                        res["ok"] = False
             q.put((rank, res))
         else:  # simulator parity: one table per rank, reference seeding
             from oracle import Ref
@@ -194,7 +203,8 @@ def test_exchange_forward_backward_gloo():
 
 def test_exchange_pipelined_groups_gloo():
     """groups > 1 (compression / transfer / decompression overlapped per table
-    group) delivers the same values and accounting as one exchange."""
+    group) delivers the same values and accounting as one exchange, forward
+    and backward."""
     out = _run("pipelined")
     for r in (0, 1):
         assert out[r]["ok"], r

@@ -34,3 +34,10 @@ def test_pipelined_exchange_single_rank(ctx, oracle):
             x = look[t].cpu().numpy().astype(np.float64)
             want = oracle.decode_chunk(oracle.encode_chunk(x.ravel(), dim, profiles[t].eb, profiles[t].codec))
             assert np.array_equal(b[t].cpu().numpy(), want.astype(np.float32).reshape(B, dim)), (it, t)
+        grads = {t: (b[t] * 0.5 + 0.01).contiguous() for t in range(T)}
+        g1 = ex1.backward(it, grads)
+        g4 = ex4.backward(it, grads)
+        torch.cuda.synchronize()
+        assert ex1.stats.payload_bytes == ex4.stats.payload_bytes
+        for t in range(T):
+            assert torch.equal(g1[t], g4[t]), ("bwd", it, t)
