@@ -335,7 +335,9 @@ def run_single(args):
             ref_vals += K.match_stats(codes, 255)[1] * dim
     algo = {
         "k_stats": 4 * n_all,                                  # fp32 in
+        "k_sizes": 4 * n_all,                                  # fp32 in (re-read: vlz matching, huffman fallback)
         "k_emit": 4 * n_all + packed_mean,                     # fp32 in (L2 re-read) + chunks out
+        "k_encode": 4 * n_all + packed_mean,                   # fp32 in + chunks out (one launch)
         "k_dec_main": packed_mean + 4 * (n_all - ref_vals) + 8 * ref_vals,  # chunks in + rows out + ref copies
     }
     hbm, peak_kind = peaks()
