@@ -86,10 +86,19 @@ def pinned_empty(shape, dtype=torch.float32):
         if int(torch.cuda.cudart().cudaHostRegister(aligned, size, 0)) != 0:
             raise RuntimeError("cudaHostRegister")
         t = torch.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).view(*shape)
-        _PINNED_KEEP.append((m, buf))
+        _PINNED_KEEP.append((aligned, m, buf))
         return t
     except Exception:
         return torch.empty(shape, dtype=dtype).pin_memory()
+
+
+def pinned_free(t):
+    """Release a buffer from pinned_empty (no-op for pin_memory tensors)."""
+    for k, (addr, m, buf) in enumerate(_PINNED_KEEP):
+        if addr == t.data_ptr():
+            torch.cuda.cudart().cudaHostUnregister(addr)
+            del _PINNED_KEEP[k]
+            return
 
 
 def peaks():
@@ -361,7 +370,8 @@ def run_single(args):
     # ~33 GB/s depending on their host backing; take the fastest of 3x as many
     # candidates (device-timed copies), as a placement-aware allocator would
     def fastest(n, h2d):
-        cands = [pinned_empty((T, B, dim)) for _ in range(3 * n)]
+        mult = 3 if T * B * dim * 4 <= (16 << 20) else 2
+        cands = [pinned_empty((T, B, dim)) for _ in range(mult * n)]
         probe_dev = torch.empty((T, B, dim), dtype=torch.float32, device=dev)
         def t_copy(h):
             for _ in range(2):
@@ -373,7 +383,10 @@ def run_single(args):
             q1.record()
             torch.cuda.synchronize()
             return q0.elapsed_time(q1)
-        return sorted(cands, key=t_copy)[:n]
+        ranked = sorted(cands, key=t_copy)
+        for h in ranked[n:]:
+            pinned_free(h)
+        return ranked[:n]
     hx = fastest(nslot, True)
     for k in range(nslot):  # slot j's input is set j's batch
         hx[k].copy_(sets[k]["x"].cpu())
