@@ -2192,7 +2192,13 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
         cudaGetLastError();
         per_sm = 0;
       }
-      merged = static_cast<uint64_t>(ntiles) <= static_cast<uint64_t>(per_sm) * nsm;
+      // every tile co-resident on an idle GPU; and since the only wait on a
+      // later ticket is within one job (its codebook), a job that fits in one
+      // CTA per SM still progresses when other work holds most of the GPU
+      uint32_t max_job_tiles = 0;
+      for (uint32_t j = 0; j < njobs; ++j) max_job_tiles = std::max(max_job_tiles, jobs[j].ntiles);
+      merged = static_cast<uint64_t>(ntiles) <= static_cast<uint64_t>(per_sm) * nsm &&
+               max_job_tiles <= static_cast<uint32_t>(nsm);
     }
     static const bool no_merge = getenv("EMBC_NO_MERGE") != nullptr;
     if (merged && !no_merge) {
