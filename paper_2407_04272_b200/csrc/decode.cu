@@ -843,6 +843,21 @@ __device__ __forceinline__ void stage_bits(uint32_t* W, uint32_t nwords, const u
   }
 }
 
+// The five staged words around one subsequence (two before it, its two, one
+// after) in registers: 32 bits at bit offset pos in [-64, 64) of the
+// subsequence without a shared-memory access on the decode chain.
+struct SubWin {
+  uint32_t a0, a1, a2, a3, a4;
+  __device__ __forceinline__ SubWin(const uint32_t* W, uint32_t w0)
+      : a0(W[w0 - 2]), a1(W[w0 - 1]), a2(W[w0]), a3(W[w0 + 1]), a4(W[w0 + 2]) {}
+  __device__ __forceinline__ uint32_t peek(int pos) const {
+    const uint32_t k = static_cast<uint32_t>(pos + 64) >> 5;  // 0..3
+    const uint32_t hi = k == 0 ? a0 : k == 1 ? a1 : k == 2 ? a2 : a3;
+    const uint32_t lo = k == 0 ? a1 : k == 1 ? a2 : k == 2 ? a3 : a4;
+    return __funnelshift_l(lo, hi, static_cast<uint32_t>(pos) & 31);
+  }
+};
+
 // 32 bits at relative bit position p of the staged words.
 __device__ __forceinline__ uint32_t speek(const uint32_t* W, uint32_t p) {
   const uint32_t i = p >> 5;
@@ -1504,14 +1519,14 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   const uint32_t i_me = threadIdx.x;
   if (i_me < nloc) {
     const uint64_t gbase = bit0 + static_cast<uint64_t>(i_me) * kSubBits;
-    const uint32_t base = kHPre * 32 + i_me * kSubBits;  // W bit of the subsequence start
+    const SubWin win(W, kHPre + 2 * i_me);  // the subsequence starts at word kHPre + 2 i
     uint64_t bm = 0;
     uint32_t x0 = 0;
     // warm-up from 64 bits earlier (none at the very start of the stream)
     int p = gbase == 0 ? 0 : -64;
     for (;;) {
       if (p < 0) {
-        const uint32_t bits = speek(W, base + p);
+        const uint32_t bits = win.peek(p);
         const uint32_t la = luta[bits >> (32 - kL0)];
         if ((la >> 10) == 2 && p + static_cast<int>(la & 31) < 0) {  // both start before the subsequence
           p += static_cast<int>((la & 31) + ((la >> 5) & 31));
@@ -1537,7 +1552,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
         x0 = pk(0, 2, cnt);
         break;
       }
-      const uint32_t bits = speek(W, base + q);
+      const uint32_t bits = win.peek(static_cast<int>(q));
       const uint32_t la = luta[bits >> (32 - kL0)];
       if ((la >> 10) == 2) {  // two codewords, the second starting inside the subsequence
         const uint32_t l1 = la & 31, l12 = l1 + ((la >> 5) & 31);
@@ -1704,8 +1719,9 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     const uint64_t gbase = bit0 + static_cast<uint64_t>(i) * kSubBits;
     uint64_t gi = s_gc[g] + pk_cnt(q);  // index of this subsequence's first symbol
     uint32_t p = pk_off(q);
+    const SubWin cwin(W, kHPre + 2 * i);
     while (p < kSubBits && gi < N && gbase + p < nbits) {
-      const uint32_t bits = speek(W, kHPre * 32 + i * kSubBits + p);
+      const uint32_t bits = cwin.peek(static_cast<int>(p));
       if (staged && gi + 1 < N) {
         const uint32_t la = luta[bits >> (32 - kL0)];
         if ((la >> 10) == 2) {
