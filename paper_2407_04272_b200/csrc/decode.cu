@@ -1342,6 +1342,7 @@ __device__ void vlz_end_check(const DecArgs& a, uint32_t c) {
 // Huffman blocks: 128 subsequences of 64 bits.
 // ===========================================================================
 constexpr uint32_t kHSub = 256;                        // subsequences per block (one per thread)
+constexpr uint32_t kMaxGroups = 16;                    // group walks per block (8 warps, up to two each)
 constexpr uint32_t kHPre = 2;                          // words staged before the block (warm-up)
 // smem: LUT | two-codeword LUT | staged words | per-subsequence chain summaries | group states, later the symbols (u16)
 __host__ __device__ constexpr uint32_t huff_smem(uint32_t hsub) {
@@ -1372,9 +1373,9 @@ __device__ __forceinline__ unsigned long long huf_state(uint32_t term, uint32_t 
 //     shared memory; the block stores them coalesced.
 __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   __shared__ HTab t;
-  __shared__ uint32_t G[kHSub / 32][32], BM[32];
-  __shared__ uint32_t s_ge[kHSub / 32], s_gt[kHSub / 32];
-  __shared__ unsigned long long s_gc[kHSub / 32];
+  __shared__ uint32_t G[kMaxGroups][32], BM[32];
+  __shared__ uint32_t s_ge[kMaxGroups], s_gt[kMaxGroups];
+  __shared__ unsigned long long s_gc[kMaxGroups];
   __shared__ unsigned long long s_in;
   __shared__ int s_use;
   const uint32_t c = a.hblk_chunk[gb];
@@ -1594,21 +1595,28 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   __syncthreads();
   DTS(blockIdx.x, 3);
   // ---- B: group walks (Gs[i][r] = state at the entry of subsequence i for group entry r);
-  //      hsub / 8 subsequences per group, so all eight warps walk
+  //      every warp walks hsub / 8 subsequences: one group on 32 lanes, or,
+  //      when codes are at most 16 bits, two groups of half the length on 16
+  //      lanes each
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t gs = hsub / 8, gsh = 31 - __clz(gs);
+  const bool dual = R <= 16;
+  const uint32_t gpw = dual ? 2 : 1;
+  const uint32_t gs = hsub / (8 * gpw), gsh = 31 - __clz(gs);
   const uint32_t ng = (nloc + gs - 1) >> gsh;
-  if (warp < ng) {
-    uint32_t e = lane, term = lane < R ? 0 : 3, cnt = 0;  // entries >= max_len are unreachable
+  if (warp * gpw < ng) {
+    const uint32_t half = dual ? lane >> 4 : 0, el = dual ? lane & 15 : lane;
+    const uint32_t g = warp * gpw + half;
+    const bool gval = g < ng;
+    uint32_t e = el, term = (gval && el < R) ? 0 : 3, cnt = 0;  // entries >= max_len are unreachable
     for (uint32_t j = 0; j < gs; ++j) {
-      const uint32_t i = warp * gs + j;
-      if (i >= nloc) break;
-      Gs[i][lane] = pk(e, term, cnt);
-      // lanes that reached the same entry share one result
-      const uint32_t peers = __match_any_sync(0xffffffffu, term ? 0xFFFFFFFFu : e);
+      const uint32_t i = g * gs + j;
+      const bool live = gval && i < nloc;
+      if (live) Gs[i][el] = pk(e, term, cnt);
+      // lanes of a group that reached the same entry share one result
+      const uint32_t peers = __match_any_sync(0xffffffffu, (term || !live) ? 0xFFFFFFFFu : (half << 5) | e);
       const int leader = __ffs(peers) - 1;
       uint32_t f = 0;
-      if (!term && static_cast<int>(lane) == leader) {
+      if (live && !term && static_cast<int>(lane) == leader) {
         const uint64_t sbm = B0[i];
         const uint32_t sx = X0[i];
         if ((sbm >> e) & 1) f = pk(pk_off(sx), pk_term(sx), pk_cnt(sx) - popc_below(sbm, e));
@@ -1616,13 +1624,16 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
         else f = run(i, e, sbm, sx);
       }
       f = __shfl_sync(0xffffffffu, f, leader);
-      if (!term) {
+      if (live && !term) {
         term = pk_term(f);
         cnt += pk_cnt(f);
         e = pk_off(f);
       }
     }
-    G[warp][lane] = pk(e, term, cnt);
+    if (gval) {
+      G[g][el] = pk(e, term, cnt);
+      if (dual) G[g][el + 16] = pk(0, 3, 0);  // entries past 16 bits: unreachable
+    }
   }
   __syncthreads();
   DTS(blockIdx.x, 4);
