@@ -1342,7 +1342,7 @@ __device__ void vlz_end_check(const DecArgs& a, uint32_t c) {
 // Huffman blocks: 128 subsequences of 64 bits.
 // ===========================================================================
 constexpr uint32_t kHSub = 256;                        // subsequences per block (one per thread)
-constexpr uint32_t kMaxGroups = 16;                    // group walks per block (8 warps, up to two each)
+constexpr uint32_t kMaxGroups = 32;                    // group walks per block (8 warps, up to four each)
 constexpr uint32_t kHPre = 2;                          // words staged before the block (warm-up)
 // smem: LUT | two-codeword LUT | staged words | per-subsequence chain summaries | group states, later the symbols (u16)
 __host__ __device__ constexpr uint32_t huff_smem(uint32_t hsub) {
@@ -1596,15 +1596,15 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   DTS(blockIdx.x, 3);
   // ---- B: group walks (Gs[i][r] = state at the entry of subsequence i for group entry r);
   //      every warp walks hsub / 8 subsequences: one group on 32 lanes, or,
-  //      when codes are at most 16 bits, two groups of half the length on 16
-  //      lanes each
+  //      when codes are at most 16 (8) bits, two (four) groups of half
+  //      (a quarter of) the length on 16 (8) lanes each
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool dual = R <= 16;
-  const uint32_t gpw = dual ? 2 : 1;
+  const uint32_t lsh = R <= 8 ? 3 : (R <= 16 ? 4 : 5), lpg = 1u << lsh;  // lanes per group
+  const uint32_t gpw = 32 >> lsh;
   const uint32_t gs = hsub / (8 * gpw), gsh = 31 - __clz(gs);
   const uint32_t ng = (nloc + gs - 1) >> gsh;
   if (warp * gpw < ng) {
-    const uint32_t half = dual ? lane >> 4 : 0, el = dual ? lane & 15 : lane;
+    const uint32_t half = lane >> lsh, el = lane & (lpg - 1);
     const uint32_t g = warp * gpw + half;
     const bool gval = g < ng;
     uint32_t e = el, term = (gval && el < R) ? 0 : 3, cnt = 0;  // entries >= max_len are unreachable
@@ -1632,7 +1632,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     }
     if (gval) {
       G[g][el] = pk(e, term, cnt);
-      if (dual) G[g][el + 16] = pk(0, 3, 0);  // entries past 16 bits: unreachable
+      for (uint32_t x = el + lpg; x < 32; x += lpg) G[g][x] = pk(0, 3, 0);  // entries past R: unreachable
     }
   }
   __syncthreads();
