@@ -51,7 +51,7 @@ namespace embc_dev {
 __device__ unsigned long long g_dts[16384][12];  // role, t1..t11 (t7 = end)
 __device__ unsigned long long g_dcalls;
 __device__ unsigned long long g_kspan[4] = {~0ull, 0, 0, 0};  // k_dec_main: first start, last end, CTAs done, calls
-__device__ unsigned long long g_dloc[12];  // huffman blocks: local tables ok / not; ns in local build, in stage
+__device__ unsigned long long g_dloc[12];  // huffman blocks: local tables ok / not; ns in local build, in stage, ...
 __device__ __forceinline__ unsigned long long dtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1923,9 +1923,6 @@ __device__ void finish_chunk(const DecArgs& a, uint32_t c) {
     if (threadIdx.x != 0) return;
     const uint32_t nb = a.nchunks + a.nseg + a.nhblk + a.nraw;
     if (a.nchunks >= 26 && (++g_dcalls) % 8 == 7 && nb <= 16384) {
-      printf("D1 vlz roots: %llu chunks, mean %llu ns (rounds 2+: %llu ns, %llu rounds, %llu active after round 1)\n", g_dloc[7],
-             g_dloc[6] / max(1ull, g_dloc[7]), g_dloc[8] / max(1ull, g_dloc[7]), g_dloc[9] / max(1ull, g_dloc[7]),
-             g_dloc[10] / max(1ull, g_dloc[7]));
       printf("D1 huffman blocks: local tables %llu, waited %llu; mean ns local build %llu (warp %llu, lut %llu), stage %llu\n",
              g_dloc[0], g_dloc[1], g_dloc[2] / max(1ull, g_dloc[0] + g_dloc[1]), g_dloc[4] / max(1ull, g_dloc[0]),
              g_dloc[5] / max(1ull, g_dloc[0]), g_dloc[3] / max(1ull, g_dloc[0] + g_dloc[1]));
