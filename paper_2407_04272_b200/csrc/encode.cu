@@ -1011,7 +1011,8 @@ __device__ __forceinline__ void stats_tile(const StatsArgs& a, const uint32_t ti
       if (v) atomicAdd(&gh[b], v);
       if (keep) a.tile_hist[static_cast<uint64_t>(tid) * kTileHist + (b - b0)] = v;
     }
-    if (keep && threadIdx.x == 0) a.tile_hr[tid] = make_int2(s_min, static_cast<int>(b1 - b0 + 1));
+    if (a.tile_hr && threadIdx.x == 0)  // a span past kTileHist is not kept: (0, 0) = re-read
+      a.tile_hr[tid] = keep ? make_int2(s_min, static_cast<int>(b1 - b0 + 1)) : make_int2(0, 0);
   } else if (!MERGED && a.tile_hr && threadIdx.x == 0) {
     a.tile_hr[tid] = make_int2(0, 0);
   }

@@ -159,6 +159,23 @@ def test_two_pass_encode_large_call(ctx, oracle):
     assert [buf[o:o + ln] for o, ln in table] == want
 
 
+def test_two_pass_huffman_tile_spans(ctx, oracle):
+    """Two-pass calls price a huffman tile from its E1 histogram when the
+    tile's code span fits the kept window, else re-read it: a call of narrow
+    tiles followed by one of wide tiles (spans > 256 codes) on the same
+    context must not price the second from the first's histograms."""
+    rng = np.random.default_rng(4096)
+    for sigma in (0.02, 0.6, 0.02):
+        jobs, want = [], []
+        for t in range(3):
+            x = (rng.standard_normal((12000, 128)) * sigma).astype(np.float32)
+            jobs.append(K.EncodeJob(dev(x), 1e-3, 2))
+            want.append(oracle.encode_chunk(x.astype(np.float64).ravel(), 128, 1e-3, 2))
+        buf = K.pack_encode(jobs)
+        table = K.unpack_table(buf)
+        assert [buf[o:o + ln] for o, ln in table] == want, sigma
+
+
 @pytest.mark.parametrize("dim,n,classes", [(16, 8192, 1), (64, 8192, 3), (4, 30000, 2), (1, 20000, 5)])
 def test_long_reference_chains(ctx, oracle, dim, n, classes):
     # every row a repeat of a handful of rows: reference chains thousands of
