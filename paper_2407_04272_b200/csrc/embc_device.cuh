@@ -140,11 +140,6 @@ __device__ __forceinline__ double reconstruct(int32_t c, double w) {
   return __dmul_rn(static_cast<double>(c), w);
 }
 
-// Programmatic dependent launch (sm_90+): let the next kernel of the stream be
-// scheduled early / wait for the previous kernel's results.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
 // ---------------------------------------------------------------------------
 // zigzag (bytes.hpp:168-174) and unsigned LEB128 (bytes.hpp:61-67)
 // ---------------------------------------------------------------------------

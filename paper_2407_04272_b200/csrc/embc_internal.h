@@ -146,24 +146,6 @@ void tmark_end(embc_ctx* ctx, cudaStream_t stream);
   } while (0)
 cudaError_t ensure_hist(embc_ctx* ctx, size_t entries);
 
-// Programmatic dependent launch: the kernel may be scheduled while its
-// predecessor in the stream is still running; it calls pdl_wait() (griddepcontrol.wait)
-// before touching the predecessor's results.
-template <typename... KArgs, typename... Args>
-inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                              Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k, args...);
-}
 embc_status set_error(embc_ctx* ctx, embc_status st, int reason, uint32_t job, uint64_t index,
                       uint64_t a, uint64_t b, const std::string& msg);
 embc_status cuda_fail(embc_ctx* ctx, cudaError_t e, const char* where);

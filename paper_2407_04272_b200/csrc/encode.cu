@@ -228,26 +228,6 @@ struct BookArgs {
   uint32_t* flags;      // call flags
 };
 
-// Warp-level bitonic sort of p2 keys in shared memory.
-__device__ __forceinline__ void warp_bitonic(uint64_t* key, uint32_t p2) {
-  const uint32_t lane = threadIdx.x & 31;
-  for (uint32_t k = 2; k <= p2; k <<= 1) {
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = lane; i < p2; i += 32) {
-        const uint32_t ixj = i ^ j;
-        if (ixj > i) {
-          const uint64_t x = key[i], y = key[ixj];
-          if ((x > y) == ((i & k) == 0)) {
-            key[i] = y;
-            key[ixj] = x;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
-}
-
 // Codebook of an alphabet of <= 256 symbols by one warp: the same steps as the
 // block version below (huffman.hpp:49-120 lengths, :165-186 canonical codes).
 // Ascending sort of n <= 64 distinct keys in shared memory by one warp: each
