@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 import torch
 
+from paper_2407_04272_b200 import _lib
 from paper_2407_04272_b200 import codec as K
 
 pytestmark = pytest.mark.gpu
@@ -184,3 +185,23 @@ def test_long_reference_chains(ctx, oracle, dim, n, classes):
     rows = (rng.standard_normal((classes, dim)) * 0.05).astype(np.float32)
     x = rows[rng.integers(0, classes, n)]
     roundtrip(oracle, x.ravel(), dim, 0.01, 1)
+
+
+def test_single_launch_encode_failure_then_recovery(ctx, oracle):
+    """A quantization failure in one job of a Kaggle-shaped call (the
+    single-launch encoder, every tile resident) reports the first failing
+    job and value like encode_chunks, and the next call on the same context
+    is byte-exact again (no state left behind by the aborted launch)."""
+    rng = np.random.default_rng(26)
+    xs = [(rng.standard_normal((2048, 16)) * 0.05).astype(np.float32) for _ in range(26)]
+    codecs = [t % 3 for t in range(26)]
+    bad = [x.copy() for x in xs]
+    bad[17][5, 3] = np.nan
+    bad[21][0, 0] = np.inf
+    with pytest.raises(_lib.CodecValueError) as e:
+        K.pack_encode([K.EncodeJob(dev(x), 0.01, c) for x, c in zip(bad, codecs)])
+    assert e.value.job == 17 and e.value.index == 5 * 16 + 3
+    assert str(e.value) == "non-finite value at index 83"
+    want = [oracle.encode_chunk(x.astype(np.float64).ravel(), 16, 0.01, c) for x, c in zip(xs, codecs)]
+    buf = K.pack_encode([K.EncodeJob(dev(x), 0.01, c) for x, c in zip(xs, codecs)])
+    assert [buf[o:o + ln] for o, ln in K.unpack_table(buf)] == want
