@@ -205,3 +205,27 @@ def test_single_launch_encode_failure_then_recovery(ctx, oracle):
     want = [oracle.encode_chunk(x.astype(np.float64).ravel(), 16, 0.01, c) for x, c in zip(xs, codecs)]
     buf = K.pack_encode([K.EncodeJob(dev(x), 0.01, c) for x, c in zip(xs, codecs)])
     assert [buf[o:o + ln] for o, ln in K.unpack_table(buf)] == want
+
+
+@pytest.mark.parametrize("rows", [2048, 50000])  # single-launch encode / two-pass encode (> 1024 tiles)
+def test_output_capacity(ctx, oracle, rows):
+    """An output buffer smaller than the packed call reports ERR_CAPACITY,
+    writes nothing past the capacity, and leaves the context usable."""
+    rng = np.random.default_rng(rows)
+    xs = [(rng.standard_normal((rows, 16)) * 0.05).astype(np.float32) for _ in range(6)]
+    jobs = [K.EncodeJob(dev(x), 0.01, t % 3) for t, x in enumerate(xs)]
+    want = [oracle.encode_chunk(x.astype(np.float64).ravel(), 16, 0.01, t % 3) for t, x in enumerate(xs)]
+    need = 4 + 16 * len(jobs) + sum(len(w) for w in want)
+    cap = need // 2
+    arena = torch.full((cap + 4096,), 0xA5, dtype=torch.uint8, device=DEV)
+    cj = [j.to_c() for j in jobs]
+    ctx.encode_raw(cj, K.LAYOUT_PACKED, arena[:cap])
+    with pytest.raises(_lib.EmbcError) as e:
+        ctx.sync()
+    assert e.value.status == _lib.ERR_CAPACITY
+    assert bool((arena[cap:] == 0xA5).all())
+    out = torch.empty(need + 64, dtype=torch.uint8, device=DEV)
+    ctx.encode_raw(cj, K.LAYOUT_PACKED, out)
+    ctx.sync()
+    buf = bytes(out[:need].cpu().numpy().tobytes())
+    assert [buf[o:o + ln] for o, ln in K.unpack_table(buf)] == want
