@@ -268,6 +268,16 @@ class Ref:
             ("ref_estimate_speedup", dbl, [dbl, dbl, dbl, dbl]),
             ("ref_codec_timed", i32, [vp, vp, vp, vp, vp, vp, u32, C.c_uint, i32, C.POINTER(dbl), C.POINTER(dbl),
                                       C.POINTER(u64), C.c_char_p, sz]),
+            ("ref_load_preset", i32, [C.c_char_p, u32, C.POINTER(u32), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                      C.POINTER(i32), C.POINTER(dbl), C.POINTER(u64), C.POINTER(u32),
+                                      C.POINTER(u32), C.POINTER(u32), C.c_char_p, sz]),
+            ("ref_offline_analysis", i32, [vp, vp, vp, vp, vp, u32, dbl, dbl, dbl, dbl, dbl, dbl, u32, C.c_char_p,
+                                           C.c_char_p, sz]),
+            ("ref_read_profiles", i32, [C.c_char_p, u32, C.POINTER(u32), vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                        C.c_char_p, sz]),
+            ("ref_encode_pack", i32, [vp, vp, vp, vp, vp, vp, u32, u32, C.c_uint, pp, C.POINTER(u64), C.c_char_p,
+                                      sz]),
+            ("ref_format_double", None, [dbl, C.c_char_p, sz]),
             ("ref_simulate", i32, [u32, u32, u32, u64, i32, dbl, dbl, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp,
                                    u32, vp, vp, vp, vp, vp, vp, vp, C.POINTER(u64), C.c_char_p, sz]),
         ]:
@@ -429,3 +439,70 @@ class Ref:
         self._call(self.L.ref_codec_timed, _p(vals), _p(offs), _p(dims), _p(ns), _p(ebs), _p(cods), len(batches),
                    workers, reps, C.byref(cs), C.byref(ds), C.byref(pl))
         return cs.value, ds.value, pl.value
+
+    @staticmethod
+    def _jobs(batches):
+        vals = np.concatenate([np.ascontiguousarray(b, np.float64).ravel() for b in batches]) if batches else \
+            np.zeros(1, np.float64)
+        offs = np.cumsum([0] + [b.size for b in batches[:-1]]).astype(np.uint64)
+        dims = np.array([b.shape[1] for b in batches], np.uint32)
+        ns = np.array([b.shape[0] for b in batches], np.uint32)
+        return vals, offs, dims, ns
+
+    def encode_pack(self, batches, ebs, codecs, workers: int = 1, window: int = 255) -> bytes:
+        """pack(encode_chunks(jobs, workers)) (container.hpp:242-256, :304-311)."""
+        vals, offs, dims, ns = self._jobs(batches)
+        e = np.ascontiguousarray(ebs, np.float64)
+        c = np.ascontiguousarray(codecs, np.uint8)
+        p, ln = C.c_void_p(), C.c_uint64()
+        self._call(self.L.ref_encode_pack, _p(vals), _p(offs), _p(dims), _p(ns), _p(e), _p(c), len(batches), window,
+                   workers, C.byref(p), C.byref(ln))
+        return self._take(p, ln.value, np.uint8).tobytes()
+
+    def load_preset(self, path: str) -> dict:
+        """load_tables + load_policy (config.hpp:184-228) of a preset .cfg file."""
+        cap = 4096
+        arrs = {k: np.zeros(cap, t) for k, t in [("rows", np.uint32), ("dim", np.uint32), ("dist", np.int32),
+                                                  ("mu", np.float64), ("sigma", np.float64), ("lo", np.float64),
+                                                  ("hi", np.float64), ("zipf", np.float64), ("seed", np.uint64)]}
+        pol = np.zeros(5, np.float64)
+        cnt, fn, st, end, steps, batch, ranks = (C.c_uint32(), C.c_int(), C.c_double(), C.c_uint64(), C.c_uint32(),
+                                                 C.c_uint32(), C.c_uint32())
+        self._call(self.L.ref_load_preset, path.encode(), cap, C.byref(cnt), *[_p(arrs[k]) for k in
+                   ("rows", "dim", "dist", "mu", "sigma", "lo", "hi", "zipf", "seed")], _p(pol), C.byref(fn),
+                   C.byref(st), C.byref(end), C.byref(steps), C.byref(batch), C.byref(ranks))
+        n = cnt.value
+        tables = [[int(arrs["rows"][i]), int(arrs["dist"][i]), float(arrs["mu"][i]), float(arrs["sigma"][i]),
+                   float(arrs["lo"][i]), float(arrs["hi"][i]), float(arrs["zipf"][i])] for i in range(n)]
+        return {"tables": tables, "dims": [int(d) for d in arrs["dim"][:n]],
+                "policy": {"global_eb": pol[0], "alpha": pol[1], "beta": pol[2], "large_threshold": pol[3],
+                           "small_threshold": pol[4], "decay_fn": fn.value, "decay_start": st.value,
+                           "decay_end": end.value, "decay_steps": steps.value},
+                "batch": batch.value, "ranks": ranks.value}
+
+    def offline_analysis(self, samples, table_ids, path: str, global_eb=0.02, alpha=5 / 3, beta=3.0,
+                         l_thr=0.70, s_thr=0.95, bandwidth=1e-300, window: int = 255) -> None:
+        """offline_analysis (policy.hpp:278-302), written with write_profiles (config.hpp:247-271)."""
+        vals, offs, dims, ns = self._jobs(samples)
+        ids = np.ascontiguousarray(table_ids, np.int32)
+        self._call(self.L.ref_offline_analysis, _p(vals), _p(offs), _p(dims), _p(ns), _p(ids), len(samples),
+                   global_eb, alpha, beta, l_thr, s_thr, bandwidth, window, path.encode())
+
+    def read_profiles(self, path: str) -> dict:
+        """read_profiles (config.hpp:273-303) -> {table_id: {...}}."""
+        cap = 4096
+        tid = np.zeros(cap, np.int32)
+        no, nq = np.zeros(cap, np.uint64), np.zeros(cap, np.uint64)
+        surv, eb, rv, rh = (np.zeros(cap, np.float64) for _ in range(4))
+        cls, cod = np.zeros(cap, np.int32), np.zeros(cap, np.int32)
+        cnt = C.c_uint32()
+        self._call(self.L.ref_read_profiles, path.encode(), cap, C.byref(cnt), _p(tid), _p(no), _p(nq), _p(surv),
+                   _p(cls), _p(cod), _p(eb), _p(rv), _p(rh))
+        return {int(tid[i]): {"n_original": int(no[i]), "n_quantized": int(nq[i]), "survival": float(surv[i]),
+                              "cls": int(cls[i]), "codec": int(cod[i]), "eb": float(eb[i]),
+                              "ratio_vlz": float(rv[i]), "ratio_huffman": float(rh[i])} for i in range(cnt.value)}
+
+    def format_double(self, v: float) -> str:
+        buf = C.create_string_buffer(64)
+        self.L.ref_format_double(v, buf, 64)
+        return buf.value.decode()

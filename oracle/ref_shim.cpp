@@ -7,6 +7,7 @@
 // Status codes: 0 ok, 1 embc::ValueError, 2 embc::FormatError, 3 other embc::Error,
 // 4 a std::exception escaping the reference (e.g. vector::reserve on a corrupt count).
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <span>
@@ -375,6 +376,119 @@ int ref_simulate(uint32_t ranks, uint32_t batch, uint32_t iterations, uint64_t s
       out_digest[i] = rep.iterations[i].delivered_digest;
     }
     *report_digest = rep.deterministic_digest();
+  })
+}
+
+// ---- presets and profiles (config.hpp) ---------------------------------------
+// load_tables + load_policy of a reference preset file (config.hpp:184-228).
+int ref_load_preset(const char* path, uint32_t cap, uint32_t* count, uint32_t* rows, uint32_t* dim,
+                    int* dist, double* mu, double* sigma, double* lo, double* hi, double* zipf,
+                    uint64_t* seed, double* policy5, int* decay_fn, double* decay_start,
+                    uint64_t* decay_end, uint32_t* decay_steps, uint32_t* batch, uint32_t* ranks,
+                    char* err, size_t errcap) {
+  GUARD({
+    const embc::KeyValueConfig kv = embc::KeyValueConfig::parse_file(path);
+    const std::vector<embc::TableSpec> t = embc::load_tables(kv);
+    const embc::PolicyConfig p = embc::load_policy(kv);
+    *count = static_cast<uint32_t>(t.size());
+    for (size_t i = 0; i < t.size() && i < cap; ++i) {
+      rows[i] = t[i].rows;
+      dim[i] = t[i].dim;
+      dist[i] = t[i].dist == embc::ValueDist::gaussian ? 0 : 1;
+      mu[i] = t[i].mu;
+      sigma[i] = t[i].sigma;
+      lo[i] = t[i].lo;
+      hi[i] = t[i].hi;
+      zipf[i] = t[i].zipf_s;
+      seed[i] = t[i].seed;
+    }
+    policy5[0] = p.global_eb;
+    policy5[1] = p.alpha;
+    policy5[2] = p.beta;
+    policy5[3] = p.large_threshold;
+    policy5[4] = p.small_threshold;
+    *decay_fn = static_cast<int>(p.decay.function);
+    *decay_start = p.decay.start_scale;
+    *decay_end = p.decay.decay_end;
+    *decay_steps = p.decay.step_count;
+    *batch = static_cast<uint32_t>(kv.get_u64("batch", 0));
+    *ranks = static_cast<uint32_t>(kv.get_u64("ranks", 0));
+  })
+}
+
+// offline_analysis (policy.hpp:278-302) of per-table samples, persisted with
+// write_profiles (config.hpp:247-271).  Samples share one value array.
+int ref_offline_analysis(const double* values, const uint64_t* offs, const uint32_t* dims,
+                         const uint32_t* ns, const int32_t* table_ids, uint32_t nsamples,
+                         double global_eb, double alpha, double beta, double l_thr, double s_thr,
+                         double bandwidth, uint32_t window, const char* out_path, char* err,
+                         size_t errcap) {
+  GUARD({
+    std::vector<embc::EmbeddingBatch> samples(nsamples);
+    for (uint32_t j = 0; j < nsamples; ++j) {
+      samples[j].table_id = table_ids[j];
+      samples[j].dim = dims[j];
+      samples[j].values.assign(values + offs[j], values + offs[j] + static_cast<size_t>(dims[j]) * ns[j]);
+    }
+    embc::PolicyConfig p;
+    p.global_eb = global_eb;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.large_threshold = l_thr;
+    p.small_threshold = s_thr;
+    const auto profiles = embc::offline_analysis(samples, p, bandwidth, embc::VlzConfig{window});
+    embc::write_profiles(out_path, profiles);
+  })
+}
+
+// read_profiles (config.hpp:273-303) into arrays (ratios 0 when not measured).
+int ref_read_profiles(const char* path, uint32_t cap, uint32_t* count, int32_t* table_id,
+                      uint64_t* n_orig, uint64_t* n_quant, double* survival, int* cls, int* codec,
+                      double* eb, double* ratio_vlz, double* ratio_huf, char* err, size_t errcap) {
+  GUARD({
+    const auto profiles = embc::read_profiles(path);
+    *count = static_cast<uint32_t>(profiles.size());
+    uint32_t i = 0;
+    for (const auto& [id, p] : profiles) {
+      if (i >= cap) break;
+      table_id[i] = id;
+      n_orig[i] = p.n_original_patterns;
+      n_quant[i] = p.n_quantized_patterns;
+      survival[i] = p.survival_ratio;
+      cls[i] = static_cast<int>(p.cls);
+      codec[i] = static_cast<int>(p.codec);
+      eb[i] = p.eb;
+      ratio_vlz[i] = ratio_huf[i] = 0.0;
+      for (const auto& m : p.measured) (m.codec == embc::Codec::vlz ? ratio_vlz : ratio_huf)[i] = m.ratio;
+      ++i;
+    }
+  })
+}
+
+// detail::format_double (csv.hpp:31-37) into buf (NUL-terminated).
+void ref_format_double(double v, char* buf, size_t cap) {
+  const std::string s = embc::detail::format_double(v);
+  std::snprintf(buf, cap, "%s", s.c_str());
+}
+
+// pack(encode_chunks(jobs, workers)) bytes (container.hpp:242-256, :304-311).
+int ref_encode_pack(const double* values, const uint64_t* offs, const uint32_t* dims,
+                    const uint32_t* ns, const double* ebs, const uint8_t* codecs, uint32_t njobs,
+                    uint32_t window, unsigned workers, uint8_t** out, uint64_t* len, char* err,
+                    size_t errcap) {
+  GUARD({
+    std::vector<embc::EmbeddingBatch> batches(njobs);
+    for (uint32_t j = 0; j < njobs; ++j) {
+      batches[j].dim = dims[j];
+      batches[j].values.assign(values + offs[j], values + offs[j] + static_cast<size_t>(dims[j]) * ns[j]);
+    }
+    std::vector<embc::EncodeJob> jobs(njobs);
+    for (uint32_t j = 0; j < njobs; ++j)
+      jobs[j] = embc::EncodeJob{&batches[j], ebs[j], static_cast<embc::Codec>(codecs[j]),
+                                embc::VlzConfig{window}};
+    const embc::PackedSendBuffer buf = embc::pack(embc::encode_chunks(jobs, workers));
+    *out = dup(buf.bytes);
+    *len = buf.bytes.size();
   })
 }
 

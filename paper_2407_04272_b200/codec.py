@@ -189,9 +189,6 @@ def encode_chunks(jobs: Sequence[EncodeJob], layout: int = LAYOUT_CHUNKS, meta: 
     ctx.encode_raw(cj, layout, out, offs, lens, md, tot, stream=stream)
     ctx.sync(stream)
     total = int(tot.item())
-    if layout == LAYOUT_PACKED and not cj:
-        total = 4
-        out[:4] = 0
     return EncodeResult(out[:total], offs[:len(cj)], lens[:len(cj)], md[:len(cj)] if md is not None else None,
                         total)
 

@@ -1829,6 +1829,12 @@ namespace embc_host {
 
 using namespace embc_dev;
 
+// An encode call with no jobs: the packed layout's rank count (0) and the total.
+__global__ void k_empty_call(uint8_t* out, uint64_t* d_total, uint64_t total) {
+  if (threadIdx.x < total) out[threadIdx.x] = 0;
+  if (threadIdx.x == 0 && d_total) *d_total = total;
+}
+
 static inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Carve {
@@ -1922,7 +1928,20 @@ static embc_status encode_impl(embc_ctx* ctx, const embc_job* hj, uint32_t njobs
   //      reference as well: ErrorBound ctor at container.hpp:308, check_shape)
   ctx->job_eb.assign(njobs, 0.0);
   ctx->job_window.assign(njobs, 0);
-  if (njobs == 0) return EMBC_OK;
+  if (njobs == 0) {
+    // pack([]) is the 4-byte rank count 0 (container.hpp:242-256); the other
+    // layouts are empty.  Written on the stream like any other output.
+    const uint64_t total = layout == EMBC_LAYOUT_PACKED ? 4 : 0;
+    if (total && (cap < total || !d_out))
+      return set_error(ctx, EMBC_ERR_CAPACITY, EMBC_R_CAPACITY, 0, 0, total, cap,
+                       format_message(EMBC_R_CAPACITY, 0, total, cap, 0.0));
+    if (total || d_total) {
+      k_empty_call<<<1, 32, 0, stream>>>(total ? d_out : nullptr, d_total, total);
+      cudaError_t ce = cudaGetLastError();
+      if (ce != cudaSuccess) return cuda_fail(ctx, ce, "empty encode");
+    }
+    return EMBC_OK;
+  }
   std::vector<DJob> jobs(njobs);
   std::vector<DTile> tiles;
   uint64_t total_values = 0, total_rows = 0;

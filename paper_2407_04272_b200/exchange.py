@@ -55,7 +55,7 @@ class GpuCodec:
         cj = [j.to_c() for j in jobs]
         arr = (K._lib.Job * len(cj))(*cj)
         bound = int(self.ctx._L.embc_encode_bound(arr, len(cj), K.LAYOUT_CHUNKS))
-        dev = jobs[0].batch.device
+        dev = jobs[0].batch.device if jobs else torch.device("cuda", self.ctx.device)
         if out is None or out.numel() < bound:
             out = torch.empty(max(bound, 1), dtype=torch.uint8, device=dev)
         lens = torch.empty(len(cj), dtype=torch.int64, device=dev)
@@ -172,8 +172,7 @@ class CompressedAllToAll:
             meta_recv.copy_(meta)
         mark("metadata")
         # the host needs the byte counts: one device -> host read per exchange
-        host = torch.cat([lens.view(-1), meta_recv.view(-1).to(torch.int64)]).cpu() if len(jobs) else \
-            torch.zeros(0, dtype=torch.int64)
+        host = torch.cat([lens.view(-1).to(torch.int64), meta_recv.view(-1).to(torch.int64)]).cpu()
         lens_h = host[:len(jobs)].tolist()
         meta_h = bytes(host[len(jobs):].to(torch.uint8).numpy().tobytes())
         send_bytes = [0] * R

@@ -126,6 +126,125 @@ def eb_at(table_id: int, iteration: int, profiles: Dict[int, TableProfile], cfg:
     return eb
 
 
+# ---- profile persistence (config.hpp:247-303) --------------------------------
+
+_CLASS_IDS = {v: k for k, v in CLASS_NAMES.items()}
+
+
+def format_double(v: float) -> str:
+    """detail::format_double (csv.hpp:31-37): std::to_chars shortest round-trip
+    form -- the shorter of fixed and scientific notation, fixed on a tie."""
+    from decimal import Decimal
+    v = float(v)
+    if v != v:
+        return "nan" if repr(v)[0] != "-" else "-nan"
+    if v in (float("inf"), float("-inf")):
+        return "inf" if v > 0 else "-inf"
+    sign = "-" if repr(v).startswith("-") else ""
+    if v == 0.0:
+        return sign + "0"
+    t = Decimal(repr(abs(v))).normalize().as_tuple()
+    digits = "".join(map(str, t.digits))
+    point = len(digits) + t.exponent  # decimal point position after `point` digits
+    if point <= 0:
+        fixed = "0." + "0" * (-point) + digits
+    elif point >= len(digits):  # an integer: to_chars spells out its exact digits (same length)
+        fixed = str(int(abs(v)))
+    else:
+        fixed = digits[:point] + "." + digits[point:]
+    se = point - 1
+    sci = digits[0] + ("." + digits[1:] if len(digits) > 1 else "") + ("e-" if se < 0 else "e+") + f"{abs(se):02d}"
+    return sign + (fixed if len(fixed) <= len(sci) else sci)
+
+
+def write_profiles(path: str, profiles: Dict[int, TableProfile]) -> None:
+    """write_profiles (config.hpp:247-271): the reference's key-value profile
+    file, byte-identical for identical profiles."""
+    lines = [f"profiles.count = {len(profiles)}"]
+    for i, tid in enumerate(sorted(profiles)):
+        p = profiles[tid]
+        pre = f"profile.{i}."
+        lines += [f"{pre}table = {tid}", f"{pre}n_original = {p.n_original_patterns}",
+                  f"{pre}n_quantized = {p.n_quantized_patterns}", f"{pre}survival = {format_double(p.survival_ratio)}",
+                  f"{pre}homo = {format_double(p.homo_index)}", f"{pre}class = {CLASS_NAMES[p.cls]}",
+                  f"{pre}codec = {K.CODEC_NAMES[p.codec]}", f"{pre}eb = {format_double(p.eb)}"]
+        for m in p.measured:
+            mp = f"{pre}{K.CODEC_NAMES[m.codec]}."
+            lines += [f"{mp}ratio = {format_double(m.ratio)}", f"{mp}comp_bps = {format_double(m.comp_bps)}",
+                      f"{mp}decomp_bps = {format_double(m.decomp_bps)}"]
+    with open(path, "w") as f:
+        f.write("".join(line + "\n" for line in lines))
+
+
+def _parse_kv(path: str) -> Dict[str, str]:
+    """KeyValueConfig::parse_file (config.hpp:37-68)."""
+    try:
+        text = open(path).read()
+    except OSError:
+        raise _lib.CodecConfigError(f"cannot open config file '{path}'", status=_lib.ERR_CONFIG)
+    kv: Dict[str, str] = {}
+    for n, line in enumerate(text.split("\n"), 1):
+        t = line.strip(" \t\r")
+        if not t or t[0] == "#":
+            continue
+        if "=" not in t:
+            raise _lib.CodecConfigError(f"{path}:{n}: expected 'key = value'", status=_lib.ERR_CONFIG)
+        k, v = t.split("=", 1)
+        k, v = k.strip(" \t\r"), v.strip(" \t\r")
+        if not k:
+            raise _lib.CodecConfigError(f"{path}:{n}: empty key", status=_lib.ERR_CONFIG)
+        kv[k] = v
+    return kv
+
+
+def _kv_get(kv: Dict[str, str], key: str) -> str:
+    if key not in kv:
+        raise _lib.CodecConfigError(f"missing config key '{key}'", status=_lib.ERR_CONFIG)
+    return kv[key]
+
+
+def _kv_u64(kv, key) -> int:
+    v = _kv_get(kv, key)
+    if not v.isdigit():
+        raise _lib.CodecConfigError(f"key '{key}' expects a non-negative integer, got '{v}'", status=_lib.ERR_CONFIG)
+    return int(v)
+
+
+def _kv_f64(kv, key) -> float:
+    v = _kv_get(kv, key)
+    try:
+        if v.strip() != v or v.lower() in ("infinity", "-infinity") or "_" in v:
+            raise ValueError
+        return float(v)
+    except ValueError:
+        raise _lib.CodecConfigError(f"key '{key}' expects a number, got '{v}'", status=_lib.ERR_CONFIG)
+
+
+def read_profiles(path: str) -> Dict[int, TableProfile]:
+    """read_profiles (config.hpp:273-303)."""
+    kv = _parse_kv(path)
+    out: Dict[int, TableProfile] = {}
+    for i in range(_kv_u64(kv, "profiles.count")):
+        pre = f"profile.{i}."
+        tid, no, nq = _kv_u64(kv, pre + "table"), _kv_u64(kv, pre + "n_original"), _kv_u64(kv, pre + "n_quantized")
+        surv, homo = _kv_f64(kv, pre + "survival"), _kv_f64(kv, pre + "homo")
+        cls_name = _kv_get(kv, pre + "class")
+        if cls_name not in _CLASS_IDS:
+            raise _lib.CodecConfigError(f"unknown table class '{cls_name}'", status=_lib.ERR_CONFIG)
+        codec_name = _kv_get(kv, pre + "codec")
+        if codec_name not in K.CODEC_IDS:
+            raise _lib.CodecConfigError(f"unknown codec '{codec_name}'", status=_lib.ERR_CONFIG)
+        p = TableProfile(tid, no, nq, surv, homo, _CLASS_IDS[cls_name], K.CODEC_IDS[codec_name],
+                         _kv_f64(kv, pre + "eb"))
+        for c in (K.CODEC_VLZ, K.CODEC_HUFFMAN):
+            mp = f"{pre}{K.CODEC_NAMES[c]}."
+            if mp + "ratio" in kv:
+                p.measured.append(ThroughputSample(c, _kv_f64(kv, mp + "comp_bps"), _kv_f64(kv, mp + "decomp_bps"),
+                                                   _kv_f64(kv, mp + "ratio")))
+        out[p.table_id] = p
+    return out
+
+
 def _median_gpu_seconds(fn, runs: int = 5) -> float:
     """detail::median_seconds (policy.hpp:218-231) with CUDA events."""
     times = []

@@ -146,6 +146,34 @@ def _worker(rank, world, port, q, mode):
                     if ex1.stats.payload_bytes != exg.stats.payload_bytes:
                         res["ok"] = False
             q.put((rank, res))
+        elif mode == "few_tables":  # T < R: a rank that owns no table still receives
+            T, dim, B = 2, 4, 32
+            specs = W.preset_tables(W.KAGGLE_TABLES, T, dim)
+            tabs = {t: W.gen_table(specs[t]) for t in range(T)}
+            profiles = {t: P.TableProfile(t, codec=1 + t % 2, eb=0.02) for t in range(T)}
+            cfg = P.PolicyConfig(global_eb=0.02)
+            from oracle import Oracle
+            o = Oracle()
+            res = {"ok": True}
+            for G in (1, 2):
+                ex = X.CompressedAllToAll(T, dim, B, profiles, cfg, backend=OracleCodec(), device=torch.device("cpu"),
+                                          groups=G)
+                look = {t: torch.cat([torch.from_numpy(tabs[t][W.lookup_indices(specs[t], B,
+                                                                               W.lookup_stream(0, t, d, world))])
+                                      for d in range(world)]) for t in ex.owned(rank)}
+                out = ex.forward(0, look)
+                for t in range(T):
+                    x = tabs[t][W.lookup_indices(specs[t], B, W.lookup_stream(0, t, rank, world))]
+                    want = o.decode_chunk(o.encode_chunk(x.astype(np.float64).ravel(), dim, 0.02, profiles[t].codec))
+                    if not np.array_equal(out[t].numpy(), want.astype(np.float32)):
+                        res["ok"] = False
+                if not ex.owned(rank) and ex.stats.payload_bytes != 0:
+                    res["ok"] = False
+                grads = {t: torch.full((B, dim), 0.01 * (t + 1), dtype=torch.float32) for t in range(T)}
+                gout = ex.backward(0, grads)
+                if sorted(gout) != ex.owned(rank):
+                    res["ok"] = False
+            q.put((rank, res))
         else:  # simulator parity: one table per rank, reference seeding
             from oracle import Ref
             ref_specs = [(64, 0, 0.0, 0.05, 0, 1, 1.1), (256, 1, 0.0, 0.1, -0.2, 0.3, 0.6)]
@@ -181,11 +209,11 @@ def _worker(rank, world, port, q, mode):
         dist.destroy_process_group()
 
 
-def _run(mode):
+def _run(mode, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, mode)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode)) for r in range(world)]
     for p in procs:
         p.start()
     out = dict(q.get(timeout=240) for _ in procs)
@@ -207,6 +235,14 @@ def test_exchange_pipelined_groups_gloo():
     and backward."""
     out = _run("pipelined")
     for r in (0, 1):
+        assert out[r]["ok"], r
+
+
+def test_exchange_rank_without_tables_gloo():
+    """T < R (3 ranks, 2 tables): the rank that owns no table sends nothing and
+    still decodes what its peers send, with one exchange or table groups."""
+    out = _run("few_tables", world=3)
+    for r in range(3):
         assert out[r]["ok"], r
 
 
