@@ -6,11 +6,11 @@ the unmodified reference headers compiled by oracle/Makefile):
     python tests/golden/make_profiles.py
 
 Writes
-  * tests/golden/presets.json -- the per-table distributions of the reference's
+  * configs/presets.json -- the per-table distributions of the reference's
     presets (proj/configs/kaggle_like.cfg, terabyte_like.cfg) as parsed by the
     reference's own load_tables / load_policy (config.hpp:184-228), plus the
     BASELINE.json shapes each workload uses;
-  * tests/golden/profiles_<workload>.cfg -- the reference's offline_analysis
+  * configs/profiles_<workload>.cfg -- the reference's offline_analysis
     (policy.hpp:278-302) of iteration-0 samples, written by the reference's
     write_profiles (config.hpp:247-271), for the Kaggle-shaped (kg),
     Terabyte-shaped (tb) and scaled (sc) workloads.
@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 from oracle import Ref  # noqa: E402
 
 CFG = "/root/reference/proj/configs"
+OUTDIR = os.path.join(ROOT, "configs")
 
 # workload -> (preset file, tables, dim, sample batch); BASELINE.json configs[1], [2], [4]
 WORKLOADS = {
@@ -71,14 +72,14 @@ def main() -> None:
         pol = p["policy"]
         specs = [p["tables"][t % len(p["tables"])] for t in range(T)]
         samples = [sample(r, specs[t], t, dim, batch, 0) for t in range(T)]
-        path = os.path.join(HERE, f"profiles_{wl}.cfg")
+        path = os.path.join(OUTDIR, f"profiles_{wl}.cfg")
         r.offline_analysis(samples, list(range(T)), path, pol["global_eb"], pol["alpha"], pol["beta"],
                            pol["large_threshold"], pol["small_threshold"], bandwidth=1e-300)
         prof = r.read_profiles(path)
         out["workloads"][wl] = {"preset": pre, "tables": T, "dim": dim, "sample_batch": batch, "sample_stream": 0,
                                 "global_eb": float(pol["global_eb"]), "profiles": os.path.basename(path)}
         print(wl, "codecs", [prof[t]["codec"] for t in range(T)], "ebs", sorted({prof[t]["eb"] for t in range(T)}))
-    with open(os.path.join(HERE, "presets.json"), "w") as f:
+    with open(os.path.join(OUTDIR, "presets.json"), "w") as f:
         json.dump(out, f, indent=1)
 
 

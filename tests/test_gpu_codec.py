@@ -331,22 +331,28 @@ def test_determinism_and_parallel_encode(ctx):
     assert a == b
 
 
-def test_large_tb_chunk_roundtrip(ctx):
-    """Terabyte-shaped rank slice (8 tables x 8192 x 64): decode(encode(x)) is
-    within eb, encode is deterministic, and the GPU CR equals the oracle's on a
-    sampled chunk."""
+def test_large_tb_chunk_roundtrip(ctx, ref):
+    """Terabyte-shaped rank slice (8 tables x 8192 x 64, one packed call through
+    the two-pass encoder): bytes == the reference's pack(encode_chunks(jobs)),
+    deterministic, decoded bits == the reference's decode_chunk, within eb."""
     tables = W.preset_tables(W.TERABYTE_TABLES, 8, 64)
-    jobs = []
+    jobs, xs = [], []
     for t, spec in enumerate(tables):
-        tab = W.Table(spec, DEV)
-        jobs.append(K.EncodeJob(tab.lookup_batch(8192, stream=W.lookup_stream(0, t, 1, 8)), 0.03, 1 + t % 2))
+        x = W.gen_table(spec)[W.lookup_indices(spec, 8192, W.lookup_stream(0, t, 1, 8))]
+        xs.append(x.astype(np.float64))
+        jobs.append(K.EncodeJob(dev(x), 0.03, 1 + t % 2))
     r1 = K.encode_chunks(jobs, K.LAYOUT_PACKED)
     r2 = K.encode_chunks(jobs, K.LAYOUT_PACKED)
     assert torch.equal(r1.buffer, r2.buffer)
-    outs = K.decode_packed(bytes(r1.buffer.cpu().numpy().tobytes()), K.OUT_F64)
+    got = bytes(r1.buffer.cpu().numpy().tobytes())
+    want = ref.encode_pack(xs, [0.03] * 8, [1 + t % 2 for t in range(8)], workers=8)
+    assert got == want
+    outs = K.decode_packed(got, K.OUT_F64)
     assert K.decode_fallbacks() == 0
-    for j, o in zip(jobs, outs):
-        assert (o - j.batch.double()).abs().max().item() <= 0.03
+    for x, o, c in zip(xs, outs, ref.unpack(want)):
+        d = o.cpu().numpy()
+        assert np.array_equal(d.view(np.uint64), ref.decode_chunk(c).view(np.uint64))
+        assert np.abs(d - x).max() <= 0.03
 
 
 def test_long_huffman_codes_parallel_path(ctx, oracle):

@@ -229,3 +229,18 @@ def test_output_capacity(ctx, oracle, rows):
     ctx.sync()
     buf = bytes(out[:need].cpu().numpy().tobytes())
     assert [buf[o:o + ln] for o, ln in K.unpack_table(buf)] == want
+
+
+def test_empty_job_list(ctx, ref):
+    """encode_chunks([]) + pack: the 4-byte rank count, written by the library
+    (d_total included); the chunk and payload layouts are empty."""
+    r = K.encode_chunks([], K.LAYOUT_PACKED)
+    assert r.total == 4 and bytes(r.buffer.cpu().numpy().tobytes()) == ref.pack([])
+    assert K.encode_chunks([], K.LAYOUT_CHUNKS).total == 0
+    out = torch.full((8,), 0xAB, dtype=torch.uint8, device=DEV)
+    tot = torch.full((1,), -1, dtype=torch.int64, device=DEV)
+    ctx.encode_raw([], K.LAYOUT_PACKED, out, total=tot)
+    ctx.sync()
+    assert tot.item() == 4 and out.cpu().tolist() == [0, 0, 0, 0] + [0xAB] * 4
+    with pytest.raises(_lib.EmbcError):
+        ctx.encode_raw([], K.LAYOUT_PACKED, out[:2], total=tot)

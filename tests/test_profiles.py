@@ -2,7 +2,7 @@
 
 * format_double / write_profiles / read_profiles (config.hpp:247-303,
   csv.hpp:31-37) are byte-identical to the reference's;
-* the committed presets (tests/golden/presets.json) and profile files
+* the committed presets (configs/presets.json) and profile files
   (profiles_{kg,tb,sc}.cfg, written by the reference's offline_analysis via
   tests/golden/make_profiles.py) agree with workload.py's preset tables.
 """
@@ -16,7 +16,7 @@ import pytest
 from paper_2407_04272_b200 import policy as P
 from paper_2407_04272_b200 import workload as W
 
-GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+GOLD = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "configs")
 
 
 def test_format_double_matches_reference(ref):
