@@ -438,3 +438,24 @@ class CompressedAllToAll:
                 out[t] = recv[off:off + B * D].view(B, D)
                 off += B * D
         return out
+
+    def uncompressed_backward(self, grads: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
+        """C3 baseline of the backward direction: every table's [B, dim]
+        gradient slice to its owner as raw fp32 all_to_all_single."""
+        R, B, D = self.R, self.B, self.dim
+        own = self.owned(self.rank)
+        parts = [grads[t] for d in range(R) for t in self.owned(d)]
+        send = torch.cat(parts) if parts else torch.zeros((0, D), device=self.device)
+        send_counts = [len(self.owned(d)) * B * D for d in range(R)]
+        recv = torch.empty(len(own) * R * B * D, dtype=torch.float32, device=self.device)
+        if R > 1:
+            dist.all_to_all_single(recv, send.reshape(-1), [len(own) * B * D] * R, send_counts, group=self.group)
+        else:
+            recv.copy_(send.reshape(-1))
+        out = {t: torch.empty((R * B, D), dtype=torch.float32, device=self.device) for t in own}
+        off = 0
+        for s in range(R):
+            for t in own:
+                out[t][s * B:(s + 1) * B] = recv[off:off + B * D].view(B, D)
+                off += B * D
+        return out
