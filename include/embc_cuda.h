@@ -45,7 +45,8 @@ typedef enum {
   EMBC_ERR_CUDA = 4,        /* CUDA runtime failure */
   EMBC_ERR_CAPACITY = 5,    /* caller buffer too small */
   EMBC_ERR_ARGUMENT = 6,    /* null pointer / bad enum at the ABI */
-  EMBC_ERR_UNSUPPORTED = 7  /* input outside the GPU path's supported envelope */
+  EMBC_ERR_UNSUPPORTED = 7, /* input outside the GPU path's supported envelope */
+  EMBC_ERR_NCCL = 8         /* NCCL failure in the exchange */
 } embc_status;
 
 /* Codec tags == embc::Codec (container.hpp:32-36). */
@@ -233,6 +234,78 @@ embc_status embc_match_stats(embc_ctx* ctx, const int32_t* d_codes, uint32_t dim
 embc_status embc_pattern_counts(embc_ctx* ctx, const float* d_x, uint32_t dim, uint32_t rows,
                                 double eb, uint64_t* h_original, uint64_t* h_quantized,
                                 void* stream);
+
+/* ---- compressed embedding all-to-all over NCCL ---------------------------
+ *
+ * Replaces the reference's in-process exchange, Simulator::rank_body stages
+ * 1-4 (commsim.hpp:286-435), with a real one between the GPUs of a node: one
+ * process per GPU, one exchange object per process.  Table t is owned by rank
+ * t mod R.
+ *   forward : the owner's [R*B, dim] lookup output of table t is cut into R
+ *             [B, dim] chunks, chunk d goes to rank d;
+ *   backward: every rank's [B, dim] gradient slice of table t goes to its
+ *             owner, which receives [R*B, dim] (rows s*B.. from rank s).
+ * Each direction: compress the rank's (destination, table) chunks (one
+ * embc_encode per table group), exchange the 25-byte ChunkMetadata records
+ * (container.hpp:186-221; commsim.hpp:321-330), exchange the payloads with
+ * grouped ncclSend/ncclRecv, decode every received chunk straight into the
+ * caller's tensors on a decode stream.  With groups > 1 the owned tables are
+ * cut into groups so compression, transfer and decompression of successive
+ * groups overlap.  The call returns when the outputs are complete on `stream`
+ * (one host wait per group for the metadata: NCCL takes host byte counts).
+ * Per-iteration bounds/codecs come from the host controller (eb_at,
+ * policy.hpp:336-342). */
+typedef struct embc_exchange embc_exchange;
+
+typedef struct {
+  uint64_t uncompressed_bytes; /* fp32 bytes of chunks sent to other ranks (commsim.hpp:351-353) */
+  uint64_t payload_bytes;      /* serialized chunk bytes sent to other ranks (commsim.hpp:326-328) */
+  uint64_t metadata_bytes;     /* 25 B per chunk sent to another rank */
+  uint64_t sent_values;        /* values compressed (all chunks, own rank included) */
+  uint64_t sent_bytes;         /* serialized bytes of all compressed chunks */
+  uint64_t recv_values;        /* values decoded */
+  uint64_t recv_bytes;         /* serialized bytes of all decoded chunks */
+} embc_exchange_stats;
+
+/* ncclGetUniqueId(): rank 0 creates it and shares it with the other ranks. */
+embc_status embc_exchange_unique_id(uint8_t out[128]);
+/* One exchange per (process, GPU): an NCCL communicator of `nranks` ranks,
+ * codec contexts for compression and decompression, and its streams. */
+embc_status embc_exchange_create(int device, int rank, int nranks, const uint8_t id[128],
+                                 uint32_t groups, embc_exchange** out);
+void embc_exchange_destroy(embc_exchange* ex);
+embc_status embc_exchange_get_error(const embc_exchange* ex, embc_error* out);
+
+/* Forward: d_lookups[t] ([R*batch, dim] fp32) for the tables this rank owns
+ * (others ignored), ebs[t] / codecs[t] for every table; d_outs[t] ([batch,
+ * dim] fp32) for every table receive this rank's slice. */
+embc_status embc_exchange_fwd(embc_exchange* ex, uint32_t ntables, uint32_t dim, uint32_t batch,
+                              const float* const* d_lookups, const double* ebs,
+                              const uint8_t* codecs, uint32_t window, float* const* d_outs,
+                              embc_exchange_stats* stats, void* stream);
+/* Backward: d_grads[t] ([batch, dim]) for every table; d_outs[t] ([R*batch,
+ * dim]) for the tables this rank owns. */
+embc_status embc_exchange_bwd(embc_exchange* ex, uint32_t ntables, uint32_t dim, uint32_t batch,
+                              const float* const* d_grads, const double* ebs,
+                              const uint8_t* codecs, uint32_t window, float* const* d_outs,
+                              embc_exchange_stats* stats, void* stream);
+/* The uncompressed baseline: the same tensors as raw fp32 grouped
+ * ncclSend/ncclRecv (commsim.hpp:331-347, :380-397). */
+embc_status embc_exchange_baseline_fwd(embc_exchange* ex, uint32_t ntables, uint32_t dim,
+                                       uint32_t batch, const float* const* d_lookups,
+                                       float* const* d_outs, void* stream);
+embc_status embc_exchange_baseline_bwd(embc_exchange* ex, uint32_t ntables, uint32_t dim,
+                                       uint32_t batch, const float* const* d_grads,
+                                       float* const* d_outs, void* stream);
+
+/* ---- packed send buffer (container.hpp:258-292) --------------------------- */
+
+/* unpack()'s validation of a PackedSendBuffer (host bytes): offsets start at
+ * 4 + 16R and are contiguous, no entry runs past the end, no trailing bytes.
+ * Writes up to `cap` (offset, length) pairs and the entry count.  The chunk
+ * bodies are parsed by embc_decode on the device. */
+embc_status embc_unpack(const uint8_t* h_buf, uint64_t len, uint64_t* h_offsets,
+                        uint64_t* h_lengths, uint32_t cap, uint32_t* h_count, embc_error* err);
 
 /* ---- host controller (policy.hpp), identical arithmetic ---------------- */
 

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "libembc_cuda.so")
 CSRC = os.path.join(HERE, "csrc")
 
 # ---- status / reason codes (embc_cuda.h) ----------------------------------
-OK, ERR_VALUE, ERR_FORMAT, ERR_CONFIG, ERR_CUDA, ERR_CAPACITY, ERR_ARGUMENT, ERR_UNSUPPORTED = range(8)
+OK, ERR_VALUE, ERR_FORMAT, ERR_CONFIG, ERR_CUDA, ERR_CAPACITY, ERR_ARGUMENT, ERR_UNSUPPORTED, ERR_NCCL = range(9)
 CODEC_RAW, CODEC_VLZ, CODEC_HUFFMAN = 0, 1, 2
 LAYOUT_CHUNKS, LAYOUT_PACKED, LAYOUT_PAYLOAD = 0, 1, 2
 SRC_F32, SRC_I32 = 0, 1
@@ -76,6 +76,12 @@ class Job(C.Structure):
                 ("pad", C.c_uint8 * 2)]
 
 
+class ExchangeStats(C.Structure):
+    _fields_ = [("uncompressed_bytes", C.c_uint64), ("payload_bytes", C.c_uint64), ("metadata_bytes", C.c_uint64),
+                ("sent_values", C.c_uint64), ("sent_bytes", C.c_uint64), ("recv_values", C.c_uint64),
+                ("recv_bytes", C.c_uint64)]
+
+
 class ChunkRef(C.Structure):
     _fields_ = [("offset", C.c_uint64), ("length", C.c_uint64), ("out", C.c_void_p),
                 ("dim", C.c_uint32), ("count", C.c_uint32), ("eb", C.c_double), ("codec", C.c_uint8),
@@ -90,6 +96,9 @@ EXPORTS = [
     "embc_classify_table", "embc_estimate_speedup", "embc_gen_table", "embc_gen_lookup_indices",
     "embc_mix_seed", "embc_gather_rows", "embc_reserve_capture", "embc_capture_reset",
     "embc_timing_enable", "embc_timing_collect", "embc_decode_fallbacks",
+    "embc_exchange_unique_id", "embc_exchange_create", "embc_exchange_destroy", "embc_exchange_get_error",
+    "embc_exchange_fwd", "embc_exchange_bwd", "embc_exchange_baseline_fwd", "embc_exchange_baseline_bwd",
+    "embc_unpack",
 ]
 
 _lock = threading.Lock()
@@ -137,6 +146,15 @@ def lib() -> C.CDLL:
                 "embc_timing_enable": (i32, [vp, i32]),
                 "embc_timing_collect": (i32, [vp, vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_float), i32]),
                 "embc_decode_fallbacks": (i32, [vp, C.POINTER(u32)]),
+                "embc_exchange_unique_id": (i32, [vp]),
+                "embc_exchange_create": (i32, [i32, i32, i32, vp, u32, C.POINTER(vp)]),
+                "embc_exchange_destroy": (None, [vp]),
+                "embc_exchange_get_error": (i32, [vp, C.POINTER(EmbcErrorRec)]),
+                "embc_exchange_fwd": (i32, [vp, u32, u32, u32, vp, vp, vp, u32, vp, C.POINTER(ExchangeStats), vp]),
+                "embc_exchange_bwd": (i32, [vp, u32, u32, u32, vp, vp, vp, u32, vp, C.POINTER(ExchangeStats), vp]),
+                "embc_exchange_baseline_fwd": (i32, [vp, u32, u32, u32, vp, vp, vp]),
+                "embc_exchange_baseline_bwd": (i32, [vp, u32, u32, u32, vp, vp, vp]),
+                "embc_unpack": (i32, [vp, u64, vp, vp, u32, C.POINTER(u32), C.POINTER(EmbcErrorRec)]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)

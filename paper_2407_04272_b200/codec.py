@@ -336,40 +336,17 @@ def pattern_counts(x: torch.Tensor, eb: float, ctx: Optional[Context] = None):
 
 
 def unpack_table(buf: bytes):
-    """unpack() offset-table validation (container.hpp:258-284) -> [(offset, length)].
-    Host-side byte parsing of the 4+16R-byte table; chunk bodies decode on the GPU."""
-    if len(buf) < 4:
-        raise _lib.CodecFormatError(f"truncated input: need 4 bytes at offset 0, have {len(buf)}",
-                                    status=_lib.ERR_FORMAT, reason=5)
-    (count,) = struct.unpack_from("<I", buf, 0)
-    table = []
-    pos = 4
-    for i in range(count):
-        if len(buf) - pos < 8:
-            raise _lib.CodecFormatError(f"truncated input: need 8 bytes at offset {pos}, have {len(buf) - pos}",
-                                        status=_lib.ERR_FORMAT, reason=5)
-        (o,) = struct.unpack_from("<Q", buf, pos)
-        pos += 8
-        if len(buf) - pos < 8:
-            raise _lib.CodecFormatError(f"truncated input: need 8 bytes at offset {pos}, have {len(buf) - pos}",
-                                        status=_lib.ERR_FORMAT, reason=5)
-        (ln,) = struct.unpack_from("<Q", buf, pos)
-        pos += 8
-        table.append((o, ln))
-    expected = 4 + 16 * count
-    for i, (o, ln) in enumerate(table):
-        if o != expected:
-            raise _lib.CodecFormatError(
-                f"send buffer offset {o} for entry {i} overlaps or skips bytes (expected {expected})",
-                status=_lib.ERR_FORMAT, reason=28)
-        if o + ln > len(buf):
-            raise _lib.CodecFormatError(f"send buffer entry {i} runs past the end", status=_lib.ERR_FORMAT,
-                                        reason=29)
-        expected = o + ln
-    if expected != len(buf):
-        raise _lib.CodecFormatError(f"send buffer has {len(buf) - expected} unclaimed trailing bytes",
-                                    status=_lib.ERR_FORMAT, reason=30)
-    return table
+    """unpack()'s offset-table validation (container.hpp:258-284) through the C
+    ABI (embc_unpack) -> [(offset, length)]; chunk bodies decode on the GPU."""
+    L = _lib.lib()
+    raw = (C.c_uint8 * max(len(buf), 1)).from_buffer_copy(bytes(buf) or b"\0")
+    cap = len(buf) // 16 + 1
+    offs, lens = (C.c_uint64 * cap)(), (C.c_uint64 * cap)()
+    n, err = C.c_uint32(), _lib.EmbcErrorRec()
+    st = L.embc_unpack(raw, len(buf), offs, lens, cap, C.byref(n), C.byref(err))
+    if st != _lib.OK:
+        _lib.raise_for(st, err.message.decode(errors="replace"), err.reason, err.job, err.index)
+    return [(offs[i], lens[i]) for i in range(n.value)]
 
 
 def decode_packed(buf: bytes, out_kind: int = OUT_F32, ctx: Optional[Context] = None):

@@ -82,11 +82,16 @@ class GpuCodec:
 @dataclass
 class ExchangeStats:
     """Per-rank accounting with the reference's definitions (commsim.hpp:68-83,
-    :322-353): bytes sent to other ranks only."""
+    :322-353): bytes sent to other ranks only; plus the codec's totals (own
+    rank included) for throughput accounting."""
     uncompressed_bytes: int = 0
     payload_bytes: int = 0
     metadata_bytes: int = 0
     times_ms: Dict[str, float] = field(default_factory=dict)
+    sent_values: int = 0
+    sent_bytes: int = 0
+    recv_values: int = 0
+    recv_bytes: int = 0
 
     @property
     def wire_bytes(self) -> int:
@@ -458,4 +463,124 @@ class CompressedAllToAll:
             for t in own:
                 out[t][s * B:(s + 1) * B] = recv[off:off + B * D].view(B, D)
                 off += B * D
+        return out
+
+
+class NcclExchange:
+    """The product exchange on GPUs: embc_exchange_* (exchange.cpp, C++ over
+    NCCL grouped send/recv, codec through the C ABI on encode / decode streams),
+    with the same interface and semantics as CompressedAllToAll.  One instance
+    per process; its NCCL communicator spans the ranks of `group` (the unique id
+    travels over torch.distributed)."""
+
+    def __init__(self, ntables: int, dim: int, batch: int, profiles: Dict[int, P.TableProfile],
+                 cfg: P.PolicyConfig, group=None, device=None, window: int = 255,
+                 grad_profiles: Optional[Dict[int, P.TableProfile]] = None,
+                 grad_cfg: Optional[P.PolicyConfig] = None, groups: int = 1):
+        import ctypes as C
+        from . import _lib
+        self._C, self._lib = C, _lib
+        self.L = _lib.lib()
+        self.group = group
+        self.R = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.T, self.dim, self.B = ntables, dim, batch
+        self.profiles, self.cfg = profiles, cfg
+        self.grad_profiles = grad_profiles if grad_profiles is not None else profiles
+        self.grad_cfg = grad_cfg if grad_cfg is not None else cfg
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.window = window
+        self.stats = ExchangeStats()
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            st = self.L.embc_exchange_unique_id(uid)
+            if st != _lib.OK:
+                raise _lib.EmbcError(f"embc_exchange_unique_id failed with status {st}", status=st)
+        if self.R > 1:
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            C.memmove(uid, box[0], 128)
+        h = C.c_void_p()
+        st = self.L.embc_exchange_create(self.device.index or 0, self.rank, self.R, uid, max(1, groups), C.byref(h))
+        if st != _lib.OK:
+            raise _lib.EmbcError(f"embc_exchange_create failed with status {st}", status=st)
+        self.handle = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.L.embc_exchange_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    def owner(self, t: int) -> int:
+        return t % self.R
+
+    def owned(self, r: int) -> List[int]:
+        return [t for t in range(self.T) if t % self.R == r]
+
+    def _check(self, st: int) -> None:
+        if st == self._lib.OK:
+            return
+        rec = self._lib.EmbcErrorRec()
+        self.L.embc_exchange_get_error(self.handle, self._C.byref(rec))
+        self._lib.raise_for(st, rec.message.decode(errors="replace"), rec.reason, rec.job, rec.index)
+
+    def _ptrs(self, tensors: Dict[int, torch.Tensor]):
+        C = self._C
+        arr = (C.c_void_p * self.T)()
+        for t, v in tensors.items():
+            if not (v.is_cuda and v.dtype == torch.float32 and v.is_contiguous()):
+                raise ValueError("exchange tensors must be contiguous float32 CUDA tensors")
+            arr[t] = v.data_ptr()
+        return arr
+
+    def _policy(self, iteration: int, profiles, cfg):
+        C = self._C
+        ebs = (C.c_double * self.T)(*[P.eb_at(t, iteration, profiles, cfg) for t in range(self.T)])
+        codecs = (C.c_uint8 * self.T)(*[profiles[t].codec if t in profiles else K.CODEC_RAW for t in range(self.T)])
+        return ebs, codecs
+
+    def _stats(self, s) -> ExchangeStats:
+        return ExchangeStats(s.uncompressed_bytes, s.payload_bytes, s.metadata_bytes, {}, s.sent_values, s.sent_bytes,
+                             s.recv_values, s.recv_bytes)
+
+    def forward(self, iteration: int, lookups: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
+        """lookups[t] for owned t: [R*B, dim].  Returns {t: [B, dim]} for every table."""
+        out = {t: torch.empty((self.B, self.dim), dtype=torch.float32, device=self.device) for t in range(self.T)}
+        ebs, codecs = self._policy(iteration, self.profiles, self.cfg)
+        st = self._lib.ExchangeStats()
+        self._check(self.L.embc_exchange_fwd(self.handle, self.T, self.dim, self.B, self._ptrs(lookups), ebs, codecs,
+                                             self.window, self._ptrs(out), self._C.byref(st),
+                                             torch.cuda.current_stream(self.device).cuda_stream))
+        self.stats = self._stats(st)
+        return out
+
+    def backward(self, iteration: int, grads: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
+        """grads[t] for every table: [B, dim].  Returns {t: [R*B, dim]} for owned tables."""
+        own = self.owned(self.rank)
+        out = {t: torch.empty((self.R * self.B, self.dim), dtype=torch.float32, device=self.device) for t in own}
+        ebs, codecs = self._policy(iteration, self.grad_profiles, self.grad_cfg)
+        st = self._lib.ExchangeStats()
+        self._check(self.L.embc_exchange_bwd(self.handle, self.T, self.dim, self.B, self._ptrs(grads), ebs, codecs,
+                                             self.window, self._ptrs(out), self._C.byref(st),
+                                             torch.cuda.current_stream(self.device).cuda_stream))
+        self.stats = self._stats(st)
+        return out
+
+    def uncompressed(self, lookups: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
+        out = {t: torch.empty((self.B, self.dim), dtype=torch.float32, device=self.device) for t in range(self.T)}
+        self._check(self.L.embc_exchange_baseline_fwd(self.handle, self.T, self.dim, self.B, self._ptrs(lookups),
+                                                      self._ptrs(out),
+                                                      torch.cuda.current_stream(self.device).cuda_stream))
+        return out
+
+    def uncompressed_backward(self, grads: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
+        own = self.owned(self.rank)
+        out = {t: torch.empty((self.R * self.B, self.dim), dtype=torch.float32, device=self.device) for t in own}
+        self._check(self.L.embc_exchange_baseline_bwd(self.handle, self.T, self.dim, self.B, self._ptrs(grads),
+                                                      self._ptrs(out),
+                                                      torch.cuda.current_stream(self.device).cuda_stream))
         return out

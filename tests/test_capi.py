@@ -6,6 +6,7 @@ import os
 import re
 
 import numpy as np
+import pytest
 
 from paper_2407_04272_b200 import _lib
 from paper_2407_04272_b200 import workload as W
@@ -71,3 +72,29 @@ def test_workload_golden_inputs(golden):
         spec = W.TableSpec(w["rows"], w["dim"], w["dist"], 0.0, w["sigma"], w["lo"], w["hi"], w["zipf"], w["seed"])
         x = W.gen_table(spec)[W.lookup_indices(spec, w["batch"], w["stream"])]
         assert hashlib.sha256(x.tobytes()).hexdigest() == w["x_sha"], w["name"]
+
+
+def test_unpack_matches_reference(ref):
+    """embc_unpack (host, no device work) == the reference's unpack()
+    (container.hpp:258-292): offsets/lengths, and the FormatError text for
+    gaps, overlaps, overruns, trailing bytes and truncated tables."""
+    from oracle import OracleError
+    from paper_2407_04272_b200 import codec as K
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal(64) * 0.1)
+    chunks = [ref.encode_chunk(x[:8 * k], 8, 0.01, k % 3) for k in range(1, 5)]
+    good = ref.pack(chunks)
+    table = K.unpack_table(good)
+    assert [good[o:o + n] for o, n in table] == chunks
+    assert K.unpack_table(ref.pack([])) == []
+    cases = [good[:3], good[:11], good + b"\0", good[:-1], bytearray(good), bytearray(good), bytearray(good)]
+    cases[4][4] ^= 1                      # first offset skips a byte
+    cases[5][12:20] = (1 << 40).to_bytes(8, "little")  # length runs past the end
+    cases[6][0] = 200                     # rank count larger than the table
+    for buf in cases:
+        buf = bytes(buf)
+        with pytest.raises(OracleError) as r:
+            ref.unpack(buf)
+        with pytest.raises(_lib.CodecFormatError) as g:
+            K.unpack_table(buf)
+        assert str(g.value) == r.value.msg, buf[:24].hex()

@@ -29,6 +29,6 @@ def test_cpp_wrapper_compiles():
 @pytest.mark.gpu
 def test_cpp_wrapper_runs():
     _build()
-    r = subprocess.run([BIN], capture_output=True, text=True, timeout=120)
+    r = subprocess.run([BIN, ROOT], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "api_test: ok" in r.stdout
