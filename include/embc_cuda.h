@@ -298,6 +298,12 @@ embc_status embc_exchange_baseline_bwd(embc_exchange* ex, uint32_t ntables, uint
                                        uint32_t batch, const float* const* d_grads,
                                        float* const* d_outs, void* stream);
 
+/* Per-kernel CUDA-event timing of the exchange's codec launches (both
+ * contexts), as embc_timing_enable / embc_timing_collect. */
+embc_status embc_exchange_timing_enable(embc_exchange* ex, int on);
+int embc_exchange_timing_collect(embc_exchange* ex, char* names, size_t names_cap, float* ms,
+                                 int max_entries);
+
 /* ---- packed send buffer (container.hpp:258-292) --------------------------- */
 
 /* unpack()'s validation of a PackedSendBuffer (host bytes): offsets start at

@@ -98,7 +98,7 @@ EXPORTS = [
     "embc_timing_enable", "embc_timing_collect", "embc_decode_fallbacks",
     "embc_exchange_unique_id", "embc_exchange_create", "embc_exchange_destroy", "embc_exchange_get_error",
     "embc_exchange_fwd", "embc_exchange_bwd", "embc_exchange_baseline_fwd", "embc_exchange_baseline_bwd",
-    "embc_unpack",
+    "embc_unpack", "embc_exchange_timing_enable", "embc_exchange_timing_collect",
 ]
 
 _lock = threading.Lock()
@@ -154,6 +154,8 @@ def lib() -> C.CDLL:
                 "embc_exchange_bwd": (i32, [vp, u32, u32, u32, vp, vp, vp, u32, vp, C.POINTER(ExchangeStats), vp]),
                 "embc_exchange_baseline_fwd": (i32, [vp, u32, u32, u32, vp, vp, vp]),
                 "embc_exchange_baseline_bwd": (i32, [vp, u32, u32, u32, vp, vp, vp]),
+                "embc_exchange_timing_enable": (i32, [vp, i32]),
+                "embc_exchange_timing_collect": (i32, [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_float), i32]),
                 "embc_unpack": (i32, [vp, u64, vp, vp, u32, C.POINTER(u32), C.POINTER(EmbcErrorRec)]),
             }
             for name, (res, args) in sig.items():

@@ -548,6 +548,22 @@ embc_status embc_exchange_baseline_bwd(embc_exchange* ex, uint32_t T, uint32_t d
   return baseline(ex, to, from, rows, static_cast<cudaStream_t>(stream));
 }
 
+embc_status embc_exchange_timing_enable(embc_exchange* ex, int on) {
+  if (!ex) return EMBC_ERR_ARGUMENT;
+  embc_timing_enable(ex->enc, on);
+  return embc_timing_enable(ex->dec, on);
+}
+
+int embc_exchange_timing_collect(embc_exchange* ex, char* names, size_t names_cap, float* ms, int max_entries) {
+  if (!ex) return -1;
+  const int a = embc_timing_collect(ex->enc, ex->s_enc, names, names_cap, ms, max_entries);
+  if (a < 0) return a;
+  size_t used = 0;
+  for (int i = 0; i < a; ++i) used += std::strlen(names + used) + 1;
+  const int b = embc_timing_collect(ex->dec, ex->s_dec, names + used, names_cap - used, ms + a, max_entries - a);
+  return b < 0 ? b : a + b;
+}
+
 // ---- unpack (container.hpp:258-292): the offset-table validation ------------
 embc_status embc_unpack(const uint8_t* buf, uint64_t len, uint64_t* offs, uint64_t* lens, uint32_t cap,
                         uint32_t* count, embc_error* err) {

@@ -584,3 +584,17 @@ class NcclExchange:
                                                       self._ptrs(out),
                                                       torch.cuda.current_stream(self.device).cuda_stream))
         return out
+
+    def timing(self, on: bool) -> None:
+        self._check(self.L.embc_exchange_timing_enable(self.handle, 1 if on else 0))
+
+    def timing_collect(self):
+        """[(kernel name, ms)] of the codec launches since timing(True)."""
+        C = self._C
+        names = C.create_string_buffer(1 << 20)
+        ms = (C.c_float * 65536)()
+        n = self.L.embc_exchange_timing_collect(self.handle, names, 1 << 20, ms, 65536)
+        if n < 0:
+            raise self._lib.EmbcError("embc_exchange_timing_collect failed")
+        out = names.raw.split(b"\0")
+        return [(out[i].decode(), float(ms[i])) for i in range(n)]
