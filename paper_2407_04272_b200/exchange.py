@@ -218,10 +218,15 @@ class CompressedAllToAll:
         self.backend.check()
         # accounting (reference definitions: d != src only)
         for l, d, j in zip(lens_h, job_dst, jobs):
+            st.sent_values += j.batch.numel()
+            st.sent_bytes += l
             if d != self.rank:
                 st.payload_bytes += l
                 st.metadata_bytes += META
                 st.uncompressed_bytes += j.batch.numel() * 4
+        for r in refs:
+            st.recv_values += r[3] * r[4]
+            st.recv_bytes += r[1]
         if self.timing:
             names = list(ev)
             for a, b in zip(names, names[1:]):
@@ -324,10 +329,15 @@ class CompressedAllToAll:
             else:
                 self.backend.decode(recv, refs, dst_tensors)
             for l, d, j in zip(lens_h, job_dst, jobs):
+                st.sent_values += j.batch.numel()
+                st.sent_bytes += l
                 if d != self.rank:
                     st.payload_bytes += l
                     st.metadata_bytes += META
                     st.uncompressed_bytes += j.batch.numel() * 4
+            for r in refs:
+                st.recv_values += r[3] * r[4]
+                st.recv_bytes += r[1]
         if cuda:
             cur.wait_stream(self._s_dec)  # outputs are ready on the caller's stream
         if self.timing:
