@@ -340,6 +340,46 @@ uint64_t embc_mix_seed(uint64_t seed, uint64_t salt);
 embc_status embc_gather_rows(const float* d_table, uint32_t dim, const uint32_t* d_idx,
                              uint32_t batch, float* d_out, void* stream);
 
+/* ---- simulator (commsim.hpp) with the codec on the GPU ------------------ */
+
+/* TableSpec (datagen.hpp:36-47); table_id and seed are derived per rank. */
+typedef struct {
+  uint32_t rows, dim;
+  int32_t dist;  /* 0 gaussian, 1 uniform */
+  uint32_t pad;
+  double mu, sigma, lo, hi, zipf_s;
+} embc_sim_table;
+
+/* SimConfig (commsim.hpp:30-62): the fields that enter the byte accounting. */
+typedef struct {
+  uint32_t ranks, batch, iterations, compression;
+  uint64_t seed;
+  double global_eb;
+  int32_t decay_fn;  /* 0 stepwise, 1 linear, 2 log (policy.hpp:52-70) */
+  uint32_t decay_steps;
+  double decay_start_scale;
+  uint64_t decay_end;
+} embc_sim_config;
+
+/* IterationStats (commsim.hpp:77-96); times are device-measured seconds. */
+typedef struct {
+  uint64_t iteration;
+  double eb_max;
+  uint64_t uncompressed_bytes, payload_bytes, metadata_bytes, wire_bytes;
+  double comp_time, decomp_time, max_abs_error;
+  uint64_t delivery_conserved, delivered_digest;
+} embc_sim_iteration;
+
+/* Simulator::run_schedule (commsim.hpp:253-266) + run_forward_alltoall
+ * (:229-250): every rank compresses its table's per-destination batches with
+ * embc_encode (packed), every received chunk is unpacked, checked against its
+ * metadata and decoded with embc_decode into doubles.  prof_codec / prof_eb
+ * are the TableProfile of table id r (= rank r), r < ranks.  Writes
+ * `iterations` records and SimReport::deterministic_digest (:146-163). */
+embc_status embc_simulate(int device, const embc_sim_config* cfg, const embc_sim_table* tables,
+                          uint32_t ntables, const uint8_t* prof_codec, const double* prof_eb,
+                          embc_sim_iteration* out, uint64_t* report_digest, embc_error* err);
+
 #ifdef __cplusplus
 }
 #endif

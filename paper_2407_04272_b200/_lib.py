@@ -82,6 +82,26 @@ class ExchangeStats(C.Structure):
                 ("recv_bytes", C.c_uint64)]
 
 
+class SimTable(C.Structure):
+    _fields_ = [("rows", C.c_uint32), ("dim", C.c_uint32), ("dist", C.c_int32), ("pad", C.c_uint32),
+                ("mu", C.c_double), ("sigma", C.c_double), ("lo", C.c_double), ("hi", C.c_double),
+                ("zipf_s", C.c_double)]
+
+
+class SimConfig(C.Structure):
+    _fields_ = [("ranks", C.c_uint32), ("batch", C.c_uint32), ("iterations", C.c_uint32),
+                ("compression", C.c_uint32), ("seed", C.c_uint64), ("global_eb", C.c_double),
+                ("decay_fn", C.c_int32), ("decay_steps", C.c_uint32), ("decay_start_scale", C.c_double),
+                ("decay_end", C.c_uint64)]
+
+
+class SimIteration(C.Structure):
+    _fields_ = [("iteration", C.c_uint64), ("eb_max", C.c_double), ("uncompressed_bytes", C.c_uint64),
+                ("payload_bytes", C.c_uint64), ("metadata_bytes", C.c_uint64), ("wire_bytes", C.c_uint64),
+                ("comp_time", C.c_double), ("decomp_time", C.c_double), ("max_abs_error", C.c_double),
+                ("delivery_conserved", C.c_uint64), ("delivered_digest", C.c_uint64)]
+
+
 class ChunkRef(C.Structure):
     _fields_ = [("offset", C.c_uint64), ("length", C.c_uint64), ("out", C.c_void_p),
                 ("dim", C.c_uint32), ("count", C.c_uint32), ("eb", C.c_double), ("codec", C.c_uint8),
@@ -98,7 +118,7 @@ EXPORTS = [
     "embc_timing_enable", "embc_timing_collect", "embc_decode_fallbacks",
     "embc_exchange_unique_id", "embc_exchange_create", "embc_exchange_destroy", "embc_exchange_get_error",
     "embc_exchange_fwd", "embc_exchange_bwd", "embc_exchange_baseline_fwd", "embc_exchange_baseline_bwd",
-    "embc_unpack", "embc_exchange_timing_enable", "embc_exchange_timing_collect",
+    "embc_unpack", "embc_exchange_timing_enable", "embc_exchange_timing_collect", "embc_simulate",
 ]
 
 _lock = threading.Lock()
@@ -157,6 +177,8 @@ def lib() -> C.CDLL:
                 "embc_exchange_timing_enable": (i32, [vp, i32]),
                 "embc_exchange_timing_collect": (i32, [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_float), i32]),
                 "embc_unpack": (i32, [vp, u64, vp, vp, u32, C.POINTER(u32), C.POINTER(EmbcErrorRec)]),
+                "embc_simulate": (i32, [i32, C.POINTER(SimConfig), C.POINTER(SimTable), u32, vp, vp,
+                                        C.POINTER(SimIteration), C.POINTER(u64), C.POINTER(EmbcErrorRec)]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)

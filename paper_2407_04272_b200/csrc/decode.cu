@@ -181,10 +181,66 @@ struct RawTile {
   uint64_t e0, ne;
 };
 
+// 16 bytes at byte offset s (0..15, uniform) of the 32-byte window a|b, as four
+// little-endian u32 words
+__device__ __forceinline__ uint4 window16(const uint4 a, const uint4 b, uint32_t s) {
+  const uint32_t m = s >> 2, r = 8 * (s & 3);
+  const uint32_t w0 = m == 0 ? a.x : m == 1 ? a.y : m == 2 ? a.z : a.w;
+  const uint32_t w1 = m == 0 ? a.y : m == 1 ? a.z : m == 2 ? a.w : b.x;
+  const uint32_t w2 = m == 0 ? a.z : m == 1 ? a.w : m == 2 ? b.x : b.y;
+  const uint32_t w3 = m == 0 ? a.w : m == 1 ? b.x : m == 2 ? b.y : b.z;
+  const uint32_t w4 = m == 0 ? b.x : m == 1 ? b.y : m == 2 ? b.z : b.w;
+  return make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r), __funnelshift_r(w2, w3, r),
+                    __funnelshift_r(w3, w4, r));
+}
+
+// fp32 output, whole quads: aligned 16-B loads of the (unaligned) code words,
+// 16-B stores, eight quads in flight per thread
+__device__ __forceinline__ void raw_tile_f32(const DChunk& C, const uint8_t* p, double w, const RawTile& T) {
+  const uintptr_t g0 = reinterpret_cast<uintptr_t>(p + 4 * T.e0);
+  const uint4* gv = reinterpret_cast<const uint4*>(g0 & ~uintptr_t(15));
+  const uint32_t s = static_cast<uint32_t>(g0 & 15);
+  const uint32_t nq = static_cast<uint32_t>(T.ne >> 2);
+  float4* o = reinterpret_cast<float4*>(static_cast<float*>(C.out) + T.e0);
+  for (uint32_t q0 = 0; q0 < nq; q0 += 8 * blockDim.x) {
+    uint4 lo[8], hi[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t q = q0 + u * blockDim.x + threadIdx.x;
+      if (q < nq) {
+        lo[u] = __ldg(gv + q);
+        hi[u] = s ? __ldg(gv + q + 1) : lo[u];  // the block holding the quad's last byte
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t q = q0 + u * blockDim.x + threadIdx.x;
+      if (q < nq) {
+        const uint4 c = window16(lo[u], hi[u], s);
+        o[q] = make_float4(__double2float_rn(reconstruct(static_cast<int32_t>(c.x), w)),
+                           __double2float_rn(reconstruct(static_cast<int32_t>(c.y), w)),
+                           __double2float_rn(reconstruct(static_cast<int32_t>(c.z), w)),
+                           __double2float_rn(reconstruct(static_cast<int32_t>(c.w), w)));
+      }
+    }
+  }
+  for (uint64_t i = T.e0 + 4ull * nq + threadIdx.x; i < T.e0 + T.ne; i += blockDim.x) {
+    const uint8_t* q = p + 4 * i;
+    const int32_t code = static_cast<int32_t>(static_cast<uint32_t>(q[0]) | (static_cast<uint32_t>(q[1]) << 8) |
+                                              (static_cast<uint32_t>(q[2]) << 16) |
+                                              (static_cast<uint32_t>(q[3]) << 24));
+    static_cast<float*>(C.out)[i] = __double2float_rn(reconstruct(code, w));
+  }
+}
+
 __device__ __forceinline__ void raw_tile(const DChunk& C, const DecState& S, const RawTile& T) {
   if (S.err != ~0ull) return;
   const uint8_t* p = C.in + S.pay_off;
   const double w = 2.0 * S.eb;
+  if (C.out_kind == EMBC_OUT_F32 && (reinterpret_cast<uintptr_t>(C.out) & 15) == 0 && (T.e0 & 3) == 0) {
+    raw_tile_f32(C, p, w, T);
+    return;
+  }
   for (uint64_t i = T.e0 + threadIdx.x; i < T.e0 + T.ne; i += blockDim.x) {
     const uint8_t* q = p + 4 * i;
     const int32_t code = static_cast<int32_t>(static_cast<uint32_t>(q[0]) | (static_cast<uint32_t>(q[1]) << 8) |
@@ -1085,6 +1141,15 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   const uint32_t sb = b0 >= kSegBack ? b0 - kSegBack : 0;
   const uint32_t la = static_cast<uint32_t>(umin64(L - (b0 + nb), 10ull * (D + 1) + 10));
   const uint32_t ns = b0 + nb + la - sb;
+  // the header is validated by the last thread while the others stage the
+  // bytes (one round of loads)
+  if (threadIdx.x == blockDim.x - 1) {
+    s_bad = 0;
+    s_nlit = 0;
+    const DecState S = parse_chunk(C);
+    s_err = S.err;
+    s_eb = S.eb;
+  }
   {  // 16-B loads of the aligned blocks covering [sb, sb + ns); B points at byte sb
     const uintptr_t g0 = reinterpret_cast<uintptr_t>(p + sb);
     const uint4* gv = reinterpret_cast<const uint4*>(g0 & ~uintptr_t(15));
@@ -1105,13 +1170,6 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
       }
     }
     B = smem + lead;
-  }
-  if (threadIdx.x == 0) {
-    s_bad = 0;
-    s_nlit = 0;
-    const DecState S = parse_chunk(C);
-    s_err = S.err;
-    s_eb = S.eb;
   }
   __syncthreads();
   if (s_err != ~0ull) return;  // every CTA of the chunk sees it: nobody waits on this segment
@@ -1199,24 +1257,55 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   __syncthreads();
   DTS(blockIdx.x, 5);
   unsigned long long* status = a.seg_status;
+  // decoupled look-back: warp 0 finds the nearest predecessor with an
+  // inclusive state; the maps published after it are loaded by the whole CTA
+  // (one round of loads per batch of `cap` maps) and applied by thread 0.
+  // Before every batch warp 0 re-reads the 32 nearest predecessors: an
+  // inclusive state published there meanwhile replaces the maps before it.
+  __shared__ uint32_t s_m0;
+  __shared__ unsigned long long s_lb;
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0 && sp.seg > 0) st_vol(status + gseg, kStAgg);
-    unsigned long long in;
     if (sp.seg == 0) {
-      in = vlz_state(false, 0, 0);
+      if (threadIdx.x == 0) {
+        s_lb = vlz_state(false, 0, 0);
+        s_m0 = gseg;
+      }
     } else {
       unsigned long long w;
       const uint32_t q = find_inclusive(status, C.seg0, gseg, &w);
-      bool dead = (w >> 61) & 1;
-      uint32_t e = static_cast<uint32_t>(w >> 32) & 0x7FF, rows = static_cast<uint32_t>(w);
-      // apply the maps published after it: batches loaded in parallel into
-      // shared memory (the literal queue is free until the tokens), applied in order
-      const uint32_t cap = max(1u, kSeg / (D + 1));  // lit holds kSeg u32
-      for (uint32_t m0 = q + 1; m0 < gseg && !dead; m0 += cap) {
-        const uint32_t nm = min(cap, gseg - m0);
-        const uint32_t* src = a.maps + C.map_base + static_cast<uint64_t>(m0 - C.seg0) * (D + 1);
-        for (uint32_t k = threadIdx.x; k < nm * (D + 1); k += 32) lit[k] = __ldcg(src + k);
-        __syncwarp();
+      if (threadIdx.x == 0) {
+        s_lb = w & ~(3ull << 62);
+        s_m0 = q + 1;
+      }
+    }
+  }
+  __syncthreads();
+  {
+    const uint32_t cap = max(1u, kSeg / (D + 1));  // lit holds kSeg u32 (free until the tokens)
+    for (;;) {
+      if (threadIdx.x < 32 && s_m0 < gseg && !((s_lb >> 61) & 1)) {
+        const uint32_t m0 = s_m0;
+        const int64_t sidx = static_cast<int64_t>(gseg) - 1 - threadIdx.x;
+        const unsigned long long sv = sidx >= static_cast<int64_t>(m0) ? ld_vol(status + sidx) : 0ull;
+        const uint32_t inc = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
+        if (inc && threadIdx.x == __ffs(inc) - 1) {
+          s_lb = sv & ~(3ull << 62);
+          s_m0 = static_cast<uint32_t>(sidx) + 1;
+        }
+      }
+      __syncthreads();
+      const uint32_t m0 = s_m0;
+      if (m0 >= gseg || ((s_lb >> 61) & 1)) break;
+      const uint32_t nm = min(cap, gseg - m0);
+      const uint32_t* src = a.maps + C.map_base + static_cast<uint64_t>(m0 - C.seg0) * (D + 1);
+      const uint32_t tot = nm * (D + 1);
+      for (uint32_t k = threadIdx.x; k < tot; k += blockDim.x) lit[k] = __ldcg(src + k);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned long long x = s_lb;
+        bool dead = false;
+        uint32_t e = static_cast<uint32_t>(x >> 32) & 0x7FF, rows = static_cast<uint32_t>(x);
         for (uint32_t m = 0; m < nm && !dead; ++m) {
           const uint32_t v = lit[m * (D + 1) + e];
           if (v == 0xFFFFFFFFu) dead = true;
@@ -1225,26 +1314,28 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
             e = v & 0xFFFF;
           }
         }
-        __syncwarp();
+        s_lb = vlz_state(dead, e, rows);
+        s_m0 = m0 + nm;
       }
-      in = vlz_state(dead, e, rows);
+      __syncthreads();
     }
-    if (threadIdx.x == 0) {
-      bool dead = (in >> 61) & 1;
-      const uint32_t e = static_cast<uint32_t>(in >> 32) & 0x7FF, rows = static_cast<uint32_t>(in);
-      uint32_t eo = 0, ro = rows;
-      if (!dead) {
-        const uint32_t v = mymap[e];
-        if (v == 0xFFFFFFFFu) dead = true;
-        else {
-          eo = v & 0xFFFF;
-          ro = rows + (v >> 16);
-          if (ro > C.count) dead = true;  // more tokens than vectors: trailing bytes
-        }
+  }
+  if (threadIdx.x == 0) {
+    const unsigned long long in = s_lb;
+    bool dead = (in >> 61) & 1;
+    const uint32_t e = static_cast<uint32_t>(in >> 32) & 0x7FF, rows = static_cast<uint32_t>(in);
+    uint32_t eo = 0, ro = rows;
+    if (!dead) {
+      const uint32_t v = mymap[e];
+      if (v == 0xFFFFFFFFu) dead = true;
+      else {
+        eo = v & 0xFFFF;
+        ro = rows + (v >> 16);
+        if (ro > C.count) dead = true;  // more tokens than vectors: trailing bytes
       }
-      st_vol(status + gseg, kStInc | vlz_state(dead, eo, ro));
-      s_in = in;
     }
+    st_vol(status + gseg, kStInc | vlz_state(dead, eo, ro));
+    s_in = in;
   }
   __syncthreads();
   DTS(blockIdx.x, 6);
@@ -1376,7 +1467,8 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   __shared__ uint32_t G[kMaxGroups][32], BM[32];
   __shared__ uint32_t s_ge[kMaxGroups], s_gt[kMaxGroups];
   __shared__ unsigned long long s_gc[kMaxGroups];
-  __shared__ unsigned long long s_in;
+  __shared__ unsigned long long s_in, s_lb;
+  __shared__ uint32_t s_m0, s_cm[kBlock / 32][32];
   __shared__ int s_use;
   const uint32_t c = a.hblk_chunk[gb];
   const DChunk& C = a.ch[c];
@@ -1407,9 +1499,27 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   // the chunk's first bytes (header, codebook of up to 64 entries) in one round
   __shared__ __align__(8) uint8_t s_hb[kLocalHdr + 8];
   __shared__ uint64_t s_vals[64], s_starts[128];
+  const uint64_t poff = C.payload_only ? 0 : kHeader;
+  // in the same round of loads: the chunk bytes that hold this block's words
+  // for any codebook of up to 64 entries (the bitstream starts 12 + 5 nent
+  // bytes into the payload), staged in the Gs region (free until phase B)
+  const int64_t ws = static_cast<int64_t>(poff + 12 + bit0 / 8) - 4 * static_cast<int64_t>(kHPre);  // >= 4
+  const uint32_t wl = 5 * 64 + 4 * hwords;
+  uint8_t* rawb = reinterpret_cast<uint8_t*>(Gs);
+  uint32_t wlead = 0;  // chunk byte y (ws <= y < wx1) is rawb[y - ws + wlead]
+  {
+    const int64_t wx1 = static_cast<int64_t>(umin64(C.length, static_cast<uint64_t>(ws + wl)));
+    if (wx1 > ws) {
+      const uintptr_t g0 = reinterpret_cast<uintptr_t>(C.in + ws);
+      const uint4* gv = reinterpret_cast<const uint4*>(g0 & ~uintptr_t(15));
+      wlead = static_cast<uint32_t>(g0 & 15);
+      const uint32_t nv = (wlead + static_cast<uint32_t>(wx1 - ws) + 15) / 16;
+      uint4* sv = reinterpret_cast<uint4*>(rawb);
+      for (uint32_t k = threadIdx.x; k < nv; k += blockDim.x) sv[k] = __ldg(gv + k);
+    }
+  }
   for (uint32_t k = threadIdx.x; k < kLocalHdr; k += blockDim.x) s_hb[k] = k < C.length ? __ldg(C.in + k) : 0;
   __syncthreads();
-  const uint64_t poff = C.payload_only ? 0 : kHeader;
   uint64_t boff = 0, nby = 0;
   if (C.length >= poff + 12) {
     boff = 12 + 5 * ld_be(s_hb + poff + 8, 4);
@@ -1418,7 +1528,25 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
 #ifdef EMBC_DEBUG
   const unsigned long long dt0 = dtime();
 #endif
-  stage(C.in + poff + boff, nby);
+  if (boff >= 12 && boff <= 12 + 5 * 64 && C.length >= poff + boff) {
+    // W[k] = big-endian word at stream byte bit0 / 8 - 4 kHPre + 4 k (zeros
+    // outside the stream); stream byte j is chunk byte poff + boff + j
+    const int64_t sbyte0 = static_cast<int64_t>(bit0 / 8) - 4 * static_cast<int64_t>(kHPre);
+    const int64_t shift = static_cast<int64_t>(poff + boff) - ws + wlead;
+    for (uint32_t k = threadIdx.x; k < hwords; k += blockDim.x) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t j = sbyte0 + 4 * static_cast<int64_t>(k) + q;
+        const uint32_t by = (j >= 0 && static_cast<uint64_t>(j) < nby) ? rawb[j + shift] : 0u;
+        v = (v << 8) | by;
+      }
+      W[k] = v;
+    }
+  } else {
+    stage(C.in + poff + boff, nby);
+  }
+  __syncthreads();  // rawb (Gs) is read above
 #ifdef EMBC_DEBUG
   __syncthreads();
   const unsigned long long dt1 = dtime();
@@ -1654,33 +1782,77 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     __threadfence();
     __syncwarp();
     if (lane == 0 && b > 0) st_vol(status + gb, kStAgg);
-    unsigned long long in;
     if (b == 0) {
-      in = huf_state(0, 0, 0);
+      if (lane == 0) {
+        s_lb = huf_state(0, 0, 0);
+        s_m0 = gb;
+      }
     } else {
       unsigned long long w;
       const uint32_t q = find_inclusive(status, C.blk0, gb, &w);
-      uint32_t tm = static_cast<uint32_t>(w >> 60) & 3, ee = static_cast<uint32_t>(w >> 55) & 31;
-      uint64_t cc = w & ((1ull << 55) - 1);
-      // maps published after it: lane e holds entry e of each map (loads in
-      // flight together), applied in order by shuffles
-      for (uint32_t m0 = q + 1; m0 < gb && !tm; m0 += 8) {
-        uint32_t f[8];
+      if (lane == 0) {
+        s_lb = w & ~(3ull << 62);
+        s_m0 = q + 1;
+      }
+    }
+  }
+  __syncthreads();
+  // the maps published after it, 128 per round: every warp loads 16 (lane e
+  // holds entry e of each) and composes them into one map by shuffles; thread
+  // 0 applies the eight composed maps in order.  Before every round warp 0
+  // re-reads the 32 nearest predecessors: an inclusive state published there
+  // meanwhile replaces the maps before it.
+  for (;;) {
+    if (warp == 0 && s_m0 < gb && !((s_lb >> 60) & 3)) {
+      const uint32_t m0 = s_m0;
+      const int64_t sidx = static_cast<int64_t>(gb) - 1 - lane;
+      const unsigned long long sv = sidx >= static_cast<int64_t>(m0) ? ld_vol(status + sidx) : 0ull;
+      const uint32_t inc = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
+      if (inc && lane == static_cast<uint32_t>(__ffs(inc) - 1)) {
+        s_lb = sv & ~(3ull << 62);
+        s_m0 = static_cast<uint32_t>(sidx) + 1;
+      }
+    }
+    __syncthreads();
+    const uint32_t m0 = s_m0;
+    if (m0 >= gb || ((s_lb >> 60) & 3)) break;
+    const uint32_t nm = min(128u, gb - m0);
+    {
+      const uint32_t w0 = m0 + 16 * warp;
+      uint32_t f[16];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) f[k] = m0 + k < gb ? __ldcg(a.bmaps + static_cast<uint64_t>(m0 + k) * 32 + lane) : 0;
+      for (int k = 0; k < 16; ++k) f[k] = w0 + k < m0 + nm ? __ldcg(a.bmaps + static_cast<uint64_t>(w0 + k) * 32 + lane) : 0;
+      uint32_t e = lane, tm = 0, cnt = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t v = __shfl_sync(0xffffffffu, f[k], ee);
-          if (m0 + k < gb && !tm) {
-            tm = pk_term(v);
-            cc += pk_cnt(v);
-            ee = pk_off(v);
-          }
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t v = __shfl_sync(0xffffffffu, f[k], e);
+        if (w0 + k < m0 + nm && !tm) {
+          tm = pk_term(v);
+          cnt += pk_cnt(v);
+          e = pk_off(v);
         }
       }
-      in = huf_state(tm, ee, cc);
+      s_cm[warp][lane] = pk(e, tm, cnt);
     }
-    if (lane == 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned long long x = s_lb;
+      uint32_t tm = static_cast<uint32_t>(x >> 60) & 3, ee = static_cast<uint32_t>(x >> 55) & 31;
+      uint64_t cc = x & ((1ull << 55) - 1);
+      for (uint32_t k = 0; k < (nm + 15) / 16 && !tm; ++k) {
+        const uint32_t v = s_cm[k][ee];
+        tm = pk_term(v);
+        cc += pk_cnt(v);
+        ee = pk_off(v);
+      }
+      s_lb = huf_state(tm, ee, cc);
+      s_m0 = m0 + nm;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const unsigned long long in = s_lb;
+    {
       uint32_t tm = static_cast<uint32_t>(in >> 60) & 3, ee = static_cast<uint32_t>(in >> 55) & 31;
       uint64_t cc = in & ((1ull << 55) - 1);
       if (!tm) {
@@ -1821,6 +1993,7 @@ __device__ void copy_tile(const DecArgs& a, uint32_t b, uint8_t* smem) {
                *reinterpret_cast<volatile uint32_t*>(&a.vflag[c]);
     }
     __syncthreads();
+    DTS(blockIdx.x, 2);
     if (s_skip) return;
   }
   {
@@ -1856,6 +2029,7 @@ __device__ void copy_tile(const DecArgs& a, uint32_t b, uint8_t* smem) {
       }
       if (!__syncthreads_or(changed)) break;
     }
+    DTS(blockIdx.x, 3);
     // 16-B units per row when rows are 16-B aligned, else 4-B (8-B for fp64) elements
     const uint32_t esz = C.out_kind == EMBC_OUT_F64 ? 8 : 4;
     const bool vec = ((D * esz) & 15) == 0 && (reinterpret_cast<uintptr_t>(C.out) & 15) == 0;
@@ -1908,6 +2082,7 @@ __device__ void finish_chunk(const DecArgs& a, uint32_t c) {
       atomicAdd(&a.tickets[2], 1u);
   }
   __syncthreads();
+  DTS(blockIdx.x, 2);
   if (codec == EMBC_CODEC_VLZ) k_dec_vlz_seq_cta(c, a.ch, a.st, nullptr, a.vflag);
   else if (codec == EMBC_CODEC_HUFFMAN) k_dec_huff_seq_cta(c, a.ch, a.st, nullptr, a.tabs, a.hflag);
   __shared__ int s_last;
@@ -1921,7 +2096,7 @@ __device__ void finish_chunk(const DecArgs& a, uint32_t c) {
     if (threadIdx.x == 0) *a.diag = atomicAdd(&a.tickets[2], 0u);  // decode fallbacks of this call
 #ifdef EMBC_DEBUG
     if (threadIdx.x != 0) return;
-    const uint32_t nb = a.nchunks + a.nseg + a.nhblk + a.nraw;
+    const uint32_t nb = a.nchunks + a.nseg + a.nhblk + a.nraw + a.nctile + a.nchunks - 1;
     if (a.nchunks >= 26 && (++g_dcalls) % 8 == 7 && nb <= 16384) {
       printf("D1 huffman blocks: local tables %llu, waited %llu; mean ns local build %llu (warp %llu, lut %llu), stage %llu\n",
              g_dloc[0], g_dloc[1], g_dloc[2] / max(1ull, g_dloc[0] + g_dloc[1]), g_dloc[4] / max(1ull, g_dloc[0]),
@@ -1929,7 +2104,7 @@ __device__ void finish_chunk(const DecArgs& a, uint32_t c) {
       for (int q = 0; q < 12; ++q) g_dloc[q] = 0;
       unsigned long long t0 = ~0ull;
       for (uint32_t k = 0; k < nb; ++k) t0 = min(t0, g_dts[k][1]);
-      const char* names[4] = {"chunk", "vlzseg", "hufblk", "raw"};
+      const char* names[6] = {"chunk", "vlzseg", "hufblk", "raw", "copy", "finish"};
       {  // huffman table build phases (slots 8000 + chunk: 8 start, 2 keys, 3 sort, 4 codes, 5 lut, 6 dup sort)
         unsigned long long n = 0, sm[6] = {0}, mx[6] = {0};
         const int ord[6] = {8, 2, 3, 4, 5, 6};
@@ -1949,7 +2124,7 @@ __device__ void finish_chunk(const DecArgs& a, uint32_t c) {
                  sm[0] / n, mx[0], sm[1] / n, mx[1], sm[2] / n, mx[2], sm[3] / n, mx[3], sm[4] / n, mx[4], sm[5] / n, mx[5]);
         for (uint32_t c = 0; c < a.nchunks && 8000 + c < 16384; ++c) g_dts[8000 + c][8] = g_dts[8000 + c][6] = 0;
       }
-      for (uint32_t role = 0; role < 4; ++role) {
+      for (uint32_t role = 0; role < 6; ++role) {
         unsigned long long n = 0, mn = ~0ull, mx = 0, sum[12] = {0}, mxs[12] = {0};
         for (uint32_t k = 0; k < nb; ++k) {
           if (g_dts[k][0] != role) continue;
@@ -2044,18 +2219,27 @@ __global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
   if (t < a.nraw) {
     DROLE(blockIdx.x, 3);
     DTS(blockIdx.x, 1);
+    __shared__ DecState sR;
     const RawTile T = a.raw[t];
     const DChunk& C = a.ch[T.chunk];
-    raw_tile(C, parse_chunk(C), T);
+    if (threadIdx.x == 0) sR = parse_chunk(C);
+    __syncthreads();
+    raw_tile(C, sR, T);
     DTS(blockIdx.x, 7);
     return;
   }
   t -= a.nraw;
   if (t < a.nctile) {
+    DROLE(blockIdx.x, 4);
+    DTS(blockIdx.x, 1);
     copy_tile(a, t, smem);
+    DTS(blockIdx.x, 7);
     return;
   }
+  DROLE(blockIdx.x, 5);
+  DTS(blockIdx.x, 1);
   finish_chunk(a, t - a.nctile);
+  DTS(blockIdx.x, 7);
 }
 
 }  // namespace embc_dev

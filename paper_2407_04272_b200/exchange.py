@@ -349,9 +349,11 @@ class CompressedAllToAll:
         self.stats = st
         return st
 
-    def forward(self, iteration: int, lookups: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
+    def forward(self, iteration: int, lookups: Dict[int, torch.Tensor],
+                out: Optional[Dict[int, torch.Tensor]] = None) -> Dict[int, torch.Tensor]:
         """lookups[t] for owned t: [R*B, dim] with rows d*B..(d+1)*B destined to
-        rank d.  Returns {t: [B, dim]} for every table (rank's data-parallel slice)."""
+        rank d.  Returns {t: [B, dim]} for every table (rank's data-parallel
+        slice), decoded into `out` when given (contiguous [B, dim] per table)."""
         R, B = self.R, self.B
         own = self.owned(self.rank)
         jobs, job_dst = [], []
@@ -361,7 +363,8 @@ class CompressedAllToAll:
                 jobs.append(K.EncodeJob(lookups[t][d * B:(d + 1) * B], eb, self._codec(self.profiles, t),
                                         self.window))
                 job_dst.append(d)
-        out = {t: torch.empty((B, self.dim), dtype=self.out_dtype, device=self.device) for t in range(self.T)}
+        if out is None:
+            out = {t: torch.empty((B, self.dim), dtype=self.out_dtype, device=self.device) for t in range(self.T)}
         if self.groups > 1:  # group k = the k-th run of every rank's owned tables
             jobs_by, dst_by, plan_by, outs_by = [], [], [], []
             G = min(self.groups, max(len(self.owned(r)) for r in range(R)))  # identical on every rank
@@ -557,9 +560,12 @@ class NcclExchange:
         return ExchangeStats(s.uncompressed_bytes, s.payload_bytes, s.metadata_bytes, {}, s.sent_values, s.sent_bytes,
                              s.recv_values, s.recv_bytes)
 
-    def forward(self, iteration: int, lookups: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
-        """lookups[t] for owned t: [R*B, dim].  Returns {t: [B, dim]} for every table."""
-        out = {t: torch.empty((self.B, self.dim), dtype=torch.float32, device=self.device) for t in range(self.T)}
+    def forward(self, iteration: int, lookups: Dict[int, torch.Tensor],
+                out: Optional[Dict[int, torch.Tensor]] = None) -> Dict[int, torch.Tensor]:
+        """lookups[t] for owned t: [R*B, dim].  Returns {t: [B, dim]} for every
+        table, decoded into `out` when given."""
+        if out is None:
+            out = {t: torch.empty((self.B, self.dim), dtype=torch.float32, device=self.device) for t in range(self.T)}
         ebs, codecs = self._policy(iteration, self.profiles, self.cfg)
         st = self._lib.ExchangeStats()
         self._check(self.L.embc_exchange_fwd(self.handle, self.T, self.dim, self.B, self._ptrs(lookups), ebs, codecs,
