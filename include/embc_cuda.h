@@ -209,6 +209,19 @@ embc_status embc_encode(embc_ctx* ctx, const embc_job* h_jobs, uint32_t njobs, i
 embc_status embc_decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* h_refs,
                         uint32_t nrefs, int out_kind, int payload_only, void* stream);
 
+/* embc_decode with the chunk lengths (and offsets) in DEVICE memory, as they
+ * arrive from a peer: h_refs[c].offset is the chunk's base offset in d_in and
+ * h_refs[c].length its capacity (the most bytes its sender may write); the
+ * chunk is d_len[c] bytes at d_in + h_refs[c].offset + (d_off ? d_off[c] : 0).
+ * The decode plan is computed on the device, so the call needs no host read
+ * and can be captured in a CUDA graph.  A length above the capacity fails the
+ * chunk (EMBC_ERR_FORMAT, reason EMBC_R_CAPACITY).  Replaces the receiving
+ * half of Simulator::rank_body stage 4 (commsim.hpp:356-378) without the
+ * metadata round trip through the host. */
+embc_status embc_decode_dev(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* h_refs, uint32_t nrefs,
+                            const uint64_t* d_off, const uint64_t* d_len, int out_kind, int payload_only,
+                            void* stream);
+
 /* Number of chunks of the last embc_decode call that took the exact
  * sequential walker instead of the parallel decoders (malformed input, or a
  * shape outside the parallel envelope).  Synchronous. */

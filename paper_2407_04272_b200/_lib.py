@@ -118,7 +118,7 @@ EXPORTS = [
     "embc_timing_enable", "embc_timing_collect", "embc_decode_fallbacks",
     "embc_exchange_unique_id", "embc_exchange_create", "embc_exchange_destroy", "embc_exchange_get_error",
     "embc_exchange_fwd", "embc_exchange_bwd", "embc_exchange_baseline_fwd", "embc_exchange_baseline_bwd",
-    "embc_unpack", "embc_exchange_timing_enable", "embc_exchange_timing_collect", "embc_simulate",
+    "embc_unpack", "embc_exchange_timing_enable", "embc_exchange_timing_collect", "embc_simulate", "embc_decode_dev",
 ]
 
 _lock = threading.Lock()
@@ -150,6 +150,7 @@ def lib() -> C.CDLL:
                 "embc_encode_bound": (u64, [C.POINTER(Job), u32, i32]),
                 "embc_encode": (i32, [vp, C.POINTER(Job), u32, i32, vp, u64, vp, vp, vp, vp, vp]),
                 "embc_decode": (i32, [vp, vp, C.POINTER(ChunkRef), u32, i32, i32, vp]),
+                "embc_decode_dev": (i32, [vp, vp, C.POINTER(ChunkRef), u32, vp, vp, i32, i32, vp]),
                 "embc_quantize": (i32, [vp, vp, i32, u64, dbl, vp, vp]),
                 "embc_dequantize": (i32, [vp, vp, u64, dbl, vp, i32, vp]),
                 "embc_match_stats": (i32, [vp, vp, u32, u32, u32, C.POINTER(u64), C.POINTER(u64), vp]),

@@ -129,6 +129,16 @@ class Context:
                                  1 if payload_only else 0, _stream_ptr(stream))
         self.check(st)
 
+    def decode_dev_raw(self, buf: torch.Tensor, refs, d_off, d_len: torch.Tensor, out_kind: int,
+                       payload_only: bool = False, stream=None) -> None:
+        """embc_decode_dev: refs carry (base offset, capacity); the received
+        relative offsets / lengths are device int64 tensors (async, capturable)."""
+        arr = (_lib.ChunkRef * len(refs))(*refs)
+        st = self._L.embc_decode_dev(self.handle, buf.data_ptr(), arr, len(refs),
+                                     d_off.data_ptr() if d_off is not None else None, d_len.data_ptr(), out_kind,
+                                     1 if payload_only else 0, _stream_ptr(stream))
+        self.check(st)
+
 
 @dataclass
 class EncodeJob:

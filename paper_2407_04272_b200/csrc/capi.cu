@@ -19,7 +19,8 @@ embc_status encode(embc_ctx* ctx, const embc_job* hj, uint32_t njobs, int layout
                    uint64_t cap, uint64_t* d_offsets, uint64_t* d_lengths, uint8_t* d_meta,
                    uint64_t* d_total, cudaStream_t stream);
 embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* refs, uint32_t n,
-                   int out_kind, int payload_only, cudaStream_t stream);
+                   int out_kind, int payload_only, cudaStream_t stream, const uint64_t* d_len = nullptr,
+                   const uint64_t* d_off = nullptr);
 embc_status match_stats(embc_ctx* ctx, const int32_t* d_codes, uint32_t dim, uint32_t n,
                         uint32_t window, uint64_t* h_lit, uint64_t* h_ref, cudaStream_t stream);
 embc_status pattern_counts(embc_ctx* ctx, const float* d_x, uint32_t dim, uint32_t rows, double eb,
@@ -403,6 +404,15 @@ embc_status embc_decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref
     return ctx ? set_error(ctx, EMBC_ERR_ARGUMENT, 0, 0, 0, 0, 0, "invalid embc_decode arguments")
                : EMBC_ERR_ARGUMENT;
   return decode(ctx, d_in, h_refs, nrefs, out_kind, payload_only, S(stream));
+}
+
+embc_status embc_decode_dev(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* h_refs, uint32_t nrefs,
+                            const uint64_t* d_off, const uint64_t* d_len, int out_kind, int payload_only,
+                            void* stream) {
+  if (!ctx || (!h_refs && nrefs) || (!d_len && nrefs) || out_kind < 0 || out_kind > 2)
+    return ctx ? set_error(ctx, EMBC_ERR_ARGUMENT, 0, 0, 0, 0, 0, "invalid embc_decode_dev arguments")
+               : EMBC_ERR_ARGUMENT;
+  return decode(ctx, d_in, h_refs, nrefs, out_kind, payload_only, S(stream), d_len, d_off);
 }
 
 embc_status embc_quantize(embc_ctx* ctx, const void* d_x, int x_f64, uint64_t n, double eb,

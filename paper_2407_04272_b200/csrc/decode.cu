@@ -1100,8 +1100,12 @@ struct DecArgs {
   uint32_t* diag;
   uint32_t nchunks, nseg, nhblk, nraw, nctile;
   uint32_t vlz_dmax;    // largest vlz dim of the call (sizes the segment smem carve)
-  uint32_t hsub;        // subsequences per huffman block (128 or 256)
+  uint32_t hsub;        // subsequences per huffman block
+  uint32_t sbits;       // bits per subsequence (32 or 64)
+  uint32_t local_tables;  // small calls: every huffman block builds its own decode tables
   uint32_t smem_bytes;  // dynamic shared memory of k_dec_main
+  const uint32_t* dcount;  // device-planned calls: [0] vlz segments, [1] huffman blocks (else null)
+  uint32_t persistent;     // CTAs loop over role tickets (device-planned calls)
 };
 
 __device__ __forceinline__ uint64_t stage_varint(const uint8_t* B, uint32_t start, uint32_t end) {
@@ -1436,9 +1440,9 @@ constexpr uint32_t kHSub = 256;                        // subsequences per block
 constexpr uint32_t kMaxGroups = 32;                    // group walks per block (8 warps, up to four each)
 constexpr uint32_t kHPre = 2;                          // words staged before the block (warm-up)
 // smem: LUT | two-codeword LUT | staged words | per-subsequence chain summaries | group states, later the symbols (u16)
-__host__ __device__ constexpr uint32_t huff_smem(uint32_t hsub) {
-  return (1u << kL0) * 4 + (1u << kL0) * 2 + (((kHPre + hsub * 2 + 4) * 4 + 15) & ~15u) + hsub * 20 +
-         (hsub * 33 * 4 > hsub * kSubBits * 2 ? hsub * 33 * 4 : hsub * kSubBits * 2);
+__host__ __device__ constexpr uint32_t huff_smem(uint32_t hsub, uint32_t sbits = kSubBits) {
+  return (1u << kL0) * 4 + (1u << kL0) * 2 + (((kHPre + hsub * sbits / 32 + 4) * 4 + 15) & ~15u) + hsub * 20 +
+         (hsub * 33 * 4 > hsub * sbits * 2 ? hsub * 33 * 4 : hsub * sbits * 2);
 }
 constexpr uint32_t kHuffSmem = huff_smem(kHSub);
 
@@ -1473,7 +1477,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   const uint32_t c = a.hblk_chunk[gb];
   const DChunk& C = a.ch[c];
   const uint32_t b = gb - C.blk0;
-  const uint32_t hsub = a.hsub, hbits = hsub * kSubBits, hwords = kHPre + hbits / 32 + 4;
+  const uint32_t hsub = a.hsub, SB = a.sbits, SW = SB / 32, hbits = hsub * SB, hwords = kHPre + hbits / 32 + 4;
   uint32_t* lut = reinterpret_cast<uint32_t*>(smem);
   uint16_t* luta = reinterpret_cast<uint16_t*>(lut + (1u << kL0));  // two-codeword steps (lengths only)
   uint32_t* W = lut + (1u << kL0) + (1u << kL0) / 2;
@@ -1553,7 +1557,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
 #endif
   // small calls (128-subsequence blocks) build block-local tables: there the
   // blocks start with the chunk CTAs and would otherwise wait on them
-  const bool local = hsub == 128 && huff_tables_local(C, s_hb, t, lut, s_vals, s_starts);
+  const bool local = a.local_tables && huff_tables_local(C, s_hb, t, lut, s_vals, s_starts);
 #ifdef EMBC_DEBUG
   if (threadIdx.x == 0) {
     atomicAdd(&g_dloc[local ? 0 : 1], 1ull);
@@ -1621,17 +1625,17 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   // decode from relative bit q (of subsequence i) until q >= 64, a start in
   // `stop` (the result then follows xs), or the end
   auto run = [&](uint32_t i, uint32_t q, uint64_t stop, uint32_t xs) -> uint32_t {
-    const uint64_t gbase = bit0 + static_cast<uint64_t>(i) * kSubBits;
+    const uint64_t gbase = bit0 + static_cast<uint64_t>(i) * SB;
     uint32_t n = 0;
     for (;;) {
-      if (q >= kSubBits) return pk(q - kSubBits, 0, n);
+      if (q >= SB) return pk(q - SB, 0, n);
       if ((stop >> q) & 1) return pk(pk_off(xs), pk_term(xs), n + pk_cnt(xs) - popc_below(stop, q));
       if (gbase + q >= nbits) return pk(0, 2, n);
-      const uint32_t bits = speek(W, (kHPre * 32) + i * kSubBits + q);
+      const uint32_t bits = speek(W, (kHPre * 32) + i * SB + q);
       const uint32_t la = luta[bits >> (32 - kL0)];
       if ((la >> 10) == 2) {
         const uint32_t l1 = la & 31, l12 = l1 + ((la >> 5) & 31);
-        if (q + l1 < kSubBits && !((stop >> (q + l1)) & 1) && gbase + q + l12 <= nbits) {
+        if (q + l1 < SB && !((stop >> (q + l1)) & 1) && gbase + q + l12 <= nbits) {
           q += l12;
           n += 2;
           continue;
@@ -1647,8 +1651,8 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   // ---- A
   const uint32_t i_me = threadIdx.x;
   if (i_me < nloc) {
-    const uint64_t gbase = bit0 + static_cast<uint64_t>(i_me) * kSubBits;
-    const SubWin win(W, kHPre + 2 * i_me);  // the subsequence starts at word kHPre + 2 i
+    const uint64_t gbase = bit0 + static_cast<uint64_t>(i_me) * SB;
+    const SubWin win(W, kHPre + SW * i_me);  // the subsequence starts at word kHPre + SW i
     uint64_t bm = 0;
     uint32_t x0 = 0;
     // warm-up from 64 bits earlier (none at the very start of the stream)
@@ -1673,8 +1677,8 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     }
     uint32_t q = static_cast<uint32_t>(p), cnt = 0;
     for (;;) {
-      if (q >= kSubBits) {
-        x0 = pk(q - kSubBits, 0, cnt);
+      if (q >= SB) {
+        x0 = pk(q - SB, 0, cnt);
         break;
       }
       if (gbase + q >= nbits) {
@@ -1685,7 +1689,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
       const uint32_t la = luta[bits >> (32 - kL0)];
       if ((la >> 10) == 2) {  // two codewords, the second starting inside the subsequence
         const uint32_t l1 = la & 31, l12 = l1 + ((la >> 5) & 31);
-        if (q + l1 < kSubBits && gbase + q + l12 <= nbits) {
+        if (q + l1 < SB && gbase + q + l12 <= nbits) {
           bm |= (1ull << q) | (1ull << (q + l1));
           q += l12;
           cnt += 2;
@@ -1899,17 +1903,17 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   auto ldv = [&](uint32_t k) -> uint64_t { return local ? vals[k] : __ldcg(vals + k); };
   if (threadIdx.x < nloc && !pk_term(q)) {
     const uint32_t i = threadIdx.x, g = i >> gsh;
-    const uint64_t gbase = bit0 + static_cast<uint64_t>(i) * kSubBits;
+    const uint64_t gbase = bit0 + static_cast<uint64_t>(i) * SB;
     uint64_t gi = s_gc[g] + pk_cnt(q);  // index of this subsequence's first symbol
     uint32_t p = pk_off(q);
-    const SubWin cwin(W, kHPre + 2 * i);
-    while (p < kSubBits && gi < N && gbase + p < nbits) {
+    const SubWin cwin(W, kHPre + SW * i);
+    while (p < SB && gi < N && gbase + p < nbits) {
       const uint32_t bits = cwin.peek(static_cast<int>(p));
       if (staged && gi + 1 < N) {
         const uint32_t la = luta[bits >> (32 - kL0)];
         if ((la >> 10) == 2) {
           const uint32_t l1 = la & 31, l12 = l1 + ((la >> 5) & 31);
-          if (p + l1 < kSubBits && gbase + p + l12 <= nbits) {
+          if (p + l1 < SB && gbase + p + l12 <= nbits) {
             const uint32_t w = bits >> (32 - kL0);
             outs[gi - blk_base] = static_cast<uint16_t>(lut[w] >> 6);
             outs[gi + 1 - blk_base] = static_cast<uint16_t>(lut[(w << l1) & ((1u << kL0) - 1)] >> 6);
@@ -1989,7 +1993,7 @@ __device__ void copy_tile(const DecArgs& a, uint32_t b, uint8_t* smem) {
     const uint32_t c = a.ctile[3 * b];
     if (threadIdx.x == 0) {
       wait_count(&a.vdone[c], a.ch[c].nseg);
-      s_skip = *reinterpret_cast<volatile unsigned long long*>(&a.st[c].err) != ~0ull ||
+      s_skip = a.ch[c].seq || *reinterpret_cast<volatile unsigned long long*>(&a.st[c].err) != ~0ull ||
                *reinterpret_cast<volatile uint32_t*>(&a.vflag[c]);
     }
     __syncthreads();
@@ -2159,36 +2163,22 @@ __device__ void finish_chunk(const DecArgs& a, uint32_t c) {
   }
 }
 
-__global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_t;
-  if (threadIdx.x == 0) s_t = atomicAdd(&a.tickets[0], 1u);
-  __syncthreads();
-  uint32_t t = s_t;  // roles in ticket order: look-back only ever waits on earlier tickets
-#ifdef EMBC_DEBUG
-  struct SpanEnd {
-    uint32_t n;
-    __device__ ~SpanEnd() {
-      if (threadIdx.x != 0) return;
-      atomicMax(&g_kspan[1], dtime());
-      __threadfence();
-      if (atomicAdd(&g_kspan[2], 1ull) == n - 1) {
-        const unsigned long long k = atomicAdd(&g_kspan[3], 1ull);
-        if (k < 400) printf("KSPAN dec %llu %llu\n", g_kspan[0], atomicMax(&g_kspan[1], 0ull));
-        g_kspan[0] = ~0ull;
-        g_kspan[1] = 0;
-        g_kspan[2] = 0;
-      }
-    }
-  } span_end{gridDim.x};
-  if (threadIdx.x == 0) atomicMin(&g_kspan[0], dtime());
-#endif
+// One role of k_dec_main, by ticket (chunk CTAs, vlz segments, huffman
+// blocks, raw tiles, copy tiles, per-chunk finishers).
+__device__ __forceinline__ void dec_role(const DecArgs& a, uint32_t t, uint8_t* smem) {
   DROLE(blockIdx.x, 0);
   DTS(blockIdx.x, 1);
   if (t < a.nchunks) {  // chunk CTA: header + (huffman) decode tables, then the ready flag
     __shared__ DecState sS;
     const DChunk& C = a.ch[t];
-    if (threadIdx.x == 0) sS = parse_chunk(C);
+    if (threadIdx.x == 0) {
+      sS = parse_chunk(C);
+      if (C.bad) {  // device-planned: the received length exceeded the chunk's capacity
+        sS.err = err_key(0, EMBC_R_CAPACITY);
+        sS.a = C.map_base;  // the received length
+        sS.b = C.length;    // the capacity
+      }
+    }
     __syncthreads();
     if (C.codec == EMBC_CODEC_HUFFMAN)
       huff_tables(t, a.ch, sS, a.keys, a.tabs, a.hflag, reinterpret_cast<uint64_t*>(smem), a.smem_bytes / 8);
@@ -2202,20 +2192,21 @@ __global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
     return;
   }
   t -= a.nchunks;
-  if (t < a.nseg) {
+  const uint32_t nseg = a.dcount ? a.dcount[0] : a.nseg, nhblk = a.dcount ? a.dcount[1] : a.nhblk;
+  if (t < nseg) {
     vlz_segment(a, t, smem);
     DTS(blockIdx.x, 7);
     done_signal(&a.vdone[a.segs[t].chunk]);
     return;
   }
-  t -= a.nseg;
-  if (t < a.nhblk) {
+  t -= nseg;
+  if (t < nhblk) {
     huff_block(a, t, smem);
     DTS(blockIdx.x, 7);
     done_signal(&a.hdone[a.hblk_chunk[t]]);
     return;
   }
-  t -= a.nhblk;
+  t -= nhblk;
   if (t < a.nraw) {
     DROLE(blockIdx.x, 3);
     DTS(blockIdx.x, 1);
@@ -2242,6 +2233,113 @@ __global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
   DTS(blockIdx.x, 7);
 }
 
+__global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_t;
+  // roles in ticket order: look-back only ever waits on earlier tickets (held
+  // by running CTAs), so persistent CTAs that loop over tickets cannot deadlock
+  for (;;) {
+    if (threadIdx.x == 0) s_t = atomicAdd(&a.tickets[0], 1u);
+    __syncthreads();
+    const uint32_t t = s_t;
+    if (a.persistent) {
+      const uint32_t total = a.nchunks + a.dcount[0] + a.dcount[1] + a.nraw + a.nctile + a.nchunks;
+      if (t >= total) return;
+    }
+    dec_role(a, t, smem);
+    if (!a.persistent) return;
+    __syncthreads();  // the role's shared state is dead before the next ticket
+  }
+}
+
+// Device-planned calls (embc_decode_dev): the received chunk lengths and
+// offsets are device data, so the per-chunk plan the host computes for
+// embc_decode (segments, blocks, table offsets) is computed here, by one CTA,
+// before k_dec_main; scratch was sized by the host from the chunk capacities.
+struct PlanArgs {
+  DChunk* ch;
+  const uint64_t* d_len;
+  const uint64_t* d_off;  // may be null
+  SegPair* segs;
+  uint32_t* hblk_chunk;
+  uint32_t* dcount;       // [0] vlz segments, [1] huffman blocks
+  uint32_t n, hsub, sbits;
+};
+
+__global__ void __launch_bounds__(1024) k_dec_plan(PlanArgs p) {
+  __shared__ unsigned long long s_tmp64[33];
+  __shared__ unsigned long long s_carry[4];
+  if (threadIdx.x < 4) s_carry[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint32_t c0 = 0; c0 < p.n; c0 += blockDim.x) {
+    const uint32_t c = c0 + threadIdx.x;
+    unsigned long long nseg = 0, maps = 0, tabb = 0, nblk = 0;
+    DChunk C{};
+    if (c < p.n) {
+      C = p.ch[c];
+      const uint64_t cap = C.length;
+      const uint64_t len = p.d_len[c];
+      if (p.d_off) C.in += p.d_off[c];
+      if (len > cap) {
+        C.bad = 1;
+        C.map_base = len;
+        C.length = 0;
+      } else {
+        C.length = len;
+      }
+      const uint64_t hdr = C.payload_only ? 0 : kHeader;
+      const uint64_t pay = C.length > hdr ? C.length - hdr : 0;
+      if (C.bad) {
+        C.seq = 1;
+      } else if (C.codec == EMBC_CODEC_VLZ) {
+        C.seq = (C.dim == 0 || C.dim > kVlzMaxDim || C.N >= (1ull << 31) || pay >= (1ull << 31) ||
+                 (pay == 0 && C.count > 0)) ? 1 : 0;
+        if (!C.seq) {
+          nseg = (pay + kSeg - 1) / kSeg;
+          maps = nseg * (C.dim + 1);
+        }
+      } else if (C.codec == EMBC_CODEC_HUFFMAN) {
+        const uint64_t ecap = pay > 12 ? (pay - 12) / 5 + 1 : 1;
+        uint64_t p2 = 1;
+        while (p2 < ecap) p2 <<= 1;
+        C.book_cap = static_cast<uint32_t>(ecap > p2 ? ecap : p2);
+        const uint64_t hb = htab_bytes(C.book_cap), kb = 8 * p2 + 16;
+        tabb = (hb > kb ? hb : kb);
+        C.nsub = static_cast<uint32_t>((8 * (pay > 12 ? pay - 12 : 0) + p.sbits - 1) / p.sbits);
+        nblk = (C.nsub + p.hsub - 1) / p.hsub;
+      }
+    }
+    unsigned long long t0, t1, t2, t3;
+    const unsigned long long e0 = block_excl_scan<unsigned long long>(nseg, s_tmp64, &t0);
+    const unsigned long long e1 = block_excl_scan<unsigned long long>(maps, s_tmp64, &t1);
+    const unsigned long long e2 = block_excl_scan<unsigned long long>(tabb, s_tmp64, &t2);
+    const unsigned long long e3 = block_excl_scan<unsigned long long>(nblk, s_tmp64, &t3);
+    if (c < p.n) {
+      C.seg0 = static_cast<uint32_t>(s_carry[0] + e0);
+      C.nseg = static_cast<uint32_t>(nseg);
+      if (!C.bad) C.map_base = s_carry[1] + e1;
+      C.tab_off = s_carry[2] + e2;
+      C.blk0 = static_cast<uint32_t>(s_carry[3] + e3);
+      C.nblk = static_cast<uint32_t>(nblk);
+      p.ch[c] = C;
+      for (uint32_t k = 0; k < nseg; ++k) p.segs[C.seg0 + k] = SegPair{c, k};
+      for (uint32_t k = 0; k < nblk; ++k) p.hblk_chunk[C.blk0 + k] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_carry[0] += t0;
+      s_carry[1] += t1;
+      s_carry[2] += t2;
+      s_carry[3] += t3;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    p.dcount[0] = static_cast<uint32_t>(s_carry[0]);
+    p.dcount[1] = static_cast<uint32_t>(s_carry[3]);
+  }
+}
+
 }  // namespace embc_dev
 
 // ===========================================================================
@@ -2258,15 +2356,24 @@ cudaError_t decode_set_attributes() {
   return e;
 }
 
+// d_len == nullptr: lengths and offsets are the refs' (host plan, exact grid).
+// d_len != nullptr (embc_decode_dev): refs[c].length is the chunk's capacity
+// and refs[c].offset its base; the received length d_len[c] and relative
+// offset d_off[c] are device data.  Scratch is sized from the capacities, the
+// plan is computed on the device (k_dec_plan), and k_dec_main runs as
+// persistent CTAs over the device-counted roles: no host read of the lengths,
+// so the call is graph-capturable.
 embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* refs, uint32_t n,
-                   int out_kind, int payload_only, cudaStream_t stream) {
+                   int out_kind, int payload_only, cudaStream_t stream, const uint64_t* d_len,
+                   const uint64_t* d_off) {
   if (n == 0) return EMBC_OK;
+  const bool dev = d_len != nullptr;
   if (!d_in) return set_error(ctx, EMBC_ERR_ARGUMENT, 0, 0, 0, 0, 0, "null input buffer");
   std::vector<DChunk> ch(n);
   std::vector<RawTile> raw_tiles;
   std::vector<SegPair> segs;
   std::vector<uint32_t> hblk, ctiles;
-  uint64_t map_total = 0, row_total = 0, tab_total = 0, huf_subs = 0;
+  uint64_t map_total = 0, row_total = 0, tab_total = 0, huf_subs = 0, huf_vals = 0, nseg_dev = 0;
   const uint64_t hdr = payload_only ? 0 : kHeader;
   for (uint32_t c = 0; c < n; ++c) {
     const embc_chunk_ref& r = refs[c];
@@ -2289,6 +2396,21 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
     if (r.codec == EMBC_CODEC_RAW) {
       const uint64_t per = 8192;
       for (uint64_t e = 0; e < C.N; e += per) raw_tiles.push_back(RawTile{c, 0, e, std::min(per, C.N - e)});
+    } else if (r.codec == EMBC_CODEC_VLZ && dev) {
+      // bounds from the capacity; k_dec_plan decides seq / segments
+      if (!(r.dim == 0 || r.dim > kVlzMaxDim || C.N >= (1ull << 31))) {
+        const uint64_t ns = (pay + kSeg - 1) / kSeg;
+        nseg_dev += ns;
+        map_total += ns * (r.dim + 1);
+        C.row_base = row_total;
+        row_total += r.count;
+        const uint32_t per = std::max<uint32_t>(8, std::min<uint32_t>(4096, 8192 / std::max<uint32_t>(r.dim, 1)));
+        for (uint32_t r0 = 0; r0 < r.count; r0 += per) {
+          ctiles.push_back(c);
+          ctiles.push_back(r0);
+          ctiles.push_back(std::min(per, r.count - r0));
+        }
+      }
     } else if (r.codec == EMBC_CODEC_VLZ) {
       C.seq = (r.dim == 0 || r.dim > kVlzMaxDim || C.N >= (1ull << 31) || pay >= (1ull << 31) ||
                (pay == 0 && r.count > 0)) ? 1 : 0;
@@ -2314,21 +2436,36 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
       C.book_cap = static_cast<uint32_t>(std::max<uint64_t>(cap, p2));  // key region must hold p2
       C.tab_off = tab_total;
       tab_total += std::max<uint64_t>(htab_bytes(C.book_cap), 8 * p2 + 16);
-      C.nsub = static_cast<uint32_t>((8 * (pay > 12 ? pay - 12 : 0) + kSubBits - 1) / kSubBits);
-      huf_subs += C.nsub;
+      huf_subs += (8 * (pay > 12 ? pay - 12 : 0) + kSubBits - 1) / kSubBits;
+      huf_vals += C.N;
     }
   }
   // huffman block size: 256 subsequences when there are enough for ~3 blocks per
   // SM slot, else 128 (more, shorter blocks for small calls)
-  const uint32_t hsub = huf_subs >= 256ull * 600 ? 256 : 128;
+  // (large calls: 16384-bit blocks of 256 x 64-bit subsequences; small calls:
+  // 8192-bit blocks of 256 x 32-bit subsequences, with block-local tables)
+  // (device-planned calls: by the number of values, the lengths being unknown)
+  const bool small_call = dev ? huf_vals < (2ull << 20) : huf_subs < 256ull * 600;
+  const uint32_t hsub = 256, sbits = small_call ? 32 : 64;
+  uint64_t nhb_dev = 0;
   for (uint32_t c = 0; c < n; ++c) {
     DChunk& C = ch[c];
     if (C.codec != EMBC_CODEC_HUFFMAN) continue;
+    const uint64_t pay = C.length > hdr ? C.length - hdr : 0;
+    const uint32_t nsub = static_cast<uint32_t>((8 * (pay > 12 ? pay - 12 : 0) + sbits - 1) / sbits);
+    if (dev) {
+      nhb_dev += (nsub + hsub - 1) / hsub;
+      continue;
+    }
+    C.nsub = nsub;
     C.nblk = (C.nsub + hsub - 1) / hsub;
     C.blk0 = static_cast<uint32_t>(hblk.size());
     for (uint32_t k = 0; k < C.nblk; ++k) hblk.push_back(c);
   }
-  const uint32_t nseg = static_cast<uint32_t>(segs.size()), nhb = static_cast<uint32_t>(hblk.size());
+  if (dev && (nseg_dev >= (1ull << 31) || nhb_dev >= (1ull << 31)))
+    return set_error(ctx, EMBC_ERR_UNSUPPORTED, 0, 0, 0, 0, 0, "chunk capacities beyond the device-planned decode");
+  const uint32_t nseg = dev ? static_cast<uint32_t>(nseg_dev) : static_cast<uint32_t>(segs.size());
+  const uint32_t nhb = dev ? static_cast<uint32_t>(nhb_dev) : static_cast<uint32_t>(hblk.size());
   const uint32_t nct = static_cast<uint32_t>(ctiles.size() / 3);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -2351,6 +2488,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   const size_t o_rsrc = take(sizeof(uint32_t) * (row_total + 1));
   const size_t o_tabs = take(tab_total + 16);
   const size_t o_keys = take(tab_total + 16);
+  const size_t o_dcount = take(sizeof(uint32_t) * 4);
   cudaError_t ce = ensure_scratch(ctx, off);
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "scratch allocation");
   uint8_t* hs = nullptr;
@@ -2360,8 +2498,10 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   std::memset(hs, 0, host_bytes);
   std::memcpy(hs + o_ch, ch.data(), sizeof(DChunk) * n);
   std::memcpy(hs + o_raw, raw_tiles.data(), sizeof(RawTile) * raw_tiles.size());
-  std::memcpy(hs + o_segs, segs.data(), sizeof(SegPair) * nseg);
-  std::memcpy(hs + o_hblk, hblk.data(), sizeof(uint32_t) * nhb);
+  if (!dev) {
+    std::memcpy(hs + o_segs, segs.data(), sizeof(SegPair) * nseg);
+    std::memcpy(hs + o_hblk, hblk.data(), sizeof(uint32_t) * nhb);
+  }
   std::memcpy(hs + o_ct, ctiles.data(), sizeof(uint32_t) * ctiles.size());
   uint8_t* d = ctx->d_scratch;
   ce = stage_upload(ctx, d, hs, host_bytes, slot, stream);
@@ -2395,14 +2535,37 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   a.nhblk = nhb;
   a.nraw = static_cast<uint32_t>(raw_tiles.size());
   a.nctile = nct;
-  const uint32_t g1 = n + nseg + nhb + a.nraw + nct + n;
+  uint32_t g1 = n + nseg + nhb + a.nraw + nct + n;
   uint32_t dmax = 1;
   for (uint32_t c = 0; c < n; ++c)
-    if (ch[c].codec == EMBC_CODEC_VLZ && !ch[c].seq) dmax = std::max(dmax, ch[c].dim);
+    if (ch[c].codec == EMBC_CODEC_VLZ && !ch[c].seq && ch[c].dim <= kVlzMaxDim) dmax = std::max(dmax, ch[c].dim);
   a.vlz_dmax = dmax;
   a.hsub = hsub;
-  uint32_t smem = std::max<uint32_t>(std::max<uint32_t>(nseg ? vlz_smem(dmax) : 0, nhb ? huff_smem(hsub) : 0), 16384);
+  a.sbits = sbits;
+  a.local_tables = small_call ? 1 : 0;
+  uint32_t smem = std::max<uint32_t>(std::max<uint32_t>(nseg ? vlz_smem(dmax) : 0, nhb ? huff_smem(hsub, sbits) : 0), 16384);
   a.smem_bytes = smem;
+  if (dev) {
+    PlanArgs pa{};
+    pa.ch = reinterpret_cast<DChunk*>(d + o_ch);
+    pa.d_len = d_len;
+    pa.d_off = d_off;
+    pa.segs = reinterpret_cast<SegPair*>(d + o_segs);
+    pa.hblk_chunk = reinterpret_cast<uint32_t*>(d + o_hblk);
+    pa.dcount = reinterpret_cast<uint32_t*>(d + o_dcount);
+    pa.n = n;
+    pa.hsub = hsub;
+    pa.sbits = sbits;
+    EMBC_TIMED(ctx, "k_dec_plan", stream, k_dec_plan<<<1, 1024, 0, stream>>>(pa));
+    a.dcount = pa.dcount;
+    a.persistent = 1;
+    // persistent CTAs: as many as are resident at once (never more than the roles)
+    int dev_id = 0, nsm = 0, per_sm = 0;
+    cudaGetDevice(&dev_id);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev_id);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dec_main, kBlock, smem);
+    g1 = std::max<uint32_t>(1, std::min<uint32_t>(g1, static_cast<uint32_t>(std::max(1, nsm * per_sm))));
+  }
   EMBC_TIMED(ctx, "k_dec_main", stream, k_dec_main<<<g1, kBlock, smem, stream>>>(a));
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "decode launch");

@@ -72,7 +72,8 @@ struct DChunk {
   uint64_t tab_off;        // byte offset of this chunk's decode tables
   uint32_t nsub;           // 64-bit subsequences of the bitstream
   uint32_t blk0, nblk;     // global index range of this chunk's decode blocks
-  uint32_t pad2;
+  uint8_t bad;             // device-planned calls: the received length exceeds the capacity
+  uint8_t pad2[3];
 };
 
 // Per-chunk decode state (device).
