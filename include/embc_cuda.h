@@ -311,6 +311,23 @@ embc_status embc_exchange_baseline_bwd(embc_exchange* ex, uint32_t ntables, uint
                                        uint32_t batch, const float* const* d_grads,
                                        float* const* d_outs, void* stream);
 
+/* Transport of the exchange: 0 = NCCL (a 25-B metadata round, the byte
+ * counts to the host, a variable-size payload round); 1 = peer-to-peer
+ * windows: each rank's encode kernels write its chunks, lengths and offsets
+ * straight into the destination's CUDA-IPC-shared window over NVLink, a
+ * release flag per (source, destination) follows, and the destination waits
+ * on the flags and decodes with embc_decode_dev -- no metadata round, no host
+ * synchronisation, graph-capturable (the fused exchange of SURVEY.md 8(f)
+ * row 1; the paper's future work).  Stats are filled only when
+ * requested (that read synchronises). */
+embc_status embc_exchange_set_mode(embc_exchange* ex, int mode);
+/* Waits for the exchange's streams; reports a codec failure or a peer that
+ * never signalled (mode 1, ~10 s) with the reference's rank/stage text. */
+embc_status embc_exchange_sync(embc_exchange* ex);
+/* embc_reserve_capture for both of the exchange's codec contexts (before
+ * capturing embc_exchange_fwd / _bwd in a CUDA graph, mode 1). */
+embc_status embc_exchange_reserve_capture(embc_exchange* ex, uint64_t bytes);
+
 /* Per-kernel CUDA-event timing of the exchange's codec launches (both
  * contexts), as embc_timing_enable / embc_timing_collect. */
 embc_status embc_exchange_timing_enable(embc_exchange* ex, int on);

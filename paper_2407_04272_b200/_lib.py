@@ -119,6 +119,7 @@ EXPORTS = [
     "embc_exchange_unique_id", "embc_exchange_create", "embc_exchange_destroy", "embc_exchange_get_error",
     "embc_exchange_fwd", "embc_exchange_bwd", "embc_exchange_baseline_fwd", "embc_exchange_baseline_bwd",
     "embc_unpack", "embc_exchange_timing_enable", "embc_exchange_timing_collect", "embc_simulate", "embc_decode_dev",
+    "embc_exchange_set_mode", "embc_exchange_sync", "embc_exchange_reserve_capture",
 ]
 
 _lock = threading.Lock()
@@ -176,6 +177,9 @@ def lib() -> C.CDLL:
                 "embc_exchange_baseline_fwd": (i32, [vp, u32, u32, u32, vp, vp, vp]),
                 "embc_exchange_baseline_bwd": (i32, [vp, u32, u32, u32, vp, vp, vp]),
                 "embc_exchange_timing_enable": (i32, [vp, i32]),
+                "embc_exchange_set_mode": (i32, [vp, i32]),
+                "embc_exchange_sync": (i32, [vp]),
+                "embc_exchange_reserve_capture": (i32, [vp, u64]),
                 "embc_exchange_timing_collect": (i32, [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_float), i32]),
                 "embc_unpack": (i32, [vp, u64, vp, vp, u32, C.POINTER(u32), C.POINTER(EmbcErrorRec)]),
                 "embc_simulate": (i32, [i32, C.POINTER(SimConfig), C.POINTER(SimTable), u32, vp, vp,

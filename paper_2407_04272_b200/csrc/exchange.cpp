@@ -15,10 +15,18 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
 #include "../../include/embc_cuda.h"
+
+namespace embc_p2p {  // p2p.cu
+cudaError_t bump(uint64_t* ctr, cudaStream_t s);
+cudaError_t signal(uint64_t* const* d_dst, uint32_t n, const uint64_t* ctr, cudaStream_t s);
+cudaError_t wait(const uint64_t* flags, uint32_t n, const uint64_t* ctr, uint64_t minus, uint32_t* timeout,
+                 cudaStream_t s);
+}  // namespace embc_p2p
 
 namespace {
 
@@ -124,9 +132,26 @@ struct RecvChunk {
 
 }  // namespace
 
+// Peer-to-peer mode (embc_exchange_set_mode(ex, 1)): every rank's window,
+// shared with its peers through CUDA IPC.  Layout of a receiver's window for
+// one direction (every rank computes every window's layout from the call's
+// shapes and codecs): data[R] | ack[R] flags (u64), then per source s its
+// chunks' lengths and slot-relative offsets (u64, sources in rank order), then
+// per source a slot holding its chunks (capacity = the chunks' encode bounds).
+struct P2PState {
+  size_t cap = 0;                 // window bytes (same on every rank)
+  uint8_t* win = nullptr;         // this rank's window
+  std::vector<uint8_t*> peer;     // every rank's window as mapped here (peer[rank] = win)
+  uint64_t* d_epoch = nullptr;    // exchange counter, bumped on the device
+  uint32_t* d_timeout = nullptr;  // a flag wait gave up
+  void* d_sig = nullptr;          // device pointer arrays for the signal kernels (2 x R)
+};
+
 struct embc_exchange {
   int device = 0, rank = 0, R = 1;
   uint32_t groups = 1;
+  int mode = 0;  // 0: NCCL metadata + payload rounds; 1: peer-to-peer windows
+  P2PState p2p;
   ncclComm_t comm = nullptr;
   embc_ctx* enc = nullptr;
   embc_ctx* dec = nullptr;
@@ -371,6 +396,273 @@ bool bad_args(embc_exchange* ex, uint32_t T, uint32_t dim, uint32_t batch, const
   return !ex || !T || !dim || !batch || !a || !b || !c || !d;
 }
 
+// ---- peer-to-peer mode ---------------------------------------------------------
+
+// Upper bound on one chunk's serialized bytes (embc_encode_bound of the job).
+uint64_t chunk_cap(uint32_t dim, uint32_t batch, uint8_t codec) {
+  embc_job j{};
+  j.dim = dim;
+  j.n = batch;
+  j.eb = 1.0;
+  j.window = 255;
+  j.codec = codec;
+  return embc_encode_bound(&j, 1, EMBC_LAYOUT_CHUNKS);
+}
+
+// A receiver's window for one direction: tables_of(s, r) lists the tables s
+// sends to r, in s's job order.
+struct Layout {
+  std::vector<uint32_t> nin;     // chunks per source
+  std::vector<uint64_t> pre;     // index of source s's first chunk
+  std::vector<std::vector<uint64_t>> caps;
+  std::vector<uint64_t> slot;    // byte offset of source s's slot
+  std::vector<uint64_t> slot_cap;
+  uint64_t off_lens = 0, off_offs = 0, total = 0;
+};
+
+Layout layout_of(int R, int r, uint32_t dim, uint32_t batch, const uint8_t* codecs,
+                 const std::function<std::vector<uint32_t>(int, int)>& tables_of) {
+  Layout L;
+  L.nin.resize(R);
+  L.pre.resize(R);
+  L.caps.resize(R);
+  L.slot.resize(R);
+  L.slot_cap.resize(R);
+  uint64_t n = 0;
+  for (int s = 0; s < R; ++s) {
+    const auto t = tables_of(s, r);
+    L.nin[s] = static_cast<uint32_t>(t.size());
+    L.pre[s] = n;
+    n += t.size();
+    uint64_t c = 0;
+    for (uint32_t x : t) {
+      L.caps[s].push_back(chunk_cap(dim, batch, codecs[x]));
+      c += L.caps[s].back();
+    }
+    L.slot_cap[s] = c;
+  }
+  L.off_lens = 16ull * R;
+  L.off_offs = L.off_lens + 8 * n;
+  uint64_t o = (L.off_offs + 8 * n + 255) & ~255ull;
+  for (int s = 0; s < R; ++s) {
+    L.slot[s] = o;
+    o = (o + L.slot_cap[s] + 255) & ~255ull;
+  }
+  L.total = o;
+  return L;
+}
+
+// A grouped send/recv of `bytes` from every rank to every rank (setup only).
+embc_status all_to_all_bytes(embc_exchange* ex, const void* d_send, void* d_recv, size_t bytes) {
+  const Nccl& N = nccl();
+  ncclResult_t nr = N.GroupStart();
+  for (int p = 0; p < ex->R && nr == ncclSuccess; ++p) {
+    nr = N.Send(static_cast<const uint8_t*>(d_send), bytes, ncclUint8, p, ex->comm, ex->s_comm);
+    if (nr == ncclSuccess) nr = N.Recv(static_cast<uint8_t*>(d_recv) + bytes * p, bytes, ncclUint8, p, ex->comm, ex->s_comm);
+  }
+  const ncclResult_t ne = N.GroupEnd();
+  if (nr != ncclSuccess) return nccl_fail(ex, nr, "window setup");
+  if (ne != ncclSuccess) return nccl_fail(ex, ne, "window setup");
+  const cudaError_t ce = cudaStreamSynchronize(ex->s_comm);
+  return ce == cudaSuccess ? EMBC_OK : cuda_fail(ex, ce, "window setup");
+}
+
+void p2p_release(embc_exchange* ex) {
+  P2PState& P = ex->p2p;
+  for (int r = 0; r < static_cast<int>(P.peer.size()); ++r)
+    if (r != ex->rank && P.peer[r]) cudaIpcCloseMemHandle(P.peer[r]);
+  P.peer.clear();
+  if (P.win) cudaFree(P.win);
+  P.win = nullptr;
+  P.cap = 0;
+}
+
+// Every rank's window of at least `need` bytes (collective: every rank makes
+// the same calls, so all grow together), mapped on every peer.
+embc_status p2p_window(embc_exchange* ex, uint64_t need) {
+  P2PState& P = ex->p2p;
+  cudaError_t ce;
+  if (!P.d_epoch) {
+    void* p = nullptr;
+    if ((ce = cudaMalloc(&p, 16)) != cudaSuccess) return cuda_fail(ex, ce, "window setup");
+    cudaMemset(p, 0, 16);
+    P.d_epoch = static_cast<uint64_t*>(p);
+    P.d_timeout = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(p) + 8);
+    if ((ce = cudaMalloc(&P.d_sig, sizeof(void*) * 2 * ex->R)) != cudaSuccess) return cuda_fail(ex, ce, "window setup");
+  }
+  if (need <= P.cap) return EMBC_OK;
+  // peers may still read the old windows: drain every stream, then a round trip
+  cudaDeviceSynchronize();
+  DevBuf tok;
+  if ((ce = tok.reserve(16ull * ex->R)) != cudaSuccess) return cuda_fail(ex, ce, "window setup");
+  embc_status st = all_to_all_bytes(ex, tok.p, tok.as<uint8_t>() + 8ull * ex->R, 8);
+  if (st != EMBC_OK) return st;
+  p2p_release(ex);
+  const uint64_t cap = std::max<uint64_t>(need + need / 4, 1 << 20);
+  if ((ce = cudaMalloc(&P.win, cap)) != cudaSuccess) return cuda_fail(ex, ce, "window allocation");
+  // flags start at 0 (epoch 0 never signalled), so a fresh window waits correctly
+  if ((ce = cudaMemset(P.win, 0, 16ull * ex->R)) != cudaSuccess) return cuda_fail(ex, ce, "window setup");
+  P.cap = cap;
+  P.peer.assign(ex->R, nullptr);
+  P.peer[ex->rank] = P.win;
+  if (ex->R > 1) {
+    cudaIpcMemHandle_t h;
+    if ((ce = cudaIpcGetMemHandle(&h, P.win)) != cudaSuccess) return cuda_fail(ex, ce, "window handle");
+    DevBuf hb;
+    if ((ce = hb.reserve(sizeof(h) * (ex->R + 1))) != cudaSuccess) return cuda_fail(ex, ce, "window setup");
+    cudaMemcpy(hb.p, &h, sizeof(h), cudaMemcpyHostToDevice);
+    st = all_to_all_bytes(ex, hb.p, hb.as<uint8_t>() + sizeof(h), sizeof(h));
+    if (st != EMBC_OK) return st;
+    std::vector<cudaIpcMemHandle_t> all(ex->R);
+    cudaMemcpy(all.data(), hb.as<uint8_t>() + sizeof(h), sizeof(h) * ex->R, cudaMemcpyDeviceToHost);
+    for (int r = 0; r < ex->R; ++r) {
+      if (r == ex->rank) continue;
+      void* p = nullptr;
+      if ((ce = cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess)) != cudaSuccess)
+        return cuda_fail(ex, ce, "peer window mapping");
+      P.peer[r] = static_cast<uint8_t*>(p);
+    }
+  }
+  // pointer tables of the signal kernels: data[me] in every destination's
+  // window, ack[me] in every source's window
+  std::vector<uint64_t*> sig(2 * ex->R);
+  for (int r = 0; r < ex->R; ++r) {
+    sig[r] = reinterpret_cast<uint64_t*>(P.peer[r]) + ex->rank;
+    sig[ex->R + r] = reinterpret_cast<uint64_t*>(P.peer[r]) + ex->R + ex->rank;
+  }
+  cudaMemcpy(P.d_sig, sig.data(), sizeof(void*) * sig.size(), cudaMemcpyHostToDevice);
+  // every rank mapped every window before anyone writes into one
+  return all_to_all_bytes(ex, tok.p, tok.as<uint8_t>() + 8ull * ex->R, 8);
+}
+
+// One direction over the windows: this rank's chunks for destination d go
+// straight into d's window (its own encode kernels store over NVLink), then
+// a flag per destination; the receive side waits for every source's flag and
+// decodes from its own window with the device-planned decoder (lengths never
+// visit the host), then acknowledges.  No host synchronisation unless
+// `stats` is requested.
+embc_status run_p2p(embc_exchange* ex, uint32_t T, uint32_t dim, uint32_t batch, const double* ebs,
+                    const uint8_t* codecs, uint32_t window,
+                    const std::function<std::vector<uint32_t>(int, int)>& tables_of,
+                    const std::function<const float*(uint32_t, int)>& src_of,
+                    const std::function<float*(uint32_t, int)>& out_of, embc_exchange_stats* stats,
+                    cudaStream_t stream, const char* dir) {
+  const int R = ex->R, me = ex->rank;
+  std::vector<Layout> L(R);
+  uint64_t need = 0;
+  for (int r = 0; r < R; ++r) {
+    L[r] = layout_of(R, r, dim, batch, codecs, tables_of);
+    need = std::max(need, L[r].total);
+  }
+  (void)T;
+  embc_status st = p2p_window(ex, need);
+  if (st != EMBC_OK) return st;
+  P2PState& P = ex->p2p;
+  auto* sig = static_cast<uint64_t* const*>(P.d_sig);
+  cudaError_t ce = embc_p2p::bump(P.d_epoch, stream);
+  if (ce == cudaSuccess) ce = cudaEventRecord(ex->ev_in, stream);
+  if (ce == cudaSuccess) ce = cudaStreamWaitEvent(ex->s_enc, ex->ev_in, 0);
+  if (ce == cudaSuccess) ce = cudaStreamWaitEvent(ex->s_dec, ex->ev_in, 0);
+  // send side: every destination has decoded what this rank wrote last time
+  if (ce == cudaSuccess)
+    ce = embc_p2p::wait(reinterpret_cast<const uint64_t*>(P.win) + R, R, P.d_epoch, 1, P.d_timeout, ex->s_enc);
+  if (ce != cudaSuccess) return cuda_fail(ex, ce, "p2p send setup");
+  embc_status first = EMBC_OK;
+  embc_exchange_stats stt{};
+  const uint64_t chunk_values = static_cast<uint64_t>(batch) * dim;
+  for (int d = 0; d < R; ++d) {
+    const auto tabs = tables_of(me, d);
+    if (tabs.empty()) continue;
+    const Layout& Ld = L[d];
+    std::vector<embc_job> cj(tabs.size());
+    for (size_t j = 0; j < tabs.size(); ++j) {
+      embc_job& c = cj[j];
+      std::memset(&c, 0, sizeof(c));
+      c.src = src_of(tabs[j], d);
+      c.dim = dim;
+      c.n = batch;
+      c.eb = ebs[tabs[j]];
+      c.window = window;
+      c.codec = codecs[tabs[j]];
+      c.src_kind = EMBC_SRC_F32;
+    }
+    uint8_t* w = P.peer[d];
+    uint64_t* lens = reinterpret_cast<uint64_t*>(w + Ld.off_lens) + Ld.pre[me];
+    uint64_t* offs = reinterpret_cast<uint64_t*>(w + Ld.off_offs) + Ld.pre[me];
+    const embc_status s = embc_encode(ex->enc, cj.data(), static_cast<uint32_t>(cj.size()), EMBC_LAYOUT_CHUNKS,
+                                      w + Ld.slot[me], Ld.slot_cap[me], offs, lens, nullptr, nullptr, ex->s_enc);
+    if (s != EMBC_OK && first == EMBC_OK) first = codec_fail(ex, ex->enc, s, std::string(dir) + " compress stage");
+  }
+  if ((ce = embc_p2p::signal(sig, R, P.d_epoch, ex->s_enc)) != cudaSuccess) return cuda_fail(ex, ce, "p2p signal");
+  Group& gr = ex->g[0];
+  if ((ce = cudaEventRecord(gr.encoded, ex->s_enc)) != cudaSuccess) return cuda_fail(ex, ce, "event");
+  // receive side: this rank's own slot comes from its encode stream (an event
+  // dependency, so no wait relies on concurrent kernels); peers' by their flags
+  if ((ce = cudaStreamWaitEvent(ex->s_dec, gr.encoded, 0)) != cudaSuccess ||
+      (ce = embc_p2p::wait(reinterpret_cast<const uint64_t*>(P.win), R, P.d_epoch, 0, P.d_timeout, ex->s_dec)) !=
+          cudaSuccess)
+    return cuda_fail(ex, ce, "p2p receive setup");
+  const Layout& Lm = L[me];
+  std::vector<embc_chunk_ref> refs;
+  for (int s = 0; s < R; ++s) {
+    const auto tabs = tables_of(s, me);
+    for (size_t k = 0; k < tabs.size(); ++k) {
+      embc_chunk_ref r{};
+      r.offset = Lm.slot[s];
+      r.length = Lm.caps[s][k];
+      r.out = out_of(tabs[k], s);
+      r.dim = dim;
+      r.count = batch;
+      r.codec = codecs[tabs[k]];
+      refs.push_back(r);
+    }
+  }
+  if (!refs.empty()) {
+    const embc_status s = embc_decode_dev(ex->dec, P.win, refs.data(), static_cast<uint32_t>(refs.size()),
+                                          reinterpret_cast<const uint64_t*>(P.win + Lm.off_offs),
+                                          reinterpret_cast<const uint64_t*>(P.win + Lm.off_lens), EMBC_OUT_F32, 0,
+                                          ex->s_dec);
+    if (s != EMBC_OK && first == EMBC_OK) first = codec_fail(ex, ex->dec, s, std::string(dir) + " decompress stage");
+  }
+  if ((ce = embc_p2p::signal(sig + R, R, P.d_epoch, ex->s_dec)) != cudaSuccess) return cuda_fail(ex, ce, "p2p ack");
+  if ((ce = cudaEventRecord(ex->ev_out, ex->s_dec)) != cudaSuccess ||
+      (ce = cudaStreamWaitEvent(stream, ex->ev_out, 0)) != cudaSuccess ||
+      (ce = cudaStreamWaitEvent(stream, gr.encoded, 0)) != cudaSuccess)
+    return cuda_fail(ex, ce, "stream join");
+  if (first != EMBC_OK) return first;
+  if (!stats) return EMBC_OK;  // asynchronous (and graph-capturable): failures at embc_exchange_sync
+  // accounting (commsim.hpp:322-353): this rank's chunk lengths as its peers received them
+  st = embc_exchange_sync(ex);
+  if (st != EMBC_OK) return st;
+  for (int d = 0; d < R; ++d) {
+    const uint32_t n = L[d].nin[me];
+    if (!n) continue;
+    std::vector<uint64_t> lens(n);
+    cudaMemcpy(lens.data(), reinterpret_cast<uint64_t*>(P.peer[d] + L[d].off_lens) + L[d].pre[me], 8 * n,
+               cudaMemcpyDeviceToHost);
+    for (uint64_t l : lens) {
+      stt.sent_values += chunk_values;
+      stt.sent_bytes += l;
+      if (d != me) {
+        stt.payload_bytes += l;
+        stt.metadata_bytes += kMeta;
+        stt.uncompressed_bytes += 4 * chunk_values;
+      }
+    }
+  }
+  {
+    std::vector<uint64_t> lens(refs.size());
+    if (!refs.empty())
+      cudaMemcpy(lens.data(), P.win + Lm.off_lens, 8 * refs.size(), cudaMemcpyDeviceToHost);
+    for (uint64_t l : lens) {
+      stt.recv_values += chunk_values;
+      stt.recv_bytes += l;
+    }
+  }
+  *stats = stt;
+  return EMBC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -430,6 +722,9 @@ void embc_exchange_destroy(embc_exchange* ex) {
     if (gr.arrived) cudaEventDestroy(gr.arrived);
   }
   ex->g.clear();
+  p2p_release(ex);
+  if (ex->p2p.d_epoch) cudaFree(ex->p2p.d_epoch);
+  if (ex->p2p.d_sig) cudaFree(ex->p2p.d_sig);
   if (ex->comm) nccl().CommDestroy(ex->comm);
   if (ex->enc) embc_ctx_destroy(ex->enc);
   if (ex->dec) embc_ctx_destroy(ex->dec);
@@ -457,6 +752,13 @@ embc_status embc_exchange_fwd(embc_exchange* ex, uint32_t T, uint32_t dim, uint3
   if (st != EMBC_OK) return st;
   const auto own = owned(T, R, ex->rank);
   const uint64_t rows = static_cast<uint64_t>(batch) * dim;
+  if (ex->mode == 1) {
+    cudaSetDevice(ex->device);
+    return run_p2p(
+        ex, T, dim, batch, ebs, codecs, window, [&](int s, int) { return owned(T, R, s); },
+        [&](uint32_t t, int d) { return d_lookups[t] + d * rows; }, [&](uint32_t t, int) { return d_outs[t]; },
+        stats, static_cast<cudaStream_t>(stream), "forward");
+  }
   std::vector<std::vector<SendJob>> jobs(G);
   std::vector<std::vector<std::vector<RecvChunk>>> recv(G, std::vector<std::vector<RecvChunk>>(R));
   for (size_t k = 0; k < G; ++k) {
@@ -485,6 +787,13 @@ embc_status embc_exchange_bwd(embc_exchange* ex, uint32_t T, uint32_t dim, uint3
   if (st != EMBC_OK) return st;
   const auto own = owned(T, R, ex->rank);
   const uint64_t rows = static_cast<uint64_t>(batch) * dim;
+  if (ex->mode == 1) {
+    cudaSetDevice(ex->device);
+    return run_p2p(
+        ex, T, dim, batch, ebs, codecs, window, [&](int, int r) { return owned(T, R, r); },
+        [&](uint32_t t, int) { return d_grads[t]; }, [&](uint32_t t, int s) { return d_outs[t] + s * rows; }, stats,
+        static_cast<cudaStream_t>(stream), "backward");
+  }
   std::vector<std::vector<SendJob>> jobs(G);
   std::vector<std::vector<std::vector<RecvChunk>>> recv(G, std::vector<std::vector<RecvChunk>>(R));
   for (size_t k = 0; k < G; ++k) {
@@ -546,6 +855,36 @@ embc_status embc_exchange_baseline_bwd(embc_exchange* ex, uint32_t T, uint32_t d
     for (uint32_t t : owned(T, ex->R, ex->rank)) from[p].push_back(d_outs[t] + p * rows);
   }
   return baseline(ex, to, from, rows, static_cast<cudaStream_t>(stream));
+}
+
+embc_status embc_exchange_set_mode(embc_exchange* ex, int mode) {
+  if (!ex || mode < 0 || mode > 1) return EMBC_ERR_ARGUMENT;
+  ex->mode = mode;
+  return EMBC_OK;
+}
+
+embc_status embc_exchange_reserve_capture(embc_exchange* ex, uint64_t bytes) {
+  if (!ex) return EMBC_ERR_ARGUMENT;
+  const embc_status a = embc_reserve_capture(ex->enc, bytes);
+  return a != EMBC_OK ? a : embc_reserve_capture(ex->dec, bytes);
+}
+
+embc_status embc_exchange_sync(embc_exchange* ex) {
+  if (!ex) return EMBC_ERR_ARGUMENT;
+  cudaSetDevice(ex->device);
+  const embc_status se = embc_sync(ex->enc, ex->s_enc);
+  const embc_status sd = embc_sync(ex->dec, ex->s_dec);
+  if (ex->p2p.d_timeout) {
+    uint32_t t = 0;
+    cudaMemcpy(&t, ex->p2p.d_timeout, 4, cudaMemcpyDeviceToHost);
+    if (t) {
+      cudaMemset(ex->p2p.d_timeout, 0, 4);
+      return fail(ex, EMBC_ERR_NCCL, 0, "rank " + std::to_string(ex->rank) + ": a peer did not signal its window");
+    }
+  }
+  if (se != EMBC_OK) return codec_fail(ex, ex->enc, se, "compress stage");
+  if (sd != EMBC_OK) return codec_fail(ex, ex->dec, sd, "decompress stage");
+  return EMBC_OK;
 }
 
 embc_status embc_exchange_timing_enable(embc_exchange* ex, int on) {

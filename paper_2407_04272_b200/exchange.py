@@ -489,7 +489,10 @@ class NcclExchange:
     def __init__(self, ntables: int, dim: int, batch: int, profiles: Dict[int, P.TableProfile],
                  cfg: P.PolicyConfig, group=None, device=None, window: int = 255,
                  grad_profiles: Optional[Dict[int, P.TableProfile]] = None,
-                 grad_cfg: Optional[P.PolicyConfig] = None, groups: int = 1):
+                 grad_cfg: Optional[P.PolicyConfig] = None, groups: int = 1, p2p: bool = False):
+        """p2p: the peer-to-peer transport (embc_exchange_set_mode 1): chunks
+        written straight into the destination's IPC-shared window, flags
+        instead of the metadata round, no host synchronisation."""
         import ctypes as C
         from . import _lib
         self._C, self._lib = C, _lib
@@ -519,6 +522,9 @@ class NcclExchange:
         if st != _lib.OK:
             raise _lib.EmbcError(f"embc_exchange_create failed with status {st}", status=st)
         self.handle = h
+        self.p2p = p2p
+        if p2p:
+            self._check(self.L.embc_exchange_set_mode(h, 1))
 
     def __del__(self):
         try:
@@ -561,29 +567,42 @@ class NcclExchange:
                              s.recv_values, s.recv_bytes)
 
     def forward(self, iteration: int, lookups: Dict[int, torch.Tensor],
-                out: Optional[Dict[int, torch.Tensor]] = None) -> Dict[int, torch.Tensor]:
+                out: Optional[Dict[int, torch.Tensor]] = None, stats: bool = True) -> Dict[int, torch.Tensor]:
         """lookups[t] for owned t: [R*B, dim].  Returns {t: [B, dim]} for every
         table, decoded into `out` when given."""
         if out is None:
             out = {t: torch.empty((self.B, self.dim), dtype=torch.float32, device=self.device) for t in range(self.T)}
         ebs, codecs = self._policy(iteration, self.profiles, self.cfg)
         st = self._lib.ExchangeStats()
+        # p2p without stats: asynchronous and graph-capturable (failures at sync())
+        sp = self._C.byref(st) if (stats or not self.p2p) else None
         self._check(self.L.embc_exchange_fwd(self.handle, self.T, self.dim, self.B, self._ptrs(lookups), ebs, codecs,
-                                             self.window, self._ptrs(out), self._C.byref(st),
+                                             self.window, self._ptrs(out), sp,
                                              torch.cuda.current_stream(self.device).cuda_stream))
-        self.stats = self._stats(st)
+        if sp is not None:
+            self.stats = self._stats(st)
         return out
 
-    def backward(self, iteration: int, grads: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:
+    def sync(self) -> None:
+        """Waits for the exchange; raises a codec failure or a silent peer."""
+        self._check(self.L.embc_exchange_sync(self.handle))
+
+    def reserve_capture(self, nbytes: int) -> None:
+        """Descriptor staging for CUDA-graph capture of the exchange's codec calls."""
+        self._check(self.L.embc_exchange_reserve_capture(self.handle, nbytes))
+
+    def backward(self, iteration: int, grads: Dict[int, torch.Tensor], stats: bool = True) -> Dict[int, torch.Tensor]:
         """grads[t] for every table: [B, dim].  Returns {t: [R*B, dim]} for owned tables."""
         own = self.owned(self.rank)
         out = {t: torch.empty((self.R * self.B, self.dim), dtype=torch.float32, device=self.device) for t in own}
         ebs, codecs = self._policy(iteration, self.grad_profiles, self.grad_cfg)
         st = self._lib.ExchangeStats()
+        sp = self._C.byref(st) if (stats or not self.p2p) else None
         self._check(self.L.embc_exchange_bwd(self.handle, self.T, self.dim, self.B, self._ptrs(grads), ebs, codecs,
-                                             self.window, self._ptrs(out), self._C.byref(st),
+                                             self.window, self._ptrs(out), sp,
                                              torch.cuda.current_stream(self.device).cuda_stream))
-        self.stats = self._stats(st)
+        if sp is not None:
+            self.stats = self._stats(st)
         return out
 
     def uncompressed(self, lookups: Dict[int, torch.Tensor]) -> Dict[int, torch.Tensor]:

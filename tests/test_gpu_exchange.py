@@ -102,3 +102,69 @@ def test_nccl_exchange_reports_codec_failure(ctx):
     look[1][5, 3] = 0.0
     out = nx.forward(0, look)
     assert all(torch.equal(out[t], look[t]) for t in range(T))
+
+
+def test_p2p_exchange_single_rank(ctx):
+    """The peer-to-peer transport (chunks written into the destination's
+    window, flags, device-planned decode) delivers byte for byte what the NCCL
+    two-round exchange delivers, with the same accounting, forward and
+    backward, over several iterations of a decaying bound (a one-rank loopback:
+    the window is this rank's own)."""
+    dev = torch.device("cuda", 0)
+    T, dim, B = 9, 16, 1024
+    specs = W.preset_tables(W.KAGGLE_TABLES, T, dim)
+    tables = [W.Table(s, dev) for s in specs]
+    profiles = {t: P.TableProfile(t, codec=t % 3, eb=0.01 + 0.02 * (t % 2)) for t in range(T)}
+    cfg = P.PolicyConfig(global_eb=0.01, decay=P.DecayConfig("stepwise", 2.0, 4, 4))
+    gprof = {t: P.TableProfile(t, codec=2 - t % 2, eb=1e-4) for t in range(T)}
+    gcfg = P.PolicyConfig(global_eb=1e-4)
+    nx = X.NcclExchange(T, dim, B, profiles, cfg, device=dev, grad_profiles=gprof, grad_cfg=gcfg)
+    px = X.NcclExchange(T, dim, B, profiles, cfg, device=dev, grad_profiles=gprof, grad_cfg=gcfg, p2p=True)
+    for it in (0, 1, 3, 6):
+        look = {t: tables[t].lookup_batch(B, W.lookup_stream(it, t, 0, 1)) for t in range(T)}
+        a = nx.forward(it, look)
+        b = px.forward(it, look)
+        assert vars(nx.stats) == vars(px.stats)
+        for t in range(T):
+            assert torch.equal(a[t], b[t]), (it, t)
+        g = {t: (torch.randn((B, dim), device=dev, generator=torch.Generator(dev).manual_seed(it * 7 + t)) * 1e-3)
+             for t in range(T)}
+        ga = nx.backward(it, g)
+        gb = px.backward(it, g)
+        assert vars(nx.stats) == vars(px.stats)
+        for t in range(T):
+            assert torch.equal(ga[t], gb[t]), ("bwd", it, t)
+
+
+def test_p2p_exchange_cuda_graph(ctx):
+    """The peer-to-peer forward is graph-capturable (no host read of the
+    lengths): one capture, replays with other iterations' lookups (other chunk
+    lengths) deliver what the eager two-round exchange delivers."""
+    dev = torch.device("cuda", 0)
+    T, dim, B = 7, 16, 2048
+    specs = W.preset_tables(W.KAGGLE_TABLES, T, dim)
+    tables = [W.Table(s, dev) for s in specs]
+    profiles = {t: P.TableProfile(t, codec=1 + t % 2, eb=0.02) for t in range(T)}
+    cfg = P.PolicyConfig(global_eb=0.02)
+    nx = X.NcclExchange(T, dim, B, profiles, cfg, device=dev)
+    px = X.NcclExchange(T, dim, B, profiles, cfg, device=dev, p2p=True)
+    look = {t: tables[t].lookup_batch(B, W.lookup_stream(0, t, 0, 1)).clone() for t in range(T)}
+    out = {t: torch.empty((B, dim), device=dev) for t in range(T)}
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        px.forward(0, look, out=out, stats=False)  # warm-up: windows and scratch sized
+    s.synchronize()
+    px.sync()
+    px.reserve_capture(64 << 20)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        px.forward(0, look, out=out, stats=False)
+    for it in (1, 2, 3):
+        for t in range(T):
+            look[t].copy_(tables[t].lookup_batch(B, W.lookup_stream(it, t, 0, 1)))
+        g.replay()
+        torch.cuda.synchronize()
+        px.sync()
+        want = nx.forward(0, look)
+        for t in range(T):
+            assert torch.equal(out[t], want[t]), (it, t)
