@@ -277,10 +277,11 @@ int cmd_analyze(const std::string& config, std::optional<uint64_t> seed_flag, st
   const uint64_t seed = seed_flag ? *seed_flag : kv.u64("seed", 1);
   const double bw = bw_flag.value_or(kv.f64("bandwidth", 4e9));
   const uint32_t batch = static_cast<uint32_t>(kv.u64("batch", 128));
+  const auto tables = seeded(kv, seed);
   Context ctx(0);
   std::vector<std::unique_ptr<DevSample>> ds;
   std::vector<Sample> samples;
-  for (const auto& t : seeded(kv, seed)) {
+  for (const auto& t : tables) {
     ds.push_back(std::make_unique<DevSample>(t, lookup_batch(t, batch, 0)));
     samples.push_back(ds.back()->s);
   }
@@ -414,6 +415,7 @@ int cmd_bench(const std::string& config, std::optional<uint64_t> seed_flag, std:
   const uint64_t seed = seed_flag ? *seed_flag : kv.u64("seed", 1);
   const double bw = bw_flag.value_or(kv.f64("bandwidth", 4e9));
   const uint32_t batch = static_cast<uint32_t>(kv.u64("batch", 128));
+  const auto tables = seeded(kv, seed);
   std::ostream* out = &std::cout;
   std::ofstream file;
   if (!csv_out.empty()) {
@@ -424,7 +426,7 @@ int cmd_bench(const std::string& config, std::optional<uint64_t> seed_flag, std:
   Csv csv(*out, "embc.bench.v1", {"table_id", "codec", "eb", "compression_ratio", "comp_bps", "decomp_bps", "est_speedup"});
   Context ctx(0);
   const Codec cands[3] = {Codec::raw, Codec::vlz, Codec::huffman};
-  for (const auto& t : seeded(kv, seed)) {
+  for (const auto& t : tables) {
     DevSample s(t, lookup_batch(t, batch, 0));
     std::vector<ThroughputSample> m;
     select_codec(ctx, s.s, policy.global_eb, cands, bw, window, true, &m);

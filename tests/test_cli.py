@@ -1,0 +1,239 @@
+"""embc_gpu, the reference CLI's commands over the GPU codec (cli_test.cc
+shapes).  CPU: usage, argument and config errors, report.  GPU: compress /
+decompress byte-for-byte against the reference (oracle/_ref), simulate's
+report digest against the reference Simulator, analyze / bench CSV schemas,
+dumped batches."""
+import os
+import struct
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "paper_2407_04272_b200", "embc_gpu")
+
+SIM_CFG = """# small simulation preset (own numbers)
+seed = 5
+ranks = 3
+bandwidth = 1e8
+latency = 0
+iterations = 4
+batch = 256
+compression = on
+policy.global_eb = 0.02
+policy.decay.function = stepwise
+policy.decay.start_scale = 2.0
+policy.decay.end = 2
+policy.decay.steps = 2
+tables.count = 3
+table.0.rows = 48
+table.0.dim = 8
+table.0.dist = gaussian
+table.0.sigma = 0.08
+table.0.zipf = 1.3
+table.1.rows = 300
+table.1.dim = 8
+table.1.dist = gaussian
+table.1.sigma = 0.01
+table.1.zipf = 1.1
+table.2.rows = 2000
+table.2.dim = 8
+table.2.dist = uniform
+table.2.lo = -0.1
+table.2.hi = 0.1
+"""
+
+
+def run(*args, check=None):
+    r = subprocess.run([CLI, *args], capture_output=True, text=True, timeout=300)
+    if check is not None:
+        assert r.returncode == check, (r.returncode, r.stdout, r.stderr)
+    return r
+
+
+def write_values(path, x):
+    n, dim = x.shape
+    with open(path, "wb") as f:
+        f.write(b"EMBV" + bytes([1]) + struct.pack("<II", dim, n) + x.astype("<f8").tobytes())
+
+
+def read_values(path):
+    d = open(path, "rb").read()
+    assert d[:5] == b"EMBV\x01"
+    dim, n = struct.unpack_from("<II", d, 5)
+    return np.frombuffer(d[13:], "<f8").reshape(n, dim)
+
+
+def read_csv(path):
+    schema, rows = None, []
+    for line in open(path):
+        line = line.rstrip("\n")
+        if line.startswith("# schema: "):
+            schema = line[10:]
+        elif line and not line.startswith("#"):
+            rows.append(line.split(","))
+    return schema, rows[0], rows[1:]
+
+
+def test_usage_and_unknown_commands():
+    assert run("--help", check=0).stdout.startswith("embc_gpu")
+    r = run("frobnicate", check=2)
+    assert "embc: unknown command 'frobnicate'" in r.stderr
+    r = run("compress", "--nope", "1", check=2)
+    assert "unknown option --nope" in r.stderr
+
+
+def test_simulate_requires_seed(tmp_path):
+    cfg = tmp_path / "s.cfg"
+    cfg.write_text(SIM_CFG)
+    r = run("simulate", "--config", str(cfg), check=2)
+    assert "--seed" in r.stderr
+
+
+def test_config_errors(tmp_path):
+    bad = tmp_path / "bad.cfg"
+    bad.write_text("seed = 1\nthis line has no equals\n")
+    r = run("simulate", "--config", str(bad), "--seed", "1", check=2)
+    assert f"{bad}:2: expected 'key = value'" in r.stderr
+    missing = tmp_path / "missing.cfg"
+    missing.write_text("seed = 1\n")
+    r = run("bench", "--config", str(missing), check=2)
+    assert "missing config key 'tables.count'" in r.stderr
+    cfg = tmp_path / "s.cfg"
+    cfg.write_text(SIM_CFG)
+    r = run("simulate", "--config", str(cfg), "--seed", "1", "--ranks", "1", check=2)
+    assert "simulation needs at least 2 ranks" in r.stderr
+    r = run("simulate", "--config", str(cfg), "--seed", "1", "--compression", "maybe", check=2)
+    assert "--compression expects on|off" in r.stderr
+
+
+def test_value_file_errors(tmp_path):
+    p = tmp_path / "v.embv"
+    p.write_bytes(b"EMBX\x01" + b"\0" * 8)
+    r = run("compress", "--in", str(p), "--out", str(tmp_path / "c"), "--eb", "0.01", check=2)
+    assert "bad value file magic" in r.stderr
+    p.write_bytes(b"EMBV\x01" + struct.pack("<II", 4, 3) + b"\0" * 16)
+    r = run("compress", "--in", str(p), "--out", str(tmp_path / "c"), "--eb", "0.01", check=2)
+    assert "value file holds 2 values, header claims 12" in r.stderr
+
+
+def test_report_summarizes_csv(tmp_path):
+    p = tmp_path / "b.csv"
+    p.write_text("# schema: embc.bench.v1\ntable_id,codec,compression_ratio\n0,raw,1\n0,vlz,3\n")
+    r = run("report", str(p), check=0)
+    assert "embc.bench.v1" in r.stdout and "mean 2" in r.stdout
+
+
+# ---- GPU ------------------------------------------------------------------------
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("codec", ["raw", "vlz", "huffman"])
+def test_compress_decompress_equal_reference(ref, tmp_path, codec):
+    from paper_2407_04272_b200 import workload as W
+    spec = W.TableSpec(5000, 16, 0, 0.0, 0.05, 0, 1, 1.2, 99)
+    x = W.gen_table(spec)[W.lookup_indices(spec, 1024, 3)].astype(np.float64)
+    x[7, 3] = 0.123456789012345  # a double that is not an fp32 value
+    vin, chunk, vout = tmp_path / "x.embv", tmp_path / "x.embc", tmp_path / "y.embv"
+    write_values(vin, x)
+    r = run("compress", "--in", str(vin), "--out", str(chunk), "--eb", "0.004", "--codec", codec, check=0)
+    assert r.stdout.startswith(f"codec {codec}, 1024 x 16 values, ratio ")
+    want = ref.encode_chunk(x, 16, 0.004, {"raw": 0, "vlz": 1, "huffman": 2}[codec])
+    assert chunk.read_bytes() == want
+    run("decompress", "--in", str(chunk), "--out", str(vout), check=0)
+    y = read_values(vout)
+    assert np.array_equal(y.view(np.uint64), ref.decode_chunk(want).reshape(1024, 16).view(np.uint64))
+    assert np.abs(y - x).max() <= 0.004
+
+
+@pytest.mark.gpu
+def test_compress_auto_picks_vlz_for_repeats(tmp_path):
+    x = np.tile(np.linspace(-0.2, 0.2, 8, dtype=np.float32).astype(np.float64), (512, 1))
+    vin = tmp_path / "r.embv"
+    write_values(vin, x)
+    r = run("compress", "--in", str(vin), "--out", str(tmp_path / "r.embc"), "--eb", "0.01", check=0)
+    assert "codec vlz" in r.stdout
+
+
+@pytest.mark.gpu
+def test_decompress_rejects_corrupt_chunk(tmp_path):
+    p = tmp_path / "bad.embc"
+    p.write_bytes(b"EMBC\x01\x01" + b"\0" * 30)
+    r = run("decompress", "--in", str(p), "--out", str(tmp_path / "o"), check=2)
+    assert r.stderr.startswith("embc:")
+
+
+@pytest.mark.gpu
+def test_simulate_report_digest_equals_reference(ref, tmp_path):
+    """With fixed profiles, the per-iteration CSV bytes/errors and the report
+    digest are the reference Simulator's (run through oracle/_ref)."""
+    import ctypes as C
+    cfg = tmp_path / "s.cfg"
+    cfg.write_text(SIM_CFG)
+    prof = tmp_path / "p.cfg"
+    codecs, ebs = [1, 2, 1], [0.03, 0.01, 0.02]
+    lines = ["profiles.count = 3"]
+    for r_ in range(3):
+        lines += [f"profile.{r_}.table = {r_}", f"profile.{r_}.n_original = 1", f"profile.{r_}.n_quantized = 1",
+                  f"profile.{r_}.survival = 1", f"profile.{r_}.homo = 0", f"profile.{r_}.class = medium",
+                  f"profile.{r_}.codec = {['raw', 'vlz', 'huffman'][codecs[r_]]}", f"profile.{r_}.eb = {ebs[r_]}"]
+    prof.write_text("\n".join(lines) + "\n")
+    out = tmp_path / "sim.csv"
+    r = run("simulate", "--config", str(cfg), "--seed", "11", "--profiles", str(prof), "--out", str(out), check=0)
+    digest = int(r.stdout.split("report digest:")[1].split()[0])
+    schema, header, rows = read_csv(out)
+    assert schema == "embc.simulate.v1"
+    assert header[:6] == ["iteration", "eb_max", "uncompressed_bytes", "payload_bytes", "metadata_bytes", "wire_bytes"]
+    n = 4
+    arr = {k: np.zeros(n, np.uint64) for k in ("unc", "pay", "meta", "dig")}
+    maxerr = np.zeros(n)
+    rows_ = np.array([48, 300, 2000], np.uint32)
+    dims = np.array([8, 8, 8], np.uint32)
+    dist = np.array([0, 0, 1], np.int32)
+    mu = np.zeros(3)
+    sig = np.array([0.08, 0.01, 0.1])
+    lo = np.array([0.0, 0.0, -0.1])
+    hi = np.array([1.0, 1.0, 0.1])
+    zf = np.array([1.3, 1.1, 0.0])
+    pc = np.array(codecs, np.uint8)
+    pe = np.array(ebs)
+    rep = C.c_uint64()
+    err = C.create_string_buffer(512)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    rc = ref.L.ref_simulate(3, 256, n, 11, 1, 0.02, 2.0, 2, 2, p(rows_), p(dims), p(dist), p(mu), p(sig), p(lo), p(hi),
+                            p(zf), 3, p(pc), p(pe), p(arr["unc"]), p(arr["pay"]), p(arr["meta"]), p(maxerr),
+                            p(arr["dig"]), C.byref(rep), err, 512)
+    assert rc == 0, err.value
+    for i, row in enumerate(rows):
+        assert int(row[2]) == arr["unc"][i] and int(row[3]) == arr["pay"][i] and int(row[4]) == arr["meta"][i]
+    assert digest == rep.value
+    # compression off: exact delivery, more wire bytes
+    off = tmp_path / "off.csv"
+    run("simulate", "--config", str(cfg), "--seed", "11", "--profiles", str(prof), "--out", str(off),
+        "--compression", "off", check=0)
+    _, _, off_rows = read_csv(off)
+    assert all(float(r_[11]) == 0.0 for r_ in off_rows)
+    assert sum(int(r_[5]) for r_ in rows) < sum(int(r_[5]) for r_ in off_rows)
+
+
+@pytest.mark.gpu
+def test_analyze_bench_and_dumps(tmp_path):
+    cfg = tmp_path / "a.cfg"
+    cfg.write_text(SIM_CFG)
+    prof, csv, dump = tmp_path / "prof.cfg", tmp_path / "an.csv", tmp_path / "dump"
+    run("analyze", "--config", str(cfg), "--out", str(prof), "--csv", str(csv), "--dump-dir", str(dump), check=0)
+    schema, header, rows = read_csv(csv)
+    assert schema == "embc.analyze.v1" and header[0] == "table_id" and len(rows) == 3
+    from paper_2407_04272_b200 import policy as P
+    profiles = P.read_profiles(str(prof))
+    assert sorted(profiles) == [0, 1, 2]
+    for t in range(3):  # dumped raw-codes chunks decode back to the sample batch shape
+        out = tmp_path / f"t{t}.embv"
+        run("decompress", "--in", str(dump / f"table_{t}.embc"), "--out", str(out), check=0)
+        assert read_values(out).shape == (256, 8)
+    bcsv = tmp_path / "b.csv"
+    run("bench", "--config", str(cfg), "--out", str(bcsv), check=0)
+    schema, header, rows = read_csv(bcsv)
+    assert schema == "embc.bench.v1" and len(rows) == 9
+    assert [r_[1] for r_ in rows[:3]] == ["raw", "vlz", "huffman"]
+    assert all(float(r_[4]) > 0 and float(r_[5]) > 0 for r_ in rows)
