@@ -195,17 +195,17 @@ __device__ __forceinline__ uint4 window16(const uint4 a, const uint4 b, uint32_t
 }
 
 // fp32 output, whole quads: aligned 16-B loads of the (unaligned) code words,
-// 16-B stores, eight quads in flight per thread
+// 16-B stores, four quads in flight per thread
 __device__ __forceinline__ void raw_tile_f32(const DChunk& C, const uint8_t* p, double w, const RawTile& T) {
   const uintptr_t g0 = reinterpret_cast<uintptr_t>(p + 4 * T.e0);
   const uint4* gv = reinterpret_cast<const uint4*>(g0 & ~uintptr_t(15));
   const uint32_t s = static_cast<uint32_t>(g0 & 15);
   const uint32_t nq = static_cast<uint32_t>(T.ne >> 2);
   float4* o = reinterpret_cast<float4*>(static_cast<float*>(C.out) + T.e0);
-  for (uint32_t q0 = 0; q0 < nq; q0 += 8 * blockDim.x) {
-    uint4 lo[8], hi[8];
+  for (uint32_t q0 = 0; q0 < nq; q0 += 4 * blockDim.x) {
+    uint4 lo[4], hi[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const uint32_t q = q0 + u * blockDim.x + threadIdx.x;
       if (q < nq) {
         lo[u] = __ldg(gv + q);
@@ -213,7 +213,7 @@ __device__ __forceinline__ void raw_tile_f32(const DChunk& C, const uint8_t* p, 
       }
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const uint32_t q = q0 + u * blockDim.x + threadIdx.x;
       if (q < nq) {
         const uint4 c = window16(lo[u], hi[u], s);
@@ -1145,15 +1145,6 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   const uint32_t sb = b0 >= kSegBack ? b0 - kSegBack : 0;
   const uint32_t la = static_cast<uint32_t>(umin64(L - (b0 + nb), 10ull * (D + 1) + 10));
   const uint32_t ns = b0 + nb + la - sb;
-  // the header is validated by the last thread while the others stage the
-  // bytes (one round of loads)
-  if (threadIdx.x == blockDim.x - 1) {
-    s_bad = 0;
-    s_nlit = 0;
-    const DecState S = parse_chunk(C);
-    s_err = S.err;
-    s_eb = S.eb;
-  }
   {  // 16-B loads of the aligned blocks covering [sb, sb + ns); B points at byte sb
     const uintptr_t g0 = reinterpret_cast<uintptr_t>(p + sb);
     const uint4* gv = reinterpret_cast<const uint4*>(g0 & ~uintptr_t(15));
@@ -1174,6 +1165,13 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
       }
     }
     B = smem + lead;
+  }
+  if (threadIdx.x == 0) {
+    s_bad = 0;
+    s_nlit = 0;
+    const DecState S = parse_chunk(C);
+    s_err = S.err;
+    s_eb = S.eb;
   }
   __syncthreads();
   if (s_err != ~0ull) return;  // every CTA of the chunk sees it: nobody waits on this segment
@@ -1261,55 +1259,24 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   __syncthreads();
   DTS(blockIdx.x, 5);
   unsigned long long* status = a.seg_status;
-  // decoupled look-back: warp 0 finds the nearest predecessor with an
-  // inclusive state; the maps published after it are loaded by the whole CTA
-  // (one round of loads per batch of `cap` maps) and applied by thread 0.
-  // Before every batch warp 0 re-reads the 32 nearest predecessors: an
-  // inclusive state published there meanwhile replaces the maps before it.
-  __shared__ uint32_t s_m0;
-  __shared__ unsigned long long s_lb;
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0 && sp.seg > 0) st_vol(status + gseg, kStAgg);
+    unsigned long long in;
     if (sp.seg == 0) {
-      if (threadIdx.x == 0) {
-        s_lb = vlz_state(false, 0, 0);
-        s_m0 = gseg;
-      }
+      in = vlz_state(false, 0, 0);
     } else {
       unsigned long long w;
       const uint32_t q = find_inclusive(status, C.seg0, gseg, &w);
-      if (threadIdx.x == 0) {
-        s_lb = w & ~(3ull << 62);
-        s_m0 = q + 1;
-      }
-    }
-  }
-  __syncthreads();
-  {
-    const uint32_t cap = max(1u, kSeg / (D + 1));  // lit holds kSeg u32 (free until the tokens)
-    for (;;) {
-      if (threadIdx.x < 32 && s_m0 < gseg && !((s_lb >> 61) & 1)) {
-        const uint32_t m0 = s_m0;
-        const int64_t sidx = static_cast<int64_t>(gseg) - 1 - threadIdx.x;
-        const unsigned long long sv = sidx >= static_cast<int64_t>(m0) ? ld_vol(status + sidx) : 0ull;
-        const uint32_t inc = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
-        if (inc && threadIdx.x == __ffs(inc) - 1) {
-          s_lb = sv & ~(3ull << 62);
-          s_m0 = static_cast<uint32_t>(sidx) + 1;
-        }
-      }
-      __syncthreads();
-      const uint32_t m0 = s_m0;
-      if (m0 >= gseg || ((s_lb >> 61) & 1)) break;
-      const uint32_t nm = min(cap, gseg - m0);
-      const uint32_t* src = a.maps + C.map_base + static_cast<uint64_t>(m0 - C.seg0) * (D + 1);
-      const uint32_t tot = nm * (D + 1);
-      for (uint32_t k = threadIdx.x; k < tot; k += blockDim.x) lit[k] = __ldcg(src + k);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned long long x = s_lb;
-        bool dead = false;
-        uint32_t e = static_cast<uint32_t>(x >> 32) & 0x7FF, rows = static_cast<uint32_t>(x);
+      bool dead = (w >> 61) & 1;
+      uint32_t e = static_cast<uint32_t>(w >> 32) & 0x7FF, rows = static_cast<uint32_t>(w);
+      // apply the maps published after it: batches loaded in parallel into
+      // shared memory (the literal queue is free until the tokens), applied in order
+      const uint32_t cap = max(1u, kSeg / (D + 1));  // lit holds kSeg u32
+      for (uint32_t m0 = q + 1; m0 < gseg && !dead; m0 += cap) {
+        const uint32_t nm = min(cap, gseg - m0);
+        const uint32_t* src = a.maps + C.map_base + static_cast<uint64_t>(m0 - C.seg0) * (D + 1);
+        for (uint32_t k = threadIdx.x; k < nm * (D + 1); k += 32) lit[k] = __ldcg(src + k);
+        __syncwarp();
         for (uint32_t m = 0; m < nm && !dead; ++m) {
           const uint32_t v = lit[m * (D + 1) + e];
           if (v == 0xFFFFFFFFu) dead = true;
@@ -1318,28 +1285,26 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
             e = v & 0xFFFF;
           }
         }
-        s_lb = vlz_state(dead, e, rows);
-        s_m0 = m0 + nm;
+        __syncwarp();
       }
-      __syncthreads();
+      in = vlz_state(dead, e, rows);
     }
-  }
-  if (threadIdx.x == 0) {
-    const unsigned long long in = s_lb;
-    bool dead = (in >> 61) & 1;
-    const uint32_t e = static_cast<uint32_t>(in >> 32) & 0x7FF, rows = static_cast<uint32_t>(in);
-    uint32_t eo = 0, ro = rows;
-    if (!dead) {
-      const uint32_t v = mymap[e];
-      if (v == 0xFFFFFFFFu) dead = true;
-      else {
-        eo = v & 0xFFFF;
-        ro = rows + (v >> 16);
-        if (ro > C.count) dead = true;  // more tokens than vectors: trailing bytes
+    if (threadIdx.x == 0) {
+      bool dead = (in >> 61) & 1;
+      const uint32_t e = static_cast<uint32_t>(in >> 32) & 0x7FF, rows = static_cast<uint32_t>(in);
+      uint32_t eo = 0, ro = rows;
+      if (!dead) {
+        const uint32_t v = mymap[e];
+        if (v == 0xFFFFFFFFu) dead = true;
+        else {
+          eo = v & 0xFFFF;
+          ro = rows + (v >> 16);
+          if (ro > C.count) dead = true;  // more tokens than vectors: trailing bytes
+        }
       }
+      st_vol(status + gseg, kStInc | vlz_state(dead, eo, ro));
+      s_in = in;
     }
-    st_vol(status + gseg, kStInc | vlz_state(dead, eo, ro));
-    s_in = in;
   }
   __syncthreads();
   DTS(blockIdx.x, 6);
@@ -1471,8 +1436,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   __shared__ uint32_t G[kMaxGroups][32], BM[32];
   __shared__ uint32_t s_ge[kMaxGroups], s_gt[kMaxGroups];
   __shared__ unsigned long long s_gc[kMaxGroups];
-  __shared__ unsigned long long s_in, s_lb;
-  __shared__ uint32_t s_m0, s_cm[kBlock / 32][32];
+  __shared__ unsigned long long s_in;
   __shared__ int s_use;
   const uint32_t c = a.hblk_chunk[gb];
   const DChunk& C = a.ch[c];
@@ -1503,27 +1467,9 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   // the chunk's first bytes (header, codebook of up to 64 entries) in one round
   __shared__ __align__(8) uint8_t s_hb[kLocalHdr + 8];
   __shared__ uint64_t s_vals[64], s_starts[128];
-  const uint64_t poff = C.payload_only ? 0 : kHeader;
-  // in the same round of loads: the chunk bytes that hold this block's words
-  // for any codebook of up to 64 entries (the bitstream starts 12 + 5 nent
-  // bytes into the payload), staged in the Gs region (free until phase B)
-  const int64_t ws = static_cast<int64_t>(poff + 12 + bit0 / 8) - 4 * static_cast<int64_t>(kHPre);  // >= 4
-  const uint32_t wl = 5 * 64 + 4 * hwords;
-  uint8_t* rawb = reinterpret_cast<uint8_t*>(Gs);
-  uint32_t wlead = 0;  // chunk byte y (ws <= y < wx1) is rawb[y - ws + wlead]
-  {
-    const int64_t wx1 = static_cast<int64_t>(umin64(C.length, static_cast<uint64_t>(ws + wl)));
-    if (wx1 > ws) {
-      const uintptr_t g0 = reinterpret_cast<uintptr_t>(C.in + ws);
-      const uint4* gv = reinterpret_cast<const uint4*>(g0 & ~uintptr_t(15));
-      wlead = static_cast<uint32_t>(g0 & 15);
-      const uint32_t nv = (wlead + static_cast<uint32_t>(wx1 - ws) + 15) / 16;
-      uint4* sv = reinterpret_cast<uint4*>(rawb);
-      for (uint32_t k = threadIdx.x; k < nv; k += blockDim.x) sv[k] = __ldg(gv + k);
-    }
-  }
   for (uint32_t k = threadIdx.x; k < kLocalHdr; k += blockDim.x) s_hb[k] = k < C.length ? __ldg(C.in + k) : 0;
   __syncthreads();
+  const uint64_t poff = C.payload_only ? 0 : kHeader;
   uint64_t boff = 0, nby = 0;
   if (C.length >= poff + 12) {
     boff = 12 + 5 * ld_be(s_hb + poff + 8, 4);
@@ -1532,25 +1478,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
 #ifdef EMBC_DEBUG
   const unsigned long long dt0 = dtime();
 #endif
-  if (boff >= 12 && boff <= 12 + 5 * 64 && C.length >= poff + boff) {
-    // W[k] = big-endian word at stream byte bit0 / 8 - 4 kHPre + 4 k (zeros
-    // outside the stream); stream byte j is chunk byte poff + boff + j
-    const int64_t sbyte0 = static_cast<int64_t>(bit0 / 8) - 4 * static_cast<int64_t>(kHPre);
-    const int64_t shift = static_cast<int64_t>(poff + boff) - ws + wlead;
-    for (uint32_t k = threadIdx.x; k < hwords; k += blockDim.x) {
-      uint32_t v = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t j = sbyte0 + 4 * static_cast<int64_t>(k) + q;
-        const uint32_t by = (j >= 0 && static_cast<uint64_t>(j) < nby) ? rawb[j + shift] : 0u;
-        v = (v << 8) | by;
-      }
-      W[k] = v;
-    }
-  } else {
-    stage(C.in + poff + boff, nby);
-  }
-  __syncthreads();  // rawb (Gs) is read above
+  stage(C.in + poff + boff, nby);
 #ifdef EMBC_DEBUG
   __syncthreads();
   const unsigned long long dt1 = dtime();
@@ -1786,77 +1714,33 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     __threadfence();
     __syncwarp();
     if (lane == 0 && b > 0) st_vol(status + gb, kStAgg);
+    unsigned long long in;
     if (b == 0) {
-      if (lane == 0) {
-        s_lb = huf_state(0, 0, 0);
-        s_m0 = gb;
-      }
+      in = huf_state(0, 0, 0);
     } else {
       unsigned long long w;
       const uint32_t q = find_inclusive(status, C.blk0, gb, &w);
-      if (lane == 0) {
-        s_lb = w & ~(3ull << 62);
-        s_m0 = q + 1;
-      }
-    }
-  }
-  __syncthreads();
-  // the maps published after it, 128 per round: every warp loads 16 (lane e
-  // holds entry e of each) and composes them into one map by shuffles; thread
-  // 0 applies the eight composed maps in order.  Before every round warp 0
-  // re-reads the 32 nearest predecessors: an inclusive state published there
-  // meanwhile replaces the maps before it.
-  for (;;) {
-    if (warp == 0 && s_m0 < gb && !((s_lb >> 60) & 3)) {
-      const uint32_t m0 = s_m0;
-      const int64_t sidx = static_cast<int64_t>(gb) - 1 - lane;
-      const unsigned long long sv = sidx >= static_cast<int64_t>(m0) ? ld_vol(status + sidx) : 0ull;
-      const uint32_t inc = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
-      if (inc && lane == static_cast<uint32_t>(__ffs(inc) - 1)) {
-        s_lb = sv & ~(3ull << 62);
-        s_m0 = static_cast<uint32_t>(sidx) + 1;
-      }
-    }
-    __syncthreads();
-    const uint32_t m0 = s_m0;
-    if (m0 >= gb || ((s_lb >> 60) & 3)) break;
-    const uint32_t nm = min(128u, gb - m0);
-    {
-      const uint32_t w0 = m0 + 16 * warp;
-      uint32_t f[16];
+      uint32_t tm = static_cast<uint32_t>(w >> 60) & 3, ee = static_cast<uint32_t>(w >> 55) & 31;
+      uint64_t cc = w & ((1ull << 55) - 1);
+      // maps published after it: lane e holds entry e of each map (loads in
+      // flight together), applied in order by shuffles
+      for (uint32_t m0 = q + 1; m0 < gb && !tm; m0 += 8) {
+        uint32_t f[8];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) f[k] = w0 + k < m0 + nm ? __ldcg(a.bmaps + static_cast<uint64_t>(w0 + k) * 32 + lane) : 0;
-      uint32_t e = lane, tm = 0, cnt = 0;
+        for (int k = 0; k < 8; ++k) f[k] = m0 + k < gb ? __ldcg(a.bmaps + static_cast<uint64_t>(m0 + k) * 32 + lane) : 0;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const uint32_t v = __shfl_sync(0xffffffffu, f[k], e);
-        if (w0 + k < m0 + nm && !tm) {
-          tm = pk_term(v);
-          cnt += pk_cnt(v);
-          e = pk_off(v);
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t v = __shfl_sync(0xffffffffu, f[k], ee);
+          if (m0 + k < gb && !tm) {
+            tm = pk_term(v);
+            cc += pk_cnt(v);
+            ee = pk_off(v);
+          }
         }
       }
-      s_cm[warp][lane] = pk(e, tm, cnt);
+      in = huf_state(tm, ee, cc);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned long long x = s_lb;
-      uint32_t tm = static_cast<uint32_t>(x >> 60) & 3, ee = static_cast<uint32_t>(x >> 55) & 31;
-      uint64_t cc = x & ((1ull << 55) - 1);
-      for (uint32_t k = 0; k < (nm + 15) / 16 && !tm; ++k) {
-        const uint32_t v = s_cm[k][ee];
-        tm = pk_term(v);
-        cc += pk_cnt(v);
-        ee = pk_off(v);
-      }
-      s_lb = huf_state(tm, ee, cc);
-      s_m0 = m0 + nm;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const unsigned long long in = s_lb;
-    {
+    if (lane == 0) {
       uint32_t tm = static_cast<uint32_t>(in >> 60) & 3, ee = static_cast<uint32_t>(in >> 55) & 31;
       uint64_t cc = in & ((1ull << 55) - 1);
       if (!tm) {
@@ -2233,22 +2117,26 @@ __device__ __forceinline__ void dec_role(const DecArgs& a, uint32_t t, uint8_t* 
   DTS(blockIdx.x, 7);
 }
 
+template <bool PERSISTENT>
 __global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_t;
-  // roles in ticket order: look-back only ever waits on earlier tickets (held
-  // by running CTAs), so persistent CTAs that loop over tickets cannot deadlock
-  for (;;) {
+  if constexpr (!PERSISTENT) {
     if (threadIdx.x == 0) s_t = atomicAdd(&a.tickets[0], 1u);
     __syncthreads();
-    const uint32_t t = s_t;
-    if (a.persistent) {
+    dec_role(a, s_t, smem);  // roles in ticket order: look-back only ever waits on earlier tickets
+  } else {
+    // device-planned calls: resident CTAs loop over the tickets (every wait is
+    // on an earlier ticket, held by a running CTA, so the loop cannot deadlock)
+    for (;;) {
+      if (threadIdx.x == 0) s_t = atomicAdd(&a.tickets[0], 1u);
+      __syncthreads();
+      const uint32_t t = s_t;
       const uint32_t total = a.nchunks + a.dcount[0] + a.dcount[1] + a.nraw + a.nctile + a.nchunks;
       if (t >= total) return;
+      dec_role(a, t, smem);
+      __syncthreads();  // the role's shared state is dead before the next ticket
     }
-    dec_role(a, t, smem);
-    if (!a.persistent) return;
-    __syncthreads();  // the role's shared state is dead before the next ticket
   }
 }
 
@@ -2352,7 +2240,8 @@ using namespace embc_dev;
 static inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
 cudaError_t decode_set_attributes() {
-  cudaError_t e = cudaFuncSetAttribute(k_dec_main, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
+  cudaError_t e = cudaFuncSetAttribute(k_dec_main<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_dec_main<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
   return e;
 }
 
@@ -2563,10 +2452,11 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
     int dev_id = 0, nsm = 0, per_sm = 0;
     cudaGetDevice(&dev_id);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev_id);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dec_main, kBlock, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dec_main<true>, kBlock, smem);
     g1 = std::max<uint32_t>(1, std::min<uint32_t>(g1, static_cast<uint32_t>(std::max(1, nsm * per_sm))));
   }
-  EMBC_TIMED(ctx, "k_dec_main", stream, k_dec_main<<<g1, kBlock, smem, stream>>>(a));
+  if (dev) EMBC_TIMED(ctx, "k_dec_main", stream, k_dec_main<true><<<g1, kBlock, smem, stream>>>(a));
+  else EMBC_TIMED(ctx, "k_dec_main", stream, k_dec_main<false><<<g1, kBlock, smem, stream>>>(a));
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return cuda_fail(ctx, ce, "decode launch");
   return EMBC_OK;
