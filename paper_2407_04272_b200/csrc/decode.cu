@@ -47,22 +47,7 @@
 
 namespace embc_dev {
 
-#ifdef EMBC_DEBUG
-__device__ unsigned long long g_dts[16384][12];  // role, t1..t11 (t7 = end)
-__device__ unsigned long long g_dcalls;
-__device__ unsigned long long g_kspan[4] = {~0ull, 0, 0, 0};  // k_dec_main: first start, last end, CTAs done, calls
-__device__ unsigned long long g_dloc[12];  // huffman blocks: local tables ok / not; ns in local build, in stage, ...
-__device__ __forceinline__ unsigned long long dtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define DTS(slot, k) do { if (threadIdx.x == 0 && (slot) < 16384) g_dts[slot][k] = dtime(); } while (0)
-#define DROLE(slot, r) do { if (threadIdx.x == 0 && (slot) < 16384) { g_dts[slot][0] = (r); for (int q = 2; q < 12; ++q) g_dts[slot][q] = 0; } } while (0)
-#else
-#define DTS(slot, k) do {} while (0)
-#define DROLE(slot, r) do {} while (0)
-#endif
+#include "decode_timeline.cuh"  // EMBC_DEBUG builds only: per-role device timestamps
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
@@ -597,9 +582,7 @@ __device__ bool huff_tables_local(const DChunk& C, const uint8_t* hb, HTab& tb, 
     }
   }
   __syncthreads();
-#ifdef EMBC_DEBUG
-  const unsigned long long lt0 = dtime();
-#endif
+  EMBC_DBG(const unsigned long long lt0 = dtime());
   if (!s_ok) return false;
   const uint32_t nent = s_nent;
   const uint8_t* p = hb + (C.payload_only ? 0 : kHeader);
@@ -609,9 +592,7 @@ __device__ bool huff_tables_local(const DChunk& C, const uint8_t* hb, HTab& tb, 
       s_ok = 0;
   }
   __syncthreads();
-#ifdef EMBC_DEBUG
-  const unsigned long long lt1 = dtime();
-#endif
+  EMBC_DBG(const unsigned long long lt1 = dtime());
   if (!s_ok) return false;
   // the prefix LUT straight from the canonical tables: a slot is the codeword
   // of length l <= kL0 whose code is its top l bits, else a prefix of a longer
@@ -631,12 +612,10 @@ __device__ bool huff_tables_local(const DChunk& C, const uint8_t* hb, HTab& tb, 
     lut[sl] = ent;
   }
   __syncthreads();
-#ifdef EMBC_DEBUG
-  if (threadIdx.x == 0) {
+  EMBC_DBG(if (threadIdx.x == 0) {
     atomicAdd(&g_dloc[4], lt1 - lt0);
     atomicAdd(&g_dloc[5], dtime() - lt1);
-  }
-#endif
+  });
   return true;
 }
 
@@ -1475,24 +1454,17 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     boff = 12 + 5 * ld_be(s_hb + poff + 8, 4);
     if (C.length - poff >= boff) nby = C.length - poff - boff;
   }
-#ifdef EMBC_DEBUG
-  const unsigned long long dt0 = dtime();
-#endif
+  EMBC_DBG(const unsigned long long dt0 = dtime());
   stage(C.in + poff + boff, nby);
-#ifdef EMBC_DEBUG
-  __syncthreads();
-  const unsigned long long dt1 = dtime();
-#endif
+  EMBC_DBG(__syncthreads(); const unsigned long long dt1 = dtime());
   // small calls (128-subsequence blocks) build block-local tables: there the
   // blocks start with the chunk CTAs and would otherwise wait on them
   const bool local = a.local_tables && huff_tables_local(C, s_hb, t, lut, s_vals, s_starts);
-#ifdef EMBC_DEBUG
-  if (threadIdx.x == 0) {
+  EMBC_DBG(if (threadIdx.x == 0) {
     atomicAdd(&g_dloc[local ? 0 : 1], 1ull);
     atomicAdd(&g_dloc[2], dtime() - dt1);
     atomicAdd(&g_dloc[3], dt1 - dt0);
-  }
-#endif
+  });
   const uint64_t* vals = s_vals;
   if (!local) {
     if (threadIdx.x == 0) {  // the chunk CTA (an earlier ticket) publishes the verdict and the tables
@@ -1982,68 +1954,7 @@ __device__ void finish_chunk(const DecArgs& a, uint32_t c) {
     __threadfence();
     dec_fold(a.st, a.nchunks, a.err);
     if (threadIdx.x == 0) *a.diag = atomicAdd(&a.tickets[2], 0u);  // decode fallbacks of this call
-#ifdef EMBC_DEBUG
-    if (threadIdx.x != 0) return;
-    const uint32_t nb = a.nchunks + a.nseg + a.nhblk + a.nraw + a.nctile + a.nchunks - 1;
-    if (a.nchunks >= 26 && (++g_dcalls) % 8 == 7 && nb <= 16384) {
-      printf("D1 huffman blocks: local tables %llu, waited %llu; mean ns local build %llu (warp %llu, lut %llu), stage %llu\n",
-             g_dloc[0], g_dloc[1], g_dloc[2] / max(1ull, g_dloc[0] + g_dloc[1]), g_dloc[4] / max(1ull, g_dloc[0]),
-             g_dloc[5] / max(1ull, g_dloc[0]), g_dloc[3] / max(1ull, g_dloc[0] + g_dloc[1]));
-      for (int q = 0; q < 12; ++q) g_dloc[q] = 0;
-      unsigned long long t0 = ~0ull;
-      for (uint32_t k = 0; k < nb; ++k) t0 = min(t0, g_dts[k][1]);
-      const char* names[6] = {"chunk", "vlzseg", "hufblk", "raw", "copy", "finish"};
-      {  // huffman table build phases (slots 8000 + chunk: 8 start, 2 keys, 3 sort, 4 codes, 5 lut, 6 dup sort)
-        unsigned long long n = 0, sm[6] = {0}, mx[6] = {0};
-        const int ord[6] = {8, 2, 3, 4, 5, 6};
-        for (uint32_t c = 0; c < a.nchunks && 8000 + c < 16384; ++c) {
-          if (!g_dts[8000 + c][8] || !g_dts[8000 + c][6]) continue;
-          ++n;
-          for (int q = 1; q < 6; ++q) {
-            const unsigned long long d = g_dts[8000 + c][ord[q]] - g_dts[8000 + c][ord[q - 1]];
-            sm[q] += d;
-            mx[q] = max(mx[q], d);
-          }
-          sm[0] += g_dts[8000 + c][8] - t0;
-          mx[0] = max(mx[0], g_dts[8000 + c][8] - t0);
-        }
-        if (n)
-          printf("D1 tables n %llu start %llu/%llu keys %llu/%llu sort %llu/%llu codes %llu/%llu lut %llu/%llu dup %llu/%llu\n", n,
-                 sm[0] / n, mx[0], sm[1] / n, mx[1], sm[2] / n, mx[2], sm[3] / n, mx[3], sm[4] / n, mx[4], sm[5] / n, mx[5]);
-        for (uint32_t c = 0; c < a.nchunks && 8000 + c < 16384; ++c) g_dts[8000 + c][8] = g_dts[8000 + c][6] = 0;
-      }
-      for (uint32_t role = 0; role < 6; ++role) {
-        unsigned long long n = 0, mn = ~0ull, mx = 0, sum[12] = {0}, mxs[12] = {0};
-        for (uint32_t k = 0; k < nb; ++k) {
-          if (g_dts[k][0] != role) continue;
-          ++n;
-          mn = min(mn, g_dts[k][1] - t0);
-          mx = max(mx, g_dts[k][7] - t0);
-          unsigned long long prev = g_dts[k][1];
-          for (int q = 2; q <= 7; ++q) {
-            if (!g_dts[k][q]) continue;
-            if (q == 7 && g_dts[k][8]) {  // extra stamps 8..11 recorded between 6 and 7
-              for (int x = 8; x <= 11; ++x) {
-                if (!g_dts[k][x]) continue;
-                const unsigned long long d = g_dts[k][x] - prev;
-                sum[x] += d;
-                mxs[x] = max(mxs[x], d);
-                prev = g_dts[k][x];
-              }
-            }
-            const unsigned long long d = g_dts[k][q] - prev;
-            sum[q] += d;
-            mxs[q] = max(mxs[q], d);
-            prev = g_dts[k][q];
-          }
-        }
-        if (!n) continue;
-        printf("D1 %-6s n %4llu span [%6llu %6llu] phase mean/max ns: 2:%llu/%llu 3:%llu/%llu 4:%llu/%llu 5:%llu/%llu 6:%llu/%llu 8:%llu/%llu 9:%llu/%llu 10:%llu/%llu 11:%llu/%llu 7:%llu/%llu\n",
-               names[role], n, mn, mx, sum[2] / n, mxs[2], sum[3] / n, mxs[3], sum[4] / n, mxs[4], sum[5] / n, mxs[5],
-               sum[6] / n, mxs[6], sum[8] / n, mxs[8], sum[9] / n, mxs[9], sum[10] / n, mxs[10], sum[11] / n, mxs[11], sum[7] / n, mxs[7]);
-      }
-    }
-#endif
+    EMBC_DBG(dbg_decode_report(a));
   }
 }
 
