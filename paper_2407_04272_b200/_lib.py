@@ -12,7 +12,7 @@ import subprocess
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libembc_cuda.so")
+LIB_PATH = os.environ.get("EMBC_LIB") or os.path.join(HERE, "libembc_cuda.so")  # EMBC_LIB: A/B builds
 CSRC = os.path.join(HERE, "csrc")
 
 # ---- status / reason codes (embc_cuda.h) ----------------------------------

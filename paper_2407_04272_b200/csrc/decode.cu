@@ -408,25 +408,50 @@ __device__ int small_book_warp(const uint8_t* p, uint32_t nent, double w, int ou
   }
   if (kraft > (1ull << 32)) return 2;
   __syncwarp();
-  uint32_t rank[2] = {0, 0};
-  bool dup = false;
-  for (uint32_t j = 0; j < nent; ++j) {
-    const uint64_t kj = kk[j];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const uint32_t i = r * 32 + lane;
-      rank[r] += (kj < k[r] || (kj == k[r] && j < i)) ? 1u : 0u;
-      dup |= i < nent && j != i && static_cast<uint32_t>(kj) == static_cast<uint32_t>(k[r]);
+  // a codebook written by write_codebook is already in canonical order
+  // (strictly ascending (length, symbol)): then the ranks are the entry
+  // indices and only duplicate symbols need checking
+  const uint64_t up0 = __shfl_up_sync(0xffffffffu, k[0], 1), up1 = __shfl_up_sync(0xffffffffu, k[1], 1);
+  const uint64_t last0 = __shfl_sync(0xffffffffu, k[0], 31);
+  bool srt = true;
+  if (lane >= 1 && lane < nent) srt = up0 < k[0];
+  if (32 + lane < nent) srt = srt && (lane == 0 ? last0 : up1) < k[1];
+  if (__all_sync(0xffffffffu, srt)) {
+    const uint32_t s0 = static_cast<uint32_t>(k[0]), s1 = static_cast<uint32_t>(k[1]);
+    const bool v0 = lane < nent, v1 = 32 + lane < nent;
+    // (warp collectives outside any short-circuit: every lane takes part)
+    const uint32_t m0 = __match_any_sync(0xffffffffu, (static_cast<uint64_t>(v0) << 32) | s0);
+    bool dup = v0 && __popc(m0) > 1;
+    if (nent > 32) {
+      const uint32_t m1 = __match_any_sync(0xffffffffu, (static_cast<uint64_t>(v1) << 32) | s1);
+      dup |= v1 && __popc(m1) > 1;
+      for (uint32_t j = 0; j < 32; ++j) {
+        const uint32_t sj = __shfl_sync(0xffffffffu, s0, j);
+        dup |= v1 && sj == s1;
+      }
     }
+    if (__any_sync(0xffffffffu, dup)) return 3;
+  } else {
+    uint32_t rank[2] = {0, 0};
+    bool dup = false;
+    for (uint32_t j = 0; j < nent; ++j) {
+      const uint64_t kj = kk[j];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t i = r * 32 + lane;
+        rank[r] += (kj < k[r] || (kj == k[r] && j < i)) ? 1u : 0u;
+        dup |= i < nent && j != i && static_cast<uint32_t>(kj) == static_cast<uint32_t>(k[r]);
+      }
+    }
+    if (__any_sync(0xffffffffu, dup)) return 3;
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      if (r * 32 + lane < nent) kk[rank[r]] = k[r];
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 2; ++r) k[r] = r * 32 + lane < nent ? kk[r * 32 + lane] : ~0ull;
   }
-  if (__any_sync(0xffffffffu, dup)) return 3;
-  __syncwarp();
-#pragma unroll
-  for (int r = 0; r < 2; ++r)
-    if (r * 32 + lane < nent) kk[rank[r]] = k[r];
-  __syncwarp();
-#pragma unroll
-  for (int r = 0; r < 2; ++r) k[r] = r * 32 + lane < nent ? kk[r * 32 + lane] : ~0ull;
   unsigned long long carry = 0;
   uint32_t prev_last = 0;  // length of the previous register's last element
   uint32_t maxl = 0;
@@ -1096,6 +1121,8 @@ __device__ __forceinline__ uint64_t stage_varint(const uint8_t* B, uint32_t star
 }
 
 __device__ void vlz_end_check(const DecArgs& a, uint32_t c);
+__device__ __forceinline__ bool vlz_roots_local(const DecArgs& a, const DChunk& C);
+__device__ void vlz_resolve_roots(const DecArgs& a, const DChunk& C, uint8_t* smem);
 
 __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   __shared__ uint32_t s_tmp32[33];
@@ -1363,7 +1390,61 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   if (!s_last) return;
   __threadfence();
   vlz_end_check(a, c);
+  __syncthreads();
+  if (vlz_roots_local(a, C) && !*reinterpret_cast<volatile uint32_t*>(&a.vflag[c])) vlz_resolve_roots(a, C, smem);
   DTS(blockIdx.x, 11);
+}
+
+// Reference rows are copied from their roots (the first occurrence of the
+// row: row_src == itself); a row's source is always an earlier row.  When the
+// chunk's row sources fit in shared memory, its last segment resolves every
+// row's root there once (pointer jumping, four rows in flight per thread) and
+// writes the roots back, so the copy tiles only copy.  Larger chunks leave the
+// jumping to the copy tiles (through L2).
+__device__ __forceinline__ bool vlz_roots_local(const DecArgs& a, const DChunk& C) {
+  return static_cast<uint64_t>(C.count) * 4 <= a.smem_bytes;
+}
+__device__ void vlz_resolve_roots(const DecArgs& a, const DChunk& C, uint8_t* smem) {
+  uint32_t* V = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* src = a.row_src + C.row_base;
+  const uint32_t n = C.count;
+  for (uint32_t q0 = 0; q0 < n; q0 += 4 * blockDim.x) {
+    uint32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t r = q0 + u * blockDim.x + threadIdx.x;
+      v[u] = r < n ? __ldcg(src + r) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t r = q0 + u * blockDim.x + threadIdx.x;
+      if (r < n) V[r] = v[u];
+    }
+  }
+  __syncthreads();
+  for (;;) {
+    bool changed = false;
+    for (uint32_t q0 = 0; q0 < n; q0 += 4 * blockDim.x) {
+      uint32_t v[4], w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t r = q0 + u * blockDim.x + threadIdx.x;
+        v[u] = r < n ? V[r] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = V[v[u]];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t r = q0 + u * blockDim.x + threadIdx.x;
+        if (r < n && w[u] != v[u]) {
+          V[r] = w[u];
+          changed = true;
+        }
+      }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+  for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) __stcg(src + r, V[r]);
 }
 
 // The chunk's end state after its last segment (vlz.hpp:154-157): the token
@@ -1413,8 +1494,6 @@ __device__ __forceinline__ unsigned long long huf_state(uint32_t term, uint32_t 
 __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   __shared__ HTab t;
   __shared__ uint32_t G[kMaxGroups][32], BM[32];
-  __shared__ uint32_t s_ge[kMaxGroups], s_gt[kMaxGroups];
-  __shared__ unsigned long long s_gc[kMaxGroups];
   __shared__ unsigned long long s_in;
   __shared__ int s_use;
   const uint32_t c = a.hblk_chunk[gb];
@@ -1430,6 +1509,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   uint32_t* Ye = Y0 + hsub;
   uint32_t(*Gs)[33] = reinterpret_cast<uint32_t(*)[33]>(Ye + hsub);
   uint16_t* outs = reinterpret_cast<uint16_t*>(Ye + hsub);  // reuses Gs after phase B
+  uint32_t* H = reinterpret_cast<uint32_t*>(B0);            // block entry x group -> state (after the walks)
   DROLE(blockIdx.x, 2);
   // the bitstream is staged while the chunk CTA builds the tables: its place
   // follows from the chunk's own bytes (header size, codebook entry count);
@@ -1671,8 +1751,11 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   DTS(blockIdx.x, 4);
   unsigned long long* status = a.blk_status;
   if (warp == 0) {
+    // lane e also records its state at every group's entry (H, over the chain
+    // summaries, dead after the walks), so phase C needs no second pass
     uint32_t e = lane, term = 0, cnt = 0;
     for (uint32_t g = 0; g < ng; ++g) {
+      H[g * 32 + lane] = pk(e, term, cnt);
       if (!term) {
         const uint32_t f = G[g][e];
         term = pk_term(f);
@@ -1726,19 +1809,6 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
       // (huffman.hpp:274-288) -> the exact walker reports it
       if (b == C.nblk - 1 && cc < C.N) atomicOr(&a.hflag[c], 1u);
       s_in = in;
-      uint32_t ge = static_cast<uint32_t>(in >> 55) & 31, gt = static_cast<uint32_t>(in >> 60) & 3;
-      unsigned long long gc = in & ((1ull << 55) - 1);
-      for (uint32_t g = 0; g < ng; ++g) {
-        s_ge[g] = ge;
-        s_gt[g] = gt;
-        s_gc[g] = gc;
-        if (!gt) {
-          const uint32_t f = G[g][ge];
-          gt = pk_term(f);
-          gc += pk_cnt(f);
-          ge = pk_off(f);
-        }
-      }
     }
   }
   __syncthreads();
@@ -1749,18 +1819,22 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   if (blk_base >= N) return;
   // ---- C: decode every subsequence from its true entry
   uint32_t q = pk(0, 1, 0);
+  uint64_t qbase = 0;  // index of the subsequence's first symbol
   if (threadIdx.x < nloc) {
-    const uint32_t g = threadIdx.x >> gsh;
-    if (!s_gt[g]) q = Gs[threadIdx.x][s_ge[g]];
+    const uint32_t h = H[(threadIdx.x >> gsh) * 32 + (static_cast<uint32_t>(s_in >> 55) & 31)];  // group entry state
+    if (!pk_term(h)) {
+      q = Gs[threadIdx.x][pk_off(h)];
+      qbase = blk_base + pk_cnt(h) + pk_cnt(q);
+    }
   }
   __syncthreads();  // Gs is dead: its bytes take the symbols
   const bool staged = nent <= 65536;
   // per-entry output values: block-local (shared) or the chunk CTA's (global, L2)
   auto ldv = [&](uint32_t k) -> uint64_t { return local ? vals[k] : __ldcg(vals + k); };
   if (threadIdx.x < nloc && !pk_term(q)) {
-    const uint32_t i = threadIdx.x, g = i >> gsh;
+    const uint32_t i = threadIdx.x;
     const uint64_t gbase = bit0 + static_cast<uint64_t>(i) * SB;
-    uint64_t gi = s_gc[g] + pk_cnt(q);  // index of this subsequence's first symbol
+    uint64_t gi = qbase;
     uint32_t p = pk_off(q);
     const SubWin cwin(W, kHPre + SW * i);
     while (p < SB && gi < N && gbase + p < nbits) {
@@ -1861,33 +1935,50 @@ __device__ void copy_tile(const DecArgs& a, uint32_t b, uint8_t* smem) {
     const DChunk& C = a.ch[c];
     uint32_t* src = a.row_src + C.row_base;
     const uint32_t D = C.dim;
-    // roots of the tile's rows: pointer jumping through row_src in L2.  Every
-    // copy tile of the chunk jumps its own rows at the same time, so each
-    // round also sees the other tiles' progress; a row's pointer only ever
-    // moves toward its root (the first occurrence, src == itself)
+    // roots of the tile's rows: resolved by the chunk's last segment when its
+    // row sources fit in shared memory; else pointer jumping through row_src
+    // in L2, every copy tile of the chunk at once, so each round also sees the
+    // other tiles' progress (a row's pointer only ever moves toward its root)
     uint32_t* V = reinterpret_cast<uint32_t*>(smem);
-    for (uint32_t r = threadIdx.x; r < nr; r += blockDim.x) V[r] = __ldcg(src + r0 + r);
-    for (;;) {
-      bool changed = false;
+    if (vlz_roots_local(a, C)) {
       for (uint32_t q0 = 0; q0 < nr; q0 += 4 * blockDim.x) {
-        uint32_t v[4], vv[4];
+        uint32_t v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t r = q0 + u * blockDim.x + threadIdx.x;
-          v[u] = r < nr ? V[r] : 0;
-          vv[u] = (r < nr && v[u] != r0 + r) ? __ldcg(src + v[u]) : v[u];
+          v[u] = r < nr ? __ldcg(src + r0 + r) : 0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t r = q0 + u * blockDim.x + threadIdx.x;
-          if (r < nr && vv[u] != v[u]) {
-            V[r] = vv[u];
-            __stcg(src + r0 + r, vv[u]);
-            changed = true;
-          }
+          if (r < nr) V[r] = v[u];
         }
       }
-      if (!__syncthreads_or(changed)) break;
+      __syncthreads();
+    } else {
+      for (uint32_t r = threadIdx.x; r < nr; r += blockDim.x) V[r] = __ldcg(src + r0 + r);
+      for (;;) {
+        bool changed = false;
+        for (uint32_t q0 = 0; q0 < nr; q0 += 4 * blockDim.x) {
+          uint32_t v[4], vv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t r = q0 + u * blockDim.x + threadIdx.x;
+            v[u] = r < nr ? V[r] : 0;
+            vv[u] = (r < nr && v[u] != r0 + r) ? __ldcg(src + v[u]) : v[u];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t r = q0 + u * blockDim.x + threadIdx.x;
+            if (r < nr && vv[u] != v[u]) {
+              V[r] = vv[u];
+              __stcg(src + r0 + r, vv[u]);
+              changed = true;
+            }
+          }
+        }
+        if (!__syncthreads_or(changed)) break;
+      }
     }
     DTS(blockIdx.x, 3);
     // 16-B units per row when rows are 16-B aligned, else 4-B (8-B for fp64) elements
@@ -2033,9 +2124,11 @@ __global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_t;
   if constexpr (!PERSISTENT) {
-    if (threadIdx.x == 0) s_t = atomicAdd(&a.tickets[0], 1u);
-    __syncthreads();
-    dec_role(a, s_t, smem);  // roles in ticket order: look-back only ever waits on earlier tickets
+    // role = block index.  Every wait is on a lower role index, and CTAs are
+    // dispatched in block-index order (the same assumption as CUB's
+    // single-pass scans), so a waited-on role is resident or finished
+    (void)s_t;
+    dec_role(a, blockIdx.x, smem);
   } else {
     // device-planned calls: resident CTAs loop over the tickets (every wait is
     // on an earlier ticket, held by a running CTA, so the loop cannot deadlock)

@@ -18,7 +18,7 @@ template <class A>
 __device__ void dbg_decode_report(const A& a) {
     if (threadIdx.x != 0) return;
     const uint32_t nb = a.nchunks + a.nseg + a.nhblk + a.nraw + a.nctile + a.nchunks - 1;
-    if (a.nchunks >= 26 && (++g_dcalls) % 8 == 7 && nb <= 16384) {
+    if ((++g_dcalls) % 8 == 7 && nb <= 16384) {
       printf("D1 huffman blocks: local tables %llu, waited %llu; mean ns local build %llu (warp %llu, lut %llu), stage %llu\n",
              g_dloc[0], g_dloc[1], g_dloc[2] / max(1ull, g_dloc[0] + g_dloc[1]), g_dloc[4] / max(1ull, g_dloc[0]),
              g_dloc[5] / max(1ull, g_dloc[0]), g_dloc[3] / max(1ull, g_dloc[0] + g_dloc[1]));
