@@ -1523,6 +1523,36 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
       stage_bits(W + kHPre, hwords - kHPre, bits, nby, bit0);
     }
   };
+  // the block's words held in registers between issuing their loads and
+  // storing them, so the loads overlap the table build (<= 3 words a thread)
+  constexpr uint32_t kStageRegs = 3;
+  uint32_t sw[kStageRegs];
+  auto stage_issue = [&](const uint8_t* bits, uint64_t nby) {
+    const int64_t byte0 = static_cast<int64_t>(bit0 >> 3) - 4 * static_cast<int64_t>(kHPre);
+#pragma unroll
+    for (uint32_t k = 0; k < kStageRegs; ++k) {
+      const uint32_t j = threadIdx.x + k * blockDim.x;
+      uint32_t v = 0;
+      const int64_t bp = byte0 + 4 * static_cast<int64_t>(j);
+      if (j < hwords && bp >= 0) {
+        const uint64_t bb = static_cast<uint64_t>(bp);
+        if (bb + 4 <= nby) {
+          v = (static_cast<uint32_t>(bits[bb]) << 24) | (static_cast<uint32_t>(bits[bb + 1]) << 16) |
+              (static_cast<uint32_t>(bits[bb + 2]) << 8) | bits[bb + 3];
+        } else {
+          for (int q = 0; q < 4; ++q) v = (v << 8) | (bb + q < nby ? bits[bb + q] : 0);
+        }
+      }
+      sw[k] = v;
+    }
+  };
+  auto stage_commit = [&]() {
+#pragma unroll
+    for (uint32_t k = 0; k < kStageRegs; ++k) {
+      const uint32_t j = threadIdx.x + k * blockDim.x;
+      if (j < hwords) W[j] = sw[k];
+    }
+  };
   // the chunk's first bytes (header, codebook of up to 64 entries) in one round
   __shared__ __align__(8) uint8_t s_hb[kLocalHdr + 8];
   __shared__ uint64_t s_vals[64], s_starts[128];
@@ -1535,7 +1565,8 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     if (C.length - poff >= boff) nby = C.length - poff - boff;
   }
   EMBC_DBG(const unsigned long long dt0 = dtime());
-  stage(C.in + poff + boff, nby);
+  if (hwords <= kStageRegs * blockDim.x) stage_issue(C.in + poff + boff, nby);
+  else stage(C.in + poff + boff, nby);
   EMBC_DBG(__syncthreads(); const unsigned long long dt1 = dtime());
   // small calls (128-subsequence blocks) build block-local tables: there the
   // blocks start with the chunk CTAs and would otherwise wait on them
@@ -1545,6 +1576,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     atomicAdd(&g_dloc[2], dtime() - dt1);
     atomicAdd(&g_dloc[3], dt1 - dt0);
   });
+  if (hwords <= kStageRegs * blockDim.x) stage_commit();  // read after the barriers below
   const uint64_t* vals = s_vals;
   if (!local) {
     if (threadIdx.x == 0) {  // the chunk CTA (an earlier ticket) publishes the verdict and the tables
@@ -2126,9 +2158,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
   if constexpr (!PERSISTENT) {
     // role = block index.  Every wait is on a lower role index, and CTAs are
     // dispatched in block-index order (the same assumption as CUB's
-    // single-pass scans), so a waited-on role is resident or finished
+    // single-pass scans), so a waited-on role is resident or finished.
     (void)s_t;
-    dec_role(a, blockIdx.x, smem);
+    const uint32_t t = blockIdx.x;
+    dec_role(a, t, smem);
   } else {
     // device-planned calls: resident CTAs loop over the tickets (every wait is
     // on an earlier ticket, held by a running CTA, so the loop cannot deadlock)

@@ -979,11 +979,9 @@ __device__ __forceinline__ void stats_tile(const StatsArgs& a, const uint32_t ti
 
 __global__ void __launch_bounds__(kBlock, 4) k_stats(StatsArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_tk;
-  // tiles in ticket order: a vlz tile only ever waits on earlier tickets
-  if (threadIdx.x == 0) s_tk = atomicAdd(&a.book.flags[CF_TICKET_S], 1u);
-  __syncthreads();
-  stats_tile<false>(a, s_tk, smem);
+  // tile = block index: a vlz tile only ever waits on lower tiles, which are
+  // dispatched first (block-index order, as CUB's single-pass scans assume)
+  stats_tile<false>(a, blockIdx.x, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -1656,12 +1654,9 @@ __device__ __forceinline__ void emit_tile(const EmitArgs& a, const uint32_t tid,
 template <int PHASE>
 __global__ void __launch_bounds__(kBlock, 4) k_emit(EmitArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_t;
-  // phase 2 (fused, small calls): tiles in ticket order, so the look-back only
-  // ever waits on CTAs that are already running
-  if (threadIdx.x == 0) s_t = PHASE == 2 ? atomicAdd(&a.flags[CF_TICKET], 1u) : blockIdx.x;
-  __syncthreads();
-  emit_tile<PHASE, false>(a, s_t, smem);
+  // tile = block index: the look-back (phase 2) only waits on lower tiles,
+  // dispatched first
+  emit_tile<PHASE, false>(a, blockIdx.x, smem);
 }
 
 // Single-launch encode of small calls: E1 then E2 (phase 2) in the same CTA,
@@ -1678,10 +1673,9 @@ struct FusedArgs {
 
 __global__ void __launch_bounds__(kBlock, 4) k_encode(FusedArgs f) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint32_t s_t;
-  if (threadIdx.x == 0) s_t = atomicAdd(&f.s.book.flags[CF_TICKET_S], 1u);
-  __syncthreads();
-  const uint32_t tid = s_t;
+  // tile = block index: every wait is on a lower tile (look-backs, vlz hash
+  // windows) or on a codebook whose builder is resident (all tiles fit at once)
+  const uint32_t tid = blockIdx.x;
   EMBC_DBG(dbg_kspan_begin());
   stats_tile<true>(f.s, tid, smem);
   const uint32_t jid = f.e.tiles[tid].job;
