@@ -1391,7 +1391,9 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   __threadfence();
   vlz_end_check(a, c);
   __syncthreads();
-  if (vlz_roots_local(a, C) && !*reinterpret_cast<volatile uint32_t*>(&a.vflag[c])) vlz_resolve_roots(a, C, smem);
+  if (vlz_roots_local(a, C) && !*reinterpret_cast<volatile uint32_t*>(&a.vflag[c])) {
+    vlz_resolve_roots(a, C, smem);
+  }
   DTS(blockIdx.x, 11);
 }
 
@@ -1404,6 +1406,7 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
 __device__ __forceinline__ bool vlz_roots_local(const DecArgs& a, const DChunk& C) {
   return static_cast<uint64_t>(C.count) * 4 <= a.smem_bytes;
 }
+
 __device__ void vlz_resolve_roots(const DecArgs& a, const DChunk& C, uint8_t* smem) {
   uint32_t* V = reinterpret_cast<uint32_t*>(smem);
   uint32_t* src = a.row_src + C.row_base;
@@ -1947,6 +1950,59 @@ __device__ __forceinline__ void wait_count(const uint32_t* cnt, uint32_t n) {
   __threadfence();
 }
 
+// Reference rows r0 .. r0 + nr - 1 of a vlz chunk <- their roots (V[r - r0]),
+// in 16-B units when rows are 16-B aligned (else 4-B / 8-B elements); eight
+// units in flight per thread, all loads before the stores (a root is a
+// literal row, never a destination)
+__device__ void copy_ref_rows(const DChunk& C, const uint32_t* V, uint32_t r0, uint32_t nr) {
+  const uint32_t D = C.dim;
+  const uint32_t esz = C.out_kind == EMBC_OUT_F64 ? 8 : 4;
+  const bool vec = ((D * esz) & 15) == 0 && (reinterpret_cast<uintptr_t>(C.out) & 15) == 0;
+  const uint32_t upr = vec ? D * esz / 16 : D;  // units per row
+  const uint32_t total = nr * upr;
+  constexpr int kU = 8;
+  for (uint32_t k0 = 0; k0 < total; k0 += kU * blockDim.x) {
+    uint64_t src[kU], dst[kU];
+    bool go[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t k = k0 + u * blockDim.x + threadIdx.x;
+      go[u] = false;
+      if (k < total) {
+        const uint32_t rl = k / upr, cc = k - rl * upr, ss = V[rl];
+        go[u] = ss != r0 + rl;
+        src[u] = static_cast<uint64_t>(ss) * upr + cc;
+        dst[u] = static_cast<uint64_t>(r0 + rl) * upr + cc;
+      }
+    }
+    if (vec) {
+      uint4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (go[u]) v[u] = __ldcg(reinterpret_cast<const uint4*>(C.out) + src[u]);
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (go[u]) reinterpret_cast<uint4*>(C.out)[dst[u]] = v[u];
+    } else if (esz == 8) {
+      unsigned long long v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (go[u]) v[u] = __ldcg(static_cast<const unsigned long long*>(C.out) + src[u]);
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (go[u]) static_cast<unsigned long long*>(C.out)[dst[u]] = v[u];
+    } else {
+      unsigned int v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (go[u]) v[u] = __ldcg(static_cast<const unsigned int*>(C.out) + src[u]);
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (go[u]) static_cast<unsigned int*>(C.out)[dst[u]] = v[u];
+    }
+  }
+}
+
 // Reference rows <- their root rows, for one tile of a vlz chunk's rows, once
 // every segment of the chunk (and the roots tail) has finished.
 __device__ void copy_tile(const DecArgs& a, uint32_t b, uint8_t* smem) {
@@ -1966,7 +2022,6 @@ __device__ void copy_tile(const DecArgs& a, uint32_t b, uint8_t* smem) {
     const uint32_t c = a.ctile[3 * b], r0 = a.ctile[3 * b + 1], nr = a.ctile[3 * b + 2];
     const DChunk& C = a.ch[c];
     uint32_t* src = a.row_src + C.row_base;
-    const uint32_t D = C.dim;
     // roots of the tile's rows: resolved by the chunk's last segment when its
     // row sources fit in shared memory; else pointer jumping through row_src
     // in L2, every copy tile of the chunk at once, so each round also sees the
@@ -2013,41 +2068,8 @@ __device__ void copy_tile(const DecArgs& a, uint32_t b, uint8_t* smem) {
       }
     }
     DTS(blockIdx.x, 3);
-    // 16-B units per row when rows are 16-B aligned, else 4-B (8-B for fp64) elements
-    const uint32_t esz = C.out_kind == EMBC_OUT_F64 ? 8 : 4;
-    const bool vec = ((D * esz) & 15) == 0 && (reinterpret_cast<uintptr_t>(C.out) & 15) == 0;
-    const uint32_t upr = vec ? D * esz / 16 : D;  // units per row
-    const uint32_t total = nr * upr;
-    for (uint32_t k0 = 0; k0 < total; k0 += 4 * blockDim.x) {
-      uint32_t rr[4], ss[4], cc[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t k = k0 + u * blockDim.x + threadIdx.x;
-        rr[u] = 0xFFFFFFFFu;
-        if (k < total) {
-          const uint32_t rl = k / upr;
-          cc[u] = k - rl * upr;
-          rr[u] = r0 + rl;
-          ss[u] = V[rl];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (rr[u] == 0xFFFFFFFFu || ss[u] == rr[u]) continue;
-        if (vec) {
-          const uint4* in = reinterpret_cast<const uint4*>(C.out) + static_cast<uint64_t>(ss[u]) * upr + cc[u];
-          uint4* o = reinterpret_cast<uint4*>(C.out) + static_cast<uint64_t>(rr[u]) * upr + cc[u];
-          *o = __ldcg(in);
-        } else if (esz == 8) {
-          static_cast<uint64_t*>(C.out)[static_cast<uint64_t>(rr[u]) * D + cc[u]] =
-              __ldcg(static_cast<const unsigned long long*>(C.out) + static_cast<uint64_t>(ss[u]) * D + cc[u]);
-        } else {
-          static_cast<uint32_t*>(C.out)[static_cast<uint64_t>(rr[u]) * D + cc[u]] =
-              __ldcg(static_cast<const unsigned int*>(C.out) + static_cast<uint64_t>(ss[u]) * D + cc[u]);
-        }
-      }
-    }
-    }
+    copy_ref_rows(C, V, r0, nr);
+  }
 }
 
 // Per chunk, once its parallel decode has finished: the exact sequential
