@@ -147,3 +147,31 @@ def test_invalid_window_value_error(ctx, ref):
     for c in (0, 2):
         assert K.encode_chunk(torch.from_numpy(x).to(DEV), 0.01, c, 0) == \
             ref.encode_chunk(x.astype(np.float64), 4, 0.01, c, 0)
+
+
+def test_select_codec_timed_eq2(ctx):
+    """select_codec (policy.hpp:239-274) with measured GPU throughputs
+    (SURVEY 8(f) row 2): the ratios equal the untimed (pinned) run's, the
+    throughputs are positive, the choice is the argmax of Eq. 2
+    (estimate_speedup, policy.hpp:202-208) over the measured samples with ties
+    to the lower codec tag, and at B -> 0 it reduces to the ratio choice the
+    reference pinned.  B = the NVLink per-direction bandwidth."""
+    wl = "kg"
+    prof = W.workload_profiles(wl)
+    specs = W.workload_specs(wl)
+    B = W.WORKLOADS[wl]["batch"](1)
+    cands = [K.CODEC_VLZ, K.CODEC_HUFFMAN]
+    for t in (0, 7, 23):
+        sample = W.Table(specs[t], DEV).lookup_batch(B, 0)
+        pinned, pm = P.select_codec(sample, prof[t].eb, cands, 1e-300, timed=False)
+        assert pinned == prof[t].codec
+        for bw in (900e9, 1e-300):
+            chosen, ms = P.select_codec(sample, prof[t].eb, cands, bw, timed=True)
+            assert [m.ratio for m in ms] == [m.ratio for m in pm]
+            assert all(m.comp_bps > 0 and m.decomp_bps > 0 and np.isfinite(m.comp_bps) for m in ms)
+            sp = [P.estimate_speedup(m.ratio, bw, m.comp_bps, m.decomp_bps) for m in ms]
+            best = max(range(len(ms)), key=lambda i: (sp[i], -ms[i].codec))
+            want = ms[best].codec if ms[best].ratio > 1.0 else K.CODEC_RAW
+            assert chosen == want, (t, bw, sp)
+            if bw < 1.0:
+                assert chosen == pinned
