@@ -1193,9 +1193,13 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
         mask |= 1u << k;
         nseg_here += x0 + k < b0 + nb;
       }
+    // one scan for both counts: units of the round (low half) and units ending
+    // inside the segment (high half; the segment lies in the first round)
     uint32_t tot;
-    uint32_t k0 = nu + block_excl_scan<uint32_t>(__popc(mask), s_tmp32, &tot);
-    if (r0 == b0) U = block_sum<uint32_t>(nseg_here, s_tmp32);  // the segment lies in the first round
+    const uint32_t ex = block_excl_scan<uint32_t>(__popc(mask) | (nseg_here << 16), s_tmp32, &tot);
+    uint32_t k0 = nu + (ex & 0xFFFF);
+    if (r0 == b0) U = tot >> 16;
+    tot &= 0xFFFF;
     uint32_t m = mask;
     while (m) {
       const int b = __ffs(m) - 1;
@@ -1207,8 +1211,8 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   }
   nu = min(nu, kUnitCap);
   if (threadIdx.x == 0) {  // the first unit may begin in the previous segment
-    uint32_t start = b0;
-    while (start > 0 && (p[start - 1] & 0x80) && b0 - start <= 10) --start;
+    uint32_t start = b0;  // walks back at most 11 bytes, inside the kSegBack staged before the segment
+    while (start > 0 && (B[start - 1 - sb] & 0x80) && b0 - start <= 10) --start;
     s_first_start = start - sb;
     // a trailing partial unit can never be consumed by a valid parse
     if (b0 + nb == L && nb > 0 && (B[L - 1 - sb] & 0x80)) s_bad = 1;
@@ -1229,11 +1233,23 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   int nlev = kLift;  // levels past the point where every jump has left the segment are copies
   for (int r = 1; r < kLift; ++r) {
     bool live = false;
-    for (uint32_t k = threadIdx.x; k < U; k += blockDim.x) {
-      const uint16_t j = J[r - 1][k];
-      const uint16_t v = (j == kInv || j >= U) ? j : J[r - 1][j];
-      J[r][k] = v;
-      live |= v != kInv && v < U;
+    for (uint32_t k0 = threadIdx.x; k0 < U; k0 += 4 * blockDim.x) {  // four units in flight
+      uint16_t j[4], v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t k = k0 + u * blockDim.x;
+        j[u] = k < U ? J[r - 1][k] : kInv;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = (j[u] == kInv || j[u] >= U) ? j[u] : J[r - 1][j[u]];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t k = k0 + u * blockDim.x;
+        if (k < U) {
+          J[r][k] = v[u];
+          live |= v[u] != kInv && v[u] < U;
+        }
+      }
     }
     if (!__syncthreads_or(live)) {
       nlev = r + 1;
@@ -1951,7 +1967,7 @@ __device__ __forceinline__ void wait_count(const uint32_t* cnt, uint32_t n) {
 }
 
 // Reference rows r0 .. r0 + nr - 1 of a vlz chunk <- their roots (V[r - r0]),
-// in 16-B units when rows are 16-B aligned (else 4-B / 8-B elements); eight
+// in 16-B units when rows are 16-B aligned (else 4-B / 8-B elements); four
 // units in flight per thread, all loads before the stores (a root is a
 // literal row, never a destination)
 __device__ void copy_ref_rows(const DChunk& C, const uint32_t* V, uint32_t r0, uint32_t nr) {
@@ -1960,45 +1976,44 @@ __device__ void copy_ref_rows(const DChunk& C, const uint32_t* V, uint32_t r0, u
   const bool vec = ((D * esz) & 15) == 0 && (reinterpret_cast<uintptr_t>(C.out) & 15) == 0;
   const uint32_t upr = vec ? D * esz / 16 : D;  // units per row
   const uint32_t total = nr * upr;
-  constexpr int kU = 8;
+  constexpr int kU = 4;
   for (uint32_t k0 = 0; k0 < total; k0 += kU * blockDim.x) {
-    uint64_t src[kU], dst[kU];
-    bool go[kU];
+    uint32_t ss[kU], rl[kU], cc[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint32_t k = k0 + u * blockDim.x + threadIdx.x;
-      go[u] = false;
+      ss[u] = 0xFFFFFFFFu;
       if (k < total) {
-        const uint32_t rl = k / upr, cc = k - rl * upr, ss = V[rl];
-        go[u] = ss != r0 + rl;
-        src[u] = static_cast<uint64_t>(ss) * upr + cc;
-        dst[u] = static_cast<uint64_t>(r0 + rl) * upr + cc;
+        rl[u] = k / upr;
+        cc[u] = k - rl[u] * upr;
+        const uint32_t src = V[rl[u]];
+        if (src != r0 + rl[u]) ss[u] = src;
       }
     }
     if (vec) {
       uint4 v[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (go[u]) v[u] = __ldcg(reinterpret_cast<const uint4*>(C.out) + src[u]);
+        if (ss[u] != 0xFFFFFFFFu) v[u] = __ldcg(reinterpret_cast<const uint4*>(C.out) + static_cast<uint64_t>(ss[u]) * upr + cc[u]);
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (go[u]) reinterpret_cast<uint4*>(C.out)[dst[u]] = v[u];
+        if (ss[u] != 0xFFFFFFFFu) reinterpret_cast<uint4*>(C.out)[static_cast<uint64_t>(r0 + rl[u]) * upr + cc[u]] = v[u];
     } else if (esz == 8) {
       unsigned long long v[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (go[u]) v[u] = __ldcg(static_cast<const unsigned long long*>(C.out) + src[u]);
+        if (ss[u] != 0xFFFFFFFFu) v[u] = __ldcg(static_cast<const unsigned long long*>(C.out) + static_cast<uint64_t>(ss[u]) * upr + cc[u]);
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (go[u]) static_cast<unsigned long long*>(C.out)[dst[u]] = v[u];
+        if (ss[u] != 0xFFFFFFFFu) static_cast<unsigned long long*>(C.out)[static_cast<uint64_t>(r0 + rl[u]) * upr + cc[u]] = v[u];
     } else {
       unsigned int v[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (go[u]) v[u] = __ldcg(static_cast<const unsigned int*>(C.out) + src[u]);
+        if (ss[u] != 0xFFFFFFFFu) v[u] = __ldcg(static_cast<const unsigned int*>(C.out) + static_cast<uint64_t>(ss[u]) * upr + cc[u]);
 #pragma unroll
       for (int u = 0; u < kU; ++u)
-        if (go[u]) static_cast<unsigned int*>(C.out)[dst[u]] = v[u];
+        if (ss[u] != 0xFFFFFFFFu) static_cast<unsigned int*>(C.out)[static_cast<uint64_t>(r0 + rl[u]) * upr + cc[u]] = v[u];
     }
   }
 }
