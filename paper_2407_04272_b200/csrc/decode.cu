@@ -40,6 +40,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -2326,6 +2327,17 @@ cudaError_t decode_set_attributes() {
 // plan is computed on the device (k_dec_plan), and k_dec_main runs as
 // persistent CTAs over the device-counted roles: no host read of the lengths,
 // so the call is graph-capturable.
+// Rows per copy tile: ~8192 values when the chunk's roots are resolved in
+// shared memory by its last segment (the tiles only copy); larger tiles when
+// they must pointer-jump through L2 themselves (each tile pays the same number
+// of dependent rounds whatever its size)
+static uint32_t copy_tile_rows(const embc_chunk_ref& r) {
+  const uint32_t d = std::max<uint32_t>(r.dim, 1);
+  const uint32_t per = std::max<uint32_t>(8, std::min<uint32_t>(4096, 8192 / d));
+  if (static_cast<uint64_t>(r.count) * 4 > kDecSmem) return std::max(per, std::min<uint32_t>(4096, 131072 / d));
+  return per;
+}
+
 embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* refs, uint32_t n,
                    int out_kind, int payload_only, cudaStream_t stream, const uint64_t* d_len,
                    const uint64_t* d_off) {
@@ -2367,7 +2379,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
         map_total += ns * (r.dim + 1);
         C.row_base = row_total;
         row_total += r.count;
-        const uint32_t per = std::max<uint32_t>(8, std::min<uint32_t>(4096, 8192 / std::max<uint32_t>(r.dim, 1)));
+        const uint32_t per = copy_tile_rows(r);
         for (uint32_t r0 = 0; r0 < r.count; r0 += per) {
           ctiles.push_back(c);
           ctiles.push_back(r0);
@@ -2385,7 +2397,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
         C.row_base = row_total;
         row_total += r.count;
         for (uint32_t s = 0; s < C.nseg; ++s) segs.push_back(SegPair{c, s});
-        const uint32_t per = std::max<uint32_t>(8, std::min<uint32_t>(4096, 8192 / std::max<uint32_t>(r.dim, 1)));
+        const uint32_t per = copy_tile_rows(r);
         for (uint32_t r0 = 0; r0 < r.count; r0 += per) {
           ctiles.push_back(c);
           ctiles.push_back(r0);
