@@ -1153,38 +1153,98 @@ __device__ void finish_call(const EmitArgs& a, uint64_t total) {
 // payload (bits), chunk offsets in job order (container.hpp:245-250), chunk
 // headers (container.hpp:74-85), pack table (container.hpp:244-250), 25-B
 // metadata (container.hpp:196-209), capacity check.
+// Segmented scan operator over (segment started, value): a later element that
+// starts a segment discards the running sum.
+struct SegVal {
+  unsigned long long v;
+  uint32_t head;
+};
+__device__ __forceinline__ SegVal seg_op(SegVal a, SegVal b) {
+  return SegVal{b.head ? b.v : a.v + b.v, a.head | b.head};
+}
+
 __device__ void layout_tail(const EmitArgs& a) {
   __shared__ unsigned long long s_tmp64[33];
-  // 1. exclusive prefix of the tile bits over all tiles
-  unsigned long long carry = 0;
-  for (uint32_t t0 = 0; t0 < a.ntiles; t0 += blockDim.x) {
-    const uint32_t t = t0 + threadIdx.x;
-    const unsigned long long v = t < a.ntiles ? __ldcg(a.tile_bits + t) : 0;
-    unsigned long long tot;
-    const unsigned long long pre = block_excl_scan<unsigned long long>(v, s_tmp64, &tot);
-    if (t < a.ntiles) a.tile_off[t] = carry + pre;
-    carry += tot;
+  __shared__ unsigned long long s_wv[32];
+  __shared__ uint32_t s_wh[32];
+  __shared__ unsigned long long s_cv;
+  // 1. every tile's bit offset inside its job's payload data: a segmented
+  //    exclusive scan of the tile bits (segments = jobs, contiguous in tile
+  //    order), kLT tiles per thread per round with all loads in flight; the
+  //    job totals (last tile of each job) go straight to job_start
+  constexpr uint32_t kLT = 8;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_cv = 0;
+  __syncthreads();
+  for (uint32_t r0 = 0; r0 < a.ntiles; r0 += kLT * blockDim.x) {
+    const uint32_t t0 = r0 + threadIdx.x * kLT;
+    unsigned long long bits[kLT];
+    uint32_t job[kLT];
+#pragma unroll
+    for (uint32_t k = 0; k < kLT; ++k) {
+      const uint32_t t = t0 + k;
+      bits[k] = t < a.ntiles ? __ldcg(a.tile_bits + t) : 0;
+      job[k] = t < a.ntiles ? a.tiles[t].job : 0xFFFFFFFFu;
+    }
+    // the job of the tile before this thread's first (segment head test)
+    const uint32_t prevj = t0 == 0 ? 0xFFFFFFFEu : (t0 - 1 < a.ntiles ? a.tiles[t0 - 1].job : 0xFFFFFFFFu);
+    // thread aggregate
+    SegVal agg{0, 0};
+    uint32_t pj = prevj;
+#pragma unroll
+    for (uint32_t k = 0; k < kLT; ++k) {
+      const SegVal e{bits[k], job[k] != pj ? 1u : 0u};
+      agg = seg_op(agg, e);
+      pj = job[k];
+    }
+    // block-wide exclusive scan of the aggregates (warp shuffles, then warps)
+    SegVal inc = agg;
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+      const unsigned long long v = __shfl_up_sync(0xffffffffu, inc.v, o);
+      const uint32_t h = __shfl_up_sync(0xffffffffu, inc.head, o);
+      if (lane >= o) inc = seg_op(SegVal{v, h}, inc);
+    }
+    if (lane == 31) {
+      s_wv[warp] = inc.v;
+      s_wh[warp] = inc.head;
+    }
+    __syncthreads();
+    // exclusive prefix of this warp: the carry-in of the round, then earlier warps
+    SegVal wpre{s_cv, 0};
+    for (uint32_t w = 0; w < warp; ++w) wpre = seg_op(wpre, SegVal{s_wv[w], s_wh[w]});
+    const unsigned long long xv = __shfl_up_sync(0xffffffffu, inc.v, 1);
+    const uint32_t xh = __shfl_up_sync(0xffffffffu, inc.head, 1);
+    const SegVal ex = lane ? seg_op(wpre, SegVal{xv, xh}) : wpre;
+    // the tiles' offsets (and each job's total at its last tile)
+    unsigned long long run = ex.v;
+    pj = prevj;
+#pragma unroll
+    for (uint32_t k = 0; k < kLT; ++k) {
+      const uint32_t t = t0 + k;
+      if (t >= a.ntiles) break;
+      if (job[k] != pj) run = 0;
+      a.tile_off[t] = run;
+      run += bits[k];
+      pj = job[k];
+      if (t + 1 == a.ntiles || (k + 1 < kLT ? job[k + 1] != job[k] : a.tiles[t + 1].job != job[k]))
+        a.job_start[job[k]] = run;  // the job's payload bits (step 3 turns it into the chunk offset)
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_cv = seg_op(ex, agg).v;  // the round's carry-out
+    __syncthreads();
   }
-  __threadfence_block();
-  __syncthreads();
-  // 2. relative to each job's first tile (the job's prefix parked in job_start)
-  for (uint32_t j = threadIdx.x; j < a.njobs; j += blockDim.x) a.job_start[j] = __ldcg(a.tile_off + a.jobs[j].tile0);
-  __threadfence_block();
-  __syncthreads();
-  for (uint32_t t = threadIdx.x; t < a.ntiles; t += blockDim.x)
-    a.tile_off[t] = __ldcg(a.tile_off + t) - __ldcg(a.job_start + a.tiles[t].job);
   __threadfence_block();
   __syncthreads();
   // 3. chunk sizes -> offsets in job order, then the per-chunk records
   const uint64_t base = a.layout == EMBC_LAYOUT_PACKED ? 4 + 16ull * a.njobs : 0;
-  carry = base;
+  unsigned long long carry = base;
   for (uint32_t j0 = 0; j0 < a.njobs; j0 += blockDim.x) {
     const uint32_t j = j0 + threadIdx.x;
     uint64_t P = 0, len = 0;
     if (j < a.njobs) {
       const DJob& J = a.jobs[j];
-      const uint32_t lt = J.tile0 + J.ntiles - 1;
-      const uint64_t bits = __ldcg(a.tile_off + lt) + __ldcg(a.tile_bits + lt);
+      const uint64_t bits = __ldcg(a.job_start + j);  // the job's payload bits (step 1)
       P = (J.codec == EMBC_CODEC_HUFFMAN ? 12 + 5ull * a.st[j].nsym : 0) + (bits + 7) / 8;
       len = J.header + P;
     }
