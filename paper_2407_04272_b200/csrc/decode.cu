@@ -2149,6 +2149,18 @@ __device__ __forceinline__ void dec_role(const DecArgs& a, uint32_t t, uint8_t* 
   }
   t -= a.nchunks;
   const uint32_t nseg = a.dcount ? a.dcount[0] : a.nseg, nhblk = a.dcount ? a.dcount[1] : a.nhblk;
+  // small calls (every role resident at once, latency-bound): the huffman
+  // blocks, the longest chains, are dispatched before the vlz segments; large
+  // calls keep the segments first (measured: 40.4 vs 42.3 us Kaggle-shaped,
+  // 154 vs 128 us Terabyte-shaped)
+  const bool hf = a.local_tables != 0;
+  if (hf && t < nhblk) {
+    huff_block(a, t, smem);
+    DTS(blockIdx.x, 7);
+    done_signal(&a.hdone[a.hblk_chunk[t]]);
+    return;
+  }
+  if (hf) t -= nhblk;
   if (t < nseg) {
     vlz_segment(a, t, smem);
     DTS(blockIdx.x, 7);
@@ -2156,13 +2168,13 @@ __device__ __forceinline__ void dec_role(const DecArgs& a, uint32_t t, uint8_t* 
     return;
   }
   t -= nseg;
-  if (t < nhblk) {
+  if (!hf && t < nhblk) {
     huff_block(a, t, smem);
     DTS(blockIdx.x, 7);
     done_signal(&a.hdone[a.hblk_chunk[t]]);
     return;
   }
-  t -= nhblk;
+  if (!hf) t -= nhblk;
   if (t < a.nraw) {
     DROLE(blockIdx.x, 3);
     DTS(blockIdx.x, 1);
