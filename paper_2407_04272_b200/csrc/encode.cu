@@ -223,13 +223,14 @@ __device__ void book_warp(const DJob& J, JobState* Sp, const BookArgs& a, uint64
   __syncwarp();
   TS1(9);
   // 4. lengths = leaf depth; the first leaf (sorted order) past 32 bits fails (huffman.hpp:110-118)
-  unsigned long long cap = ~0ull;
+  unsigned long long cap = ~0ull, bits = 0;
   for (uint32_t i = lane; i < nsym; i += 32) {
     uint32_t depth = 0;
     if (nsym == 1) depth = 1;
     else
       for (int32_t q = parent[i]; q != -1; q = parent[q]) ++depth;
     if (depth > 32) cap = min(cap, (static_cast<unsigned long long>(i) << 32) | depth);
+    bits += (key[i] >> 32) * depth;  // count x code length: the payload bits
     key[i] = (static_cast<uint64_t>(depth > 32 ? 63 : depth) << 32) | (key[i] & 0xFFFFFFFFull);
   }
   cap = warp_min_u64(cap);
@@ -251,7 +252,7 @@ __device__ void book_warp(const DJob& J, JobState* Sp, const BookArgs& a, uint64
   }
   TS1(11);
   // 6. canonical codes: code_i = sum_{j<i} 2^(len_i - len_j) (finalize, huffman.hpp:170-181)
-  unsigned long long carry = 0, bits = 0;
+  unsigned long long carry = 0;
   for (uint32_t i0 = 0; i0 < nsym; i0 += 32) {
     const uint32_t i = i0 + lane;
     uint32_t len = 0, symoff = 0;
@@ -269,7 +270,6 @@ __device__ void book_warp(const DJob& J, JobState* Sp, const BookArgs& a, uint64
       uint8_t* e = book + 12 + 5ull * i;
       st_be(e, static_cast<uint32_t>(static_cast<int32_t>(static_cast<int64_t>(cmin) + symoff)), 4);
       e[4] = static_cast<uint8_t>(len);
-      bits += static_cast<unsigned long long>(__ldcg(gh + symoff)) * len;
     }
     carry += __shfl_sync(0xffffffffu, inc, 31);
   }
@@ -351,17 +351,20 @@ __device__ void build_book(const DJob& J, JobState* Sp, const BookArgs& a, uint8
   }
 
   // 1. nonzero bins -> symbols in ascending order (sorted histogram, huffman.hpp:51)
-  uint32_t cnt = 0;
-  for (uint64_t b = threadIdx.x; b < span; b += blockDim.x) cnt += __ldcg(gh + b) != 0;
-  const uint32_t nsym = block_sum<uint32_t>(cnt, s_tmp32);
+  //    as (count << 32 | sym - cmin) keys; one pass when the span alone bounds
+  //    the symbols to the shared-memory sort, else a counting pass first
+  uint32_t nsym = 0;
+  if (span > kSmemBook) {
+    uint32_t cnt = 0;
+    for (uint64_t b = threadIdx.x; b < span; b += blockDim.x) cnt += __ldcg(gh + b) != 0;
+    nsym = block_sum<uint32_t>(cnt, s_tmp32);
+  }
   TS1(6);
-  uint32_t p2 = 1;
-  while (p2 < nsym) p2 <<= 1;
-  const bool in_smem = p2 <= kSmemBook;
+  const bool in_smem = span <= kSmemBook || nsym <= kSmemBook;
   uint64_t* key = in_smem ? reinterpret_cast<uint64_t*>(smem) : a.gs.key + hj * a.gs_stride;
   uint64_t* wgt = in_smem ? key + kSmemBook : a.gs.wgt + hj * 2 * a.gs_stride;
   int32_t* parent = in_smem ? reinterpret_cast<int32_t*>(wgt + 2 * kSmemBook) : a.gs.parent + hj * 2 * a.gs_stride;
-  {  // (count << 32 | sym - cmin) keys in symbol order
+  {
     uint64_t base = 0;
     for (uint64_t b0 = 0; b0 < span; b0 += blockDim.x) {
       const uint64_t b = b0 + threadIdx.x;
@@ -371,7 +374,10 @@ __device__ void build_book(const DJob& J, JobState* Sp, const BookArgs& a, uint8
       if (c) key[base + pos] = (static_cast<uint64_t>(c) << 32) | b;
       base += tot;
     }
+    nsym = static_cast<uint32_t>(base);
   }
+  uint32_t p2 = 1;
+  while (p2 < nsym) p2 <<= 1;
   for (uint32_t i = nsym + threadIdx.x; i < p2; i += blockDim.x) key[i] = ~0ull;
   __syncthreads();
   uint8_t* book = a.books + hj * a.book_stride;
