@@ -2205,6 +2205,7 @@ template <bool PERSISTENT>
 __global__ void __launch_bounds__(kBlock, 4) k_dec_main(DecArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t s_t;
+  EMBC_DBG(if (threadIdx.x == 0 && blockIdx.x < 16384) g_cta0[blockIdx.x] = dtime());
   if constexpr (!PERSISTENT) {
     // role = block index.  Every wait is on a lower role index, and CTAs are
     // dispatched in block-index order (the same assumption as CUB's

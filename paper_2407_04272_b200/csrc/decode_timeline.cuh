@@ -4,6 +4,7 @@
 #pragma once
 #ifdef EMBC_DEBUG
 __device__ unsigned long long g_dts[16384][12];  // role, t1..t11 (t7 = end)
+__device__ unsigned long long g_cta0[16384];     // %globaltimer at each CTA's first instruction
 __device__ unsigned long long g_dcalls;
 __device__ unsigned long long g_kspan[4] = {~0ull, 0, 0, 0};  // k_dec_main: first start, last end, CTAs done, calls
 __device__ unsigned long long g_dloc[12];  // huffman blocks: local tables ok / not; ns in local build, in stage, ...
@@ -26,6 +27,17 @@ __device__ void dbg_decode_report(const A& a) {
       unsigned long long t0 = ~0ull;
       for (uint32_t k = 0; k < nb; ++k) t0 = min(t0, g_dts[k][1]);
       const char* names[6] = {"chunk", "vlzseg", "hufblk", "raw", "copy", "finish"};
+      {  // CTA dispatch: first instruction of every CTA relative to the earliest role stamp
+        unsigned long long c0 = ~0ull, c1 = 0, cl = 0, cend = 0;
+        for (uint32_t k = 0; k < nb; ++k) {
+          c0 = min(c0, g_cta0[k]);
+          c1 = max(c1, g_cta0[k]);
+          cend = max(cend, g_dts[k][7]);
+        }
+        cl = g_cta0[nb - 1];
+        printf("D1 cta starts: first %lld last %lld (last block %lld) last role end %lld ns (rel. to first role stamp)\n",
+               (long long)(c0 - t0), (long long)(c1 - t0), (long long)(cl - t0), (long long)(cend - t0));
+      }
       {  // huffman table build phases (slots 8000 + chunk: 8 start, 2 keys, 3 sort, 4 codes, 5 lut, 6 dup sort)
         unsigned long long n = 0, sm[6] = {0}, mx[6] = {0};
         const int ord[6] = {8, 2, 3, 4, 5, 6};
