@@ -87,7 +87,18 @@ __device__ __forceinline__ void copy_value(const DChunk& C, uint64_t dst, uint64
 // + raw size (container.hpp:152-155).  Deterministic: every CTA of a chunk
 // computes the same state; the chunk CTA stores it.
 // ---------------------------------------------------------------------------
+__device__ DecState parse_chunk_hb(const DChunk& C, const uint8_t* hb);
 __device__ DecState parse_chunk(const DChunk& C) {
+  // the 30 header bytes in one round of independent loads, then parsed from registers
+  uint8_t hb[kHeader];
+  if (!C.payload_only) {
+#pragma unroll
+    for (uint32_t k = 0; k < kHeader; ++k) hb[k] = k < C.length ? __ldg(C.in + k) : 0;
+  }
+  return parse_chunk_hb(C, hb);
+}
+// parse_chunk on header bytes already at hand (hb[k] = byte k, 0 past the chunk)
+__device__ DecState parse_chunk_hb(const DChunk& C, const uint8_t* hb) {
   DecState S;
   S.err = ~0ull;
   S.a = S.b = 0;
@@ -98,11 +109,6 @@ __device__ DecState parse_chunk(const DChunk& C) {
   S.nsym = 0;
   S.bit_off = 0;
   if (!C.payload_only) {
-    // the 30 header bytes in one round of independent loads, then parsed from registers
-    uint8_t hb[kHeader];
-    const uint8_t* src = C.in;
-#pragma unroll
-    for (uint32_t k = 0; k < kHeader; ++k) hb[k] = k < C.length ? __ldg(src + k) : 0;
     const uint8_t* p = hb;
     const uint64_t L = C.length;
     // field layout: magic[4] ver codec eb:8 dim:4 count:4 paylen:8
@@ -1071,8 +1077,21 @@ __host__ __device__ constexpr uint32_t vlz_smem(uint32_t dmax) {
 }
 constexpr uint32_t kVlzSmem = vlz_smem(kVlzMaxDim);
 
+// huffman block descriptor: staging the block needs no chunk descriptor
+struct HBlkDesc {
+  uint32_t chunk, blk;
+  const uint8_t* in;
+  uint64_t length;
+};
+
+// vlz segment descriptor: the chunk, the segment, and what staging the
+// segment's bytes needs, so the bytes load right after this descriptor (the
+// chunk descriptor and the header check follow off the critical path)
 struct SegPair {
   uint32_t chunk, seg;
+  const uint8_t* in;  // the chunk's first byte
+  uint32_t length;    // the chunk's bytes (< 2^31 for a parallel-decoded chunk)
+  uint32_t dim;
 };
 
 // inclusive vlz state: flag | dead (61) | entry unit offset (42:32) | rows (31:0)
@@ -1085,6 +1104,7 @@ struct DecArgs {
   DecState* st;
   const SegPair* segs;
   const uint32_t* hblk_chunk;  // huffman block -> chunk
+  const struct HBlkDesc* hblk; // huffman block -> (chunk, block in chunk, chunk bytes)
   const RawTile* raw;
   const uint32_t* ctile;       // D2 copy tiles: (chunk << 0) in [0], row0 in [1], rows in [2] (triplets)
   uint32_t* vflag;
@@ -1111,6 +1131,7 @@ struct DecArgs {
   uint32_t smem_bytes;  // dynamic shared memory of k_dec_main
   const uint32_t* dcount;  // device-planned calls: [0] vlz segments, [1] huffman blocks (else null)
   uint32_t persistent;     // CTAs loop over role tickets (device-planned calls)
+  uint32_t payload_only;   // chunks are bare payloads (no header)
 };
 
 __device__ __forceinline__ uint64_t stage_varint(const uint8_t* B, uint32_t start, uint32_t end) {
@@ -1132,11 +1153,21 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   __shared__ int s_last;
   const SegPair sp = a.segs[gseg];
   const uint32_t c = sp.chunk;
-  const DChunk& C = a.ch[c];
+  // the chunk descriptor, copied to shared memory by the last warp while the
+  // other threads stage the segment's bytes (read after the unit-table barriers)
+  __shared__ __align__(8) DChunk sC;
+  const DChunk& C = sC;
   __shared__ unsigned long long s_err;
   __shared__ double s_eb;
   DROLE(blockIdx.x, 1);
-  const uint32_t D = C.dim;
+  const uint32_t D = sp.dim;
+  __shared__ uint8_t s_hdr[32];
+  if (threadIdx.x >= blockDim.x - 32) {  // with the header bytes, in the same round
+    const uint32_t l = threadIdx.x - (blockDim.x - 32);
+    if (l < sizeof(DChunk) / 8)
+      reinterpret_cast<unsigned long long*>(&sC)[l] = __ldg(reinterpret_cast<const unsigned long long*>(a.ch + c) + l);
+    s_hdr[l] = (!a.payload_only && l < kHeader && l < sp.length) ? __ldg(sp.in + l) : 0;
+  }
   const uint32_t kUnitCap = vlz_unit_cap(a.vlz_dmax);
   uint8_t* B = smem;                                                          // staged bytes (set below)
   uint16_t* uend = reinterpret_cast<uint16_t*>(smem + vlz_bytes_cap(a.vlz_dmax));  // unit terminal byte
@@ -1144,9 +1175,9 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   uint32_t* lit = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(J) + kLift * kSeg * 2);  // literal tokens (<= kSeg/2)
   // the payload's place follows from the plan (the host cut the segments from
   // length - header); the header is validated by thread 0 while the bytes load
-  const uint64_t poff = C.payload_only ? 0 : kHeader;
-  const uint8_t* p = C.in + poff;
-  const uint64_t L = C.length - poff;
+  const uint64_t poff = a.payload_only ? 0 : kHeader;
+  const uint8_t* p = sp.in + poff;
+  const uint64_t L = sp.length - poff;
   const uint32_t b0 = sp.seg * kSeg;
   const uint32_t nb = static_cast<uint32_t>(umin64(kSeg, L - b0));
   const uint32_t sb = b0 >= kSegBack ? b0 - kSegBack : 0;
@@ -1176,12 +1207,15 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   if (threadIdx.x == 0) {
     s_bad = 0;
     s_nlit = 0;
-    const DecState S = parse_chunk(C);
+  }
+  __syncthreads();
+  // header check (parse_chunk on the staged header bytes); its verdict is
+  // read before the segment publishes anything
+  if (threadIdx.x == 0) {
+    const DecState S = parse_chunk_hb(C, s_hdr);
     s_err = S.err;
     s_eb = S.eb;
   }
-  __syncthreads();
-  if (s_err != ~0ull) return;  // every CTA of the chunk sees it: nobody waits on this segment
   DTS(blockIdx.x, 2);
   // unit table: terminal bytes at payload offsets [b0, b0 + nb + la)
   uint32_t nu = 0, U = 0;
@@ -1258,6 +1292,7 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
     }
   }
   DTS(blockIdx.x, 4);
+  if (s_err != ~0ull) return;  // every CTA of the chunk sees it: nobody waits on this segment
   // entry -> (exit offset into the next segment, tokens) for entries 0..D
   uint32_t* mymap = a.maps + C.map_base + static_cast<uint64_t>(sp.seg) * (D + 1);
   for (uint32_t e = threadIdx.x; e <= D; e += blockDim.x) {
@@ -1516,9 +1551,18 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   __shared__ uint32_t G[kMaxGroups][32], BM[32];
   __shared__ unsigned long long s_in;
   __shared__ int s_use;
-  const uint32_t c = a.hblk_chunk[gb];
-  const DChunk& C = a.ch[c];
-  const uint32_t b = gb - C.blk0;
+  const HBlkDesc hd = a.hblk[gb];
+  const uint32_t c = hd.chunk;
+  // the chunk descriptor, copied to shared memory by the last warp while the
+  // chunk's first bytes load (read after the barrier below)
+  __shared__ __align__(8) DChunk sC;
+  const DChunk& C = sC;
+  if (threadIdx.x >= blockDim.x - 32) {
+    const uint32_t l = threadIdx.x - (blockDim.x - 32);
+    if (l < sizeof(DChunk) / 8)
+      reinterpret_cast<unsigned long long*>(&sC)[l] = __ldg(reinterpret_cast<const unsigned long long*>(a.ch + c) + l);
+  }
+  const uint32_t b = hd.blk;
   const uint32_t hsub = a.hsub, SB = a.sbits, SW = SB / 32, hbits = hsub * SB, hwords = kHPre + hbits / 32 + 4;
   uint32_t* lut = reinterpret_cast<uint32_t*>(smem);
   uint16_t* luta = reinterpret_cast<uint16_t*>(lut + (1u << kL0));  // two-codeword steps (lengths only)
@@ -1576,7 +1620,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   // the chunk's first bytes (header, codebook of up to 64 entries) in one round
   __shared__ __align__(8) uint8_t s_hb[kLocalHdr + 8];
   __shared__ uint64_t s_vals[64], s_starts[128];
-  for (uint32_t k = threadIdx.x; k < kLocalHdr; k += blockDim.x) s_hb[k] = k < C.length ? __ldg(C.in + k) : 0;
+  for (uint32_t k = threadIdx.x; k < kLocalHdr; k += blockDim.x) s_hb[k] = k < hd.length ? __ldg(hd.in + k) : 0;
   __syncthreads();
   const uint64_t poff = C.payload_only ? 0 : kHeader;
   uint64_t boff = 0, nby = 0;
@@ -2238,6 +2282,7 @@ struct PlanArgs {
   const uint64_t* d_off;  // may be null
   SegPair* segs;
   uint32_t* hblk_chunk;
+  HBlkDesc* hblk;
   uint32_t* dcount;       // [0] vlz segments, [1] huffman blocks
   uint32_t n, hsub, sbits;
 };
@@ -2298,8 +2343,11 @@ __global__ void __launch_bounds__(1024) k_dec_plan(PlanArgs p) {
       C.blk0 = static_cast<uint32_t>(s_carry[3] + e3);
       C.nblk = static_cast<uint32_t>(nblk);
       p.ch[c] = C;
-      for (uint32_t k = 0; k < nseg; ++k) p.segs[C.seg0 + k] = SegPair{c, k};
-      for (uint32_t k = 0; k < nblk; ++k) p.hblk_chunk[C.blk0 + k] = c;
+      for (uint32_t k = 0; k < nseg; ++k) p.segs[C.seg0 + k] = SegPair{c, k, C.in, static_cast<uint32_t>(C.length), C.dim};
+      for (uint32_t k = 0; k < nblk; ++k) {
+        p.hblk_chunk[C.blk0 + k] = c;
+        p.hblk[C.blk0 + k] = HBlkDesc{c, k, C.in, C.length};
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -2361,6 +2409,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   std::vector<RawTile> raw_tiles;
   std::vector<SegPair> segs;
   std::vector<uint32_t> hblk, ctiles;
+  std::vector<HBlkDesc> hdesc;
   uint64_t map_total = 0, row_total = 0, tab_total = 0, huf_subs = 0, huf_vals = 0, nseg_dev = 0;
   const uint64_t hdr = payload_only ? 0 : kHeader;
   for (uint32_t c = 0; c < n; ++c) {
@@ -2409,7 +2458,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
         map_total += static_cast<uint64_t>(C.nseg) * (r.dim + 1);
         C.row_base = row_total;
         row_total += r.count;
-        for (uint32_t s = 0; s < C.nseg; ++s) segs.push_back(SegPair{c, s});
+        for (uint32_t s = 0; s < C.nseg; ++s) segs.push_back(SegPair{c, s, C.in, static_cast<uint32_t>(C.length), C.dim});
         const uint32_t per = copy_tile_rows(r);
         for (uint32_t r0 = 0; r0 < r.count; r0 += per) {
           ctiles.push_back(c);
@@ -2448,7 +2497,10 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
     C.nsub = nsub;
     C.nblk = (C.nsub + hsub - 1) / hsub;
     C.blk0 = static_cast<uint32_t>(hblk.size());
-    for (uint32_t k = 0; k < C.nblk; ++k) hblk.push_back(c);
+    for (uint32_t k = 0; k < C.nblk; ++k) {
+      hblk.push_back(c);
+      hdesc.push_back(HBlkDesc{c, k, C.in, C.length});
+    }
   }
   if (dev && (nseg_dev >= (1ull << 31) || nhb_dev >= (1ull << 31)))
     return set_error(ctx, EMBC_ERR_UNSUPPORTED, 0, 0, 0, 0, 0, "chunk capacities beyond the device-planned decode");
@@ -2465,6 +2517,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   const size_t o_raw = take(sizeof(RawTile) * (raw_tiles.size() + 1));
   const size_t o_segs = take(sizeof(SegPair) * (nseg + 1));
   const size_t o_hblk = take(sizeof(uint32_t) * (nhb + 1));
+  const size_t o_hdesc = take(sizeof(HBlkDesc) * (nhb + 1));
   const size_t o_ct = take(sizeof(uint32_t) * (ctiles.size() + 1));
   const size_t o_flags = take(sizeof(uint32_t) * (6 * n + 4));  // vflag | hflag | ready | cnt | vdone | hdone | tickets
   const size_t o_sst = take(sizeof(unsigned long long) * (nseg + 1));
@@ -2489,6 +2542,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   if (!dev) {
     std::memcpy(hs + o_segs, segs.data(), sizeof(SegPair) * nseg);
     std::memcpy(hs + o_hblk, hblk.data(), sizeof(uint32_t) * nhb);
+    std::memcpy(hs + o_hdesc, hdesc.data(), sizeof(HBlkDesc) * nhb);
   }
   std::memcpy(hs + o_ct, ctiles.data(), sizeof(uint32_t) * ctiles.size());
   uint8_t* d = ctx->d_scratch;
@@ -2499,6 +2553,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   a.st = reinterpret_cast<DecState*>(d + o_st);
   a.segs = reinterpret_cast<const SegPair*>(d + o_segs);
   a.hblk_chunk = reinterpret_cast<const uint32_t*>(d + o_hblk);
+  a.hblk = reinterpret_cast<const HBlkDesc*>(d + o_hdesc);
   a.raw = reinterpret_cast<const RawTile*>(d + o_raw);
   a.ctile = reinterpret_cast<const uint32_t*>(d + o_ct);
   uint32_t* flags = reinterpret_cast<uint32_t*>(d + o_flags);
@@ -2530,6 +2585,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
   a.vlz_dmax = dmax;
   a.hsub = hsub;
   a.sbits = sbits;
+  a.payload_only = payload_only ? 1 : 0;
   a.local_tables = small_call ? 1 : 0;
   uint32_t smem = std::max<uint32_t>(std::max<uint32_t>(nseg ? vlz_smem(dmax) : 0, nhb ? huff_smem(hsub, sbits) : 0), 16384);
   a.smem_bytes = smem;
@@ -2540,6 +2596,7 @@ embc_status decode(embc_ctx* ctx, const uint8_t* d_in, const embc_chunk_ref* ref
     pa.d_off = d_off;
     pa.segs = reinterpret_cast<SegPair*>(d + o_segs);
     pa.hblk_chunk = reinterpret_cast<uint32_t*>(d + o_hblk);
+    pa.hblk = reinterpret_cast<HBlkDesc*>(d + o_hdesc);
     pa.dcount = reinterpret_cast<uint32_t*>(d + o_dcount);
     pa.n = n;
     pa.hsub = hsub;
