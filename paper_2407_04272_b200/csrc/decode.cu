@@ -629,17 +629,37 @@ __device__ bool huff_tables_local(const DChunk& C, const uint8_t* hb, HTab& tb, 
   // the prefix LUT straight from the canonical tables: a slot is the codeword
   // of length l <= kL0 whose code is its top l bits, else a prefix of a longer
   // codeword (kLong), else no codeword (0)
+  //   Canonical codes of increasing length occupy increasing, contiguous
+  //   slot ranges: length l holds [lim[l-1], lim[l]) with
+  //   lim[l] = (first[l] + count[l]) << (kL0 - l); prefixes of longer codes
+  //   follow up to lim[kL0 + 1]; an incomplete code leaves the rest empty.
+  __shared__ uint32_t s_lim[kL0 + 2];
   const uint32_t ml = tb.max_len;
+  if (threadIdx.x == 0) {
+    uint32_t prev = 0;
+    for (uint32_t l = 1; l <= kL0; ++l) {
+      if (l <= ml && tb.count[l]) prev = (tb.first[l] + tb.count[l]) << (kL0 - l);
+      s_lim[l] = prev;
+    }
+    uint32_t endl = prev;
+    for (uint32_t l = kL0 + 1; l <= ml; ++l)
+      if (tb.count[l])
+        endl = max(endl, static_cast<uint32_t>(((static_cast<uint64_t>(tb.first[l]) + tb.count[l] - 1) >> (l - kL0)) + 1));
+    s_lim[kL0 + 1] = endl;
+  }
+  __syncthreads();
+  uint32_t lim[kL0 + 2];
+#pragma unroll
+  for (uint32_t l = 1; l <= kL0 + 1; ++l) lim[l] = s_lim[l];
   for (uint32_t sl = threadIdx.x; sl < (1u << kL0); sl += blockDim.x) {
     uint32_t ent = 0;
-    for (uint32_t l = 1; l <= min(ml, kL0) && !ent; ++l) {
-      const uint32_t d = (sl >> (kL0 - l)) - tb.first[l];
-      if (d < tb.count[l]) ent = ((tb.base[l] + d) << 6) | l;
-    }
-    for (uint32_t l = kL0 + 1; l <= ml && !ent; ++l) {
-      if (!tb.count[l]) continue;
-      const uint64_t f = tb.first[l];
-      if (sl >= (f >> (l - kL0)) && sl <= ((f + tb.count[l] - 1) >> (l - kL0))) ent = kLong;
+    if (sl < lim[kL0]) {
+      uint32_t l = 1;
+#pragma unroll
+      for (uint32_t k = 1; k < kL0; ++k) l += sl >= lim[k] ? 1u : 0u;
+      ent = ((tb.base[l] + (sl >> (kL0 - l)) - tb.first[l]) << 6) | l;
+    } else if (sl < lim[kL0 + 1]) {
+      ent = kLong;
     }
     lut[sl] = ent;
   }
