@@ -2408,13 +2408,13 @@ cudaError_t decode_set_attributes() {
 // plan is computed on the device (k_dec_plan), and k_dec_main runs as
 // persistent CTAs over the device-counted roles: no host read of the lengths,
 // so the call is graph-capturable.
-// Rows per copy tile: ~8192 values when the chunk's roots are resolved in
+// Rows per copy tile: ~16384 values when the chunk's roots are resolved in
 // shared memory by its last segment (the tiles only copy); larger tiles when
 // they must pointer-jump through L2 themselves (each tile pays the same number
 // of dependent rounds whatever its size)
 static uint32_t copy_tile_rows(const embc_chunk_ref& r) {
   const uint32_t d = std::max<uint32_t>(r.dim, 1);
-  const uint32_t per = std::max<uint32_t>(8, std::min<uint32_t>(4096, 8192 / d));
+  const uint32_t per = std::max<uint32_t>(8, std::min<uint32_t>(4096, 16384 / d));
   if (static_cast<uint64_t>(r.count) * 4 > kDecSmem) return std::max(per, std::min<uint32_t>(4096, 131072 / d));
   return per;
 }
