@@ -1744,81 +1744,134 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
       ++n;
     }
   };
-  // ---- A
+  // ---- A.  Codes of at most 8 bits (the near-fixed-length books of the
+  //      benchmarked tables among them, which self-synchronise slowly): every
+  //      subsequence's full map, the state after it for each of the R entry
+  //      offsets (Gs[i][16 + e]) -- the chain from offset 0 with its starts,
+  //      the others until they land on one -- so the group walks below are a
+  //      lookup per step.  Longer codes: a warmed-up chain per subsequence and
+  //      the chain from the previous exit (A2), the walks decode the rest.
   const uint32_t i_me = threadIdx.x;
-  if (i_me < nloc) {
-    const uint64_t gbase = bit0 + static_cast<uint64_t>(i_me) * SB;
-    const SubWin win(W, kHPre + SW * i_me);  // the subsequence starts at word kHPre + SW i
-    uint64_t bm = 0;
-    uint32_t x0 = 0;
-    // warm-up from 64 bits earlier (none at the very start of the stream)
-    int p = gbase == 0 ? 0 : -64;
-    for (;;) {
-      if (p < 0) {
-        const uint32_t bits = win.peek(p);
+  const bool fm = R <= 8;
+  if (fm) {
+    if (i_me < nloc) {
+      const uint64_t gbase = bit0 + static_cast<uint64_t>(i_me) * SB;
+      const SubWin win(W, kHPre + SW * i_me);
+      uint64_t bm = 0;
+      uint32_t x0 = 0, q = 0, cnt = 0;
+      for (;;) {
+        if (q >= SB) {
+          x0 = pk(q - SB, 0, cnt);
+          break;
+        }
+        if (gbase + q >= nbits) {
+          x0 = pk(0, 2, cnt);
+          break;
+        }
+        const uint32_t bits = win.peek(static_cast<int>(q));
         const uint32_t la = luta[bits >> (32 - kL0)];
-        if ((la >> 10) == 2 && p + static_cast<int>(la & 31) < 0) {  // both start before the subsequence
-          p += static_cast<int>((la & 31) + ((la >> 5) & 31));
-          continue;
+        if ((la >> 10) == 2) {
+          const uint32_t l1 = la & 31, l12 = l1 + ((la >> 5) & 31);
+          if (q + l1 < SB && gbase + q + l12 <= nbits) {
+            bm |= (1ull << q) | (1ull << (q + l1));
+            q += l12;
+            cnt += 2;
+            continue;
+          }
         }
         uint32_t len = 0;
         if (decode_one(lut, t, bits, &len) < 0) {
-          p = 0;  // the early chain died: start at the subsequence itself
+          x0 = pk(0, 1, cnt);
+          break;
+        }
+        if (gbase + q + len > nbits) {
+          x0 = pk(0, 2, cnt);
+          break;
+        }
+        bm |= 1ull << q;
+        q += len;
+        ++cnt;
+      }
+      Gs[i_me][16] = x0;
+      for (uint32_t e = 1; e < R; ++e)
+        Gs[i_me][16 + e] = ((bm >> e) & 1) ? pk(pk_off(x0), pk_term(x0), pk_cnt(x0) - popc_below(bm, e))
+                                            : run(i_me, e, bm, x0);
+    }
+  } else {
+    if (i_me < nloc) {
+      const uint64_t gbase = bit0 + static_cast<uint64_t>(i_me) * SB;
+      const SubWin win(W, kHPre + SW * i_me);  // the subsequence starts at word kHPre + SW i
+      uint64_t bm = 0;
+      uint32_t x0 = 0;
+      // warm-up from 64 bits earlier (none at the very start of the stream)
+      int p = gbase == 0 ? 0 : -64;
+      for (;;) {
+        if (p < 0) {
+          const uint32_t bits = win.peek(p);
+          const uint32_t la = luta[bits >> (32 - kL0)];
+          if ((la >> 10) == 2 && p + static_cast<int>(la & 31) < 0) {  // both start before the subsequence
+            p += static_cast<int>((la & 31) + ((la >> 5) & 31));
+            continue;
+          }
+          uint32_t len = 0;
+          if (decode_one(lut, t, bits, &len) < 0) {
+            p = 0;  // the early chain died: start at the subsequence itself
+            continue;
+          }
+          p += static_cast<int>(len);
           continue;
         }
-        p += static_cast<int>(len);
-        continue;
-      }
-      break;
-    }
-    uint32_t q = static_cast<uint32_t>(p), cnt = 0;
-    for (;;) {
-      if (q >= SB) {
-        x0 = pk(q - SB, 0, cnt);
         break;
       }
-      if (gbase + q >= nbits) {
-        x0 = pk(0, 2, cnt);
-        break;
-      }
-      const uint32_t bits = win.peek(static_cast<int>(q));
-      const uint32_t la = luta[bits >> (32 - kL0)];
-      if ((la >> 10) == 2) {  // two codewords, the second starting inside the subsequence
-        const uint32_t l1 = la & 31, l12 = l1 + ((la >> 5) & 31);
-        if (q + l1 < SB && gbase + q + l12 <= nbits) {
-          bm |= (1ull << q) | (1ull << (q + l1));
-          q += l12;
-          cnt += 2;
-          continue;
+      uint32_t q = static_cast<uint32_t>(p), cnt = 0;
+      for (;;) {
+        if (q >= SB) {
+          x0 = pk(q - SB, 0, cnt);
+          break;
         }
+        if (gbase + q >= nbits) {
+          x0 = pk(0, 2, cnt);
+          break;
+        }
+        const uint32_t bits = win.peek(static_cast<int>(q));
+        const uint32_t la = luta[bits >> (32 - kL0)];
+        if ((la >> 10) == 2) {  // two codewords, the second starting inside the subsequence
+          const uint32_t l1 = la & 31, l12 = l1 + ((la >> 5) & 31);
+          if (q + l1 < SB && gbase + q + l12 <= nbits) {
+            bm |= (1ull << q) | (1ull << (q + l1));
+            q += l12;
+            cnt += 2;
+            continue;
+          }
+        }
+        uint32_t len = 0;
+        if (decode_one(lut, t, bits, &len) < 0) {
+          x0 = pk(0, 1, cnt);
+          break;
+        }
+        if (gbase + q + len > nbits) {
+          x0 = pk(0, 2, cnt);
+          break;
+        }
+        bm |= 1ull << q;
+        q += len;
+        ++cnt;
       }
-      uint32_t len = 0;
-      if (decode_one(lut, t, bits, &len) < 0) {
-        x0 = pk(0, 1, cnt);
-        break;
-      }
-      if (gbase + q + len > nbits) {
-        x0 = pk(0, 2, cnt);
-        break;
-      }
-      bm |= 1ull << q;
-      q += len;
-      ++cnt;
+      B0[i_me] = bm;
+      X0[i_me] = x0;
     }
-    B0[i_me] = bm;
-    X0[i_me] = x0;
-  }
-  __syncthreads();
-  if (i_me < nloc) {
-    uint32_t r = 0xFFFFFFFFu, y = 0;
-    if (i_me > 0 && !pk_term(X0[i_me - 1])) {
-      r = pk_off(X0[i_me - 1]);
-      const uint64_t bm = B0[i_me];
-      const uint32_t x0 = X0[i_me];
-      y = ((bm >> r) & 1) ? pk(pk_off(x0), pk_term(x0), pk_cnt(x0) - popc_below(bm, r)) : run(i_me, r, bm, x0);
+    __syncthreads();
+    if (i_me < nloc) {
+      uint32_t r = 0xFFFFFFFFu, y = 0;
+      if (i_me > 0 && !pk_term(X0[i_me - 1])) {
+        r = pk_off(X0[i_me - 1]);
+        const uint64_t bm = B0[i_me];
+        const uint32_t x0 = X0[i_me];
+        y = ((bm >> r) & 1) ? pk(pk_off(x0), pk_term(x0), pk_cnt(x0) - popc_below(bm, r)) : run(i_me, r, bm, x0);
+      }
+      Ye[i_me] = r;
+      Y0[i_me] = y;
     }
-    Ye[i_me] = r;
-    Y0[i_me] = y;
   }
   __syncthreads();
   DTS(blockIdx.x, 3);
@@ -1840,18 +1893,22 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
       const uint32_t i = g * gs + j;
       const bool live = gval && i < nloc;
       if (live) Gs[i][el] = pk(e, term, cnt);
-      // lanes of a group that reached the same entry share one result
-      const uint32_t peers = __match_any_sync(0xffffffffu, (term || !live) ? 0xFFFFFFFFu : (half << 5) | e);
-      const int leader = __ffs(peers) - 1;
       uint32_t f = 0;
-      if (live && !term && static_cast<int>(lane) == leader) {
-        const uint64_t sbm = B0[i];
-        const uint32_t sx = X0[i];
-        if ((sbm >> e) & 1) f = pk(pk_off(sx), pk_term(sx), pk_cnt(sx) - popc_below(sbm, e));
-        else if (Ye[i] == e) f = Y0[i];
-        else f = run(i, e, sbm, sx);
+      if (fm) {
+        if (live && !term) f = Gs[i][16 + e];  // the subsequence's full map
+      } else {
+        // lanes of a group that reached the same entry share one result
+        const uint32_t peers = __match_any_sync(0xffffffffu, (term || !live) ? 0xFFFFFFFFu : (half << 5) | e);
+        const int leader = __ffs(peers) - 1;
+        if (live && !term && static_cast<int>(lane) == leader) {
+          const uint64_t sbm = B0[i];
+          const uint32_t sx = X0[i];
+          if ((sbm >> e) & 1) f = pk(pk_off(sx), pk_term(sx), pk_cnt(sx) - popc_below(sbm, e));
+          else if (Ye[i] == e) f = Y0[i];
+          else f = run(i, e, sbm, sx);
+        }
+        f = __shfl_sync(0xffffffffu, f, leader);
       }
-      f = __shfl_sync(0xffffffffu, f, leader);
       if (live && !term) {
         term = pk_term(f);
         cnt += pk_cnt(f);
