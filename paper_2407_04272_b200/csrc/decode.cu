@@ -1035,6 +1035,12 @@ constexpr unsigned long long kStAgg = 1ull << 62, kStInc = 2ull << 62;
 __device__ __forceinline__ unsigned long long ld_vol(const unsigned long long* p) {
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
+// Status store without a fence: for an aggregate flag whose data every writer
+// fenced before a barrier the storing thread passed, and for inclusive states
+// (values that publish no other data).
+__device__ __forceinline__ void st_flag(unsigned long long* p, unsigned long long v) {
+  *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
 __device__ __forceinline__ void st_vol(unsigned long long* p, unsigned long long v) {
   __threadfence();
   *reinterpret_cast<volatile unsigned long long*>(p) = v;
@@ -1338,7 +1344,7 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   DTS(blockIdx.x, 5);
   unsigned long long* status = a.seg_status;
   if (threadIdx.x < 32) {
-    if (threadIdx.x == 0 && sp.seg > 0) st_vol(status + gseg, kStAgg);
+    if (threadIdx.x == 0 && sp.seg > 0) st_flag(status + gseg, kStAgg);  // maps fenced before the barrier
     unsigned long long in;
     if (sp.seg == 0) {
       in = vlz_state(false, 0, 0);
@@ -1380,7 +1386,7 @@ __device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
           if (ro > C.count) dead = true;  // more tokens than vectors: trailing bytes
         }
       }
-      st_vol(status + gseg, kStInc | vlz_state(dead, eo, ro));
+      st_flag(status + gseg, kStInc | vlz_state(dead, eo, ro));
       s_in = in;
     }
   }
@@ -1941,7 +1947,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
     a.bmaps[static_cast<uint64_t>(gb) * 32 + lane] = bm;
     __threadfence();
     __syncwarp();
-    if (lane == 0 && b > 0) st_vol(status + gb, kStAgg);
+    if (lane == 0 && b > 0) st_flag(status + gb, kStAgg);  // maps fenced before the warp barrier
     unsigned long long in;
     if (b == 0) {
       in = huf_state(0, 0, 0);
@@ -1977,7 +1983,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
         cc += pk_cnt(f);
         ee = pk_off(f);
       }
-      st_vol(status + gb, kStInc | huf_state(tm, ee, cc));
+      st_flag(status + gb, kStInc | huf_state(tm, ee, cc));
       // fewer decodable symbols than the count: exhaustion / invalid prefix
       // (huffman.hpp:274-288) -> the exact walker reports it
       if (b == C.nblk - 1 && cc < C.N) atomicOr(&a.hflag[c], 1u);
