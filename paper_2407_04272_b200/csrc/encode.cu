@@ -1065,8 +1065,9 @@ __device__ __forceinline__ uint64_t look_back(const unsigned long long* status, 
   return acc + base;
 }
 
+// Look-back status words carry their value (tile bits, job offsets) and
+// publish no other data: a volatile store, no fence.
 __device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
-  __threadfence();
   *reinterpret_cast<volatile unsigned long long*>(p) = v;
 }
 
