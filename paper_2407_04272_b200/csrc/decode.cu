@@ -1064,7 +1064,7 @@ __device__ __forceinline__ uint32_t find_inclusive(const unsigned long long* sta
     const uint32_t need = fi == 32 ? 0xffffffffu : ((2u << fi) - 1);
     if (zero & need) {  // a predecessor has not published yet: back off, re-read
       __nanosleep(delay);
-      delay = min(delay * 2, 256u);
+      delay = min(delay * 2, kPollMaxNs);
       continue;
     }
     if (fi < 32) {
@@ -1673,7 +1673,7 @@ __device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
       uint32_t delay = 32;
       while (!*reinterpret_cast<volatile uint32_t*>(&a.ready[c])) {
         __nanosleep(delay);
-        delay = min(delay * 2, 256u);
+        delay = min(delay * 2, kPollMaxNs);
       }
       __threadfence();
       const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&a.st[c].err);
@@ -2089,7 +2089,7 @@ __device__ __forceinline__ void wait_count(const uint32_t* cnt, uint32_t n) {
   uint32_t delay = 32;
   while (*reinterpret_cast<const volatile uint32_t*>(cnt) < n) {
     __nanosleep(delay);
-    delay = min(delay * 2, 256u);
+    delay = min(delay * 2, kPollMaxNs);
   }
   __threadfence();
 }

@@ -54,6 +54,12 @@ struct JobState {
 enum : uint32_t { JF_ABORT = 1u };
 
 // Per-chunk decode descriptor (host-planned; shapes come from metadata).
+// longest sleep between two polls of a flag another CTA of the launch sets (ns)
+#ifndef EMBC_POLL_MAX_NS
+#define EMBC_POLL_MAX_NS 256u
+#endif
+constexpr uint32_t kPollMaxNs = EMBC_POLL_MAX_NS;
+
 struct DChunk {
   const uint8_t* in;   // start of the serialized chunk (or bare payload)
   uint64_t length;     // bytes of this chunk

@@ -939,7 +939,7 @@ __device__ __forceinline__ void stats_tile(const StatsArgs& a, const uint32_t ti
       uint32_t delay = 32;
       while (!*reinterpret_cast<volatile uint32_t*>(&a.hready[t])) {
         __nanosleep(delay);
-        delay = min(delay * 2, 256u);
+        delay = min(delay * 2, kPollMaxNs);
       }
     }
     __threadfence();
@@ -1751,7 +1751,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_encode(FusedArgs f) {
       uint32_t delay = 32;
       while (!*reinterpret_cast<volatile uint32_t*>(&f.e.st[jid].flags)) {
         __nanosleep(delay);
-        delay = min(delay * 2, 256u);
+        delay = min(delay * 2, kPollMaxNs);
       }
       __threadfence();
     }
