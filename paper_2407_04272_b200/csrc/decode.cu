@@ -48,6 +48,16 @@
 
 namespace embc_dev {
 
+// Rarely executed paths (sequential walkers, big-codebook tables, the error
+// fold) and, optionally, the roles are kept out of line so the hot code of
+// the roles resident on an SM stays compact in the instruction cache.
+#ifndef EMBC_COLD
+#define EMBC_COLD __device__ __noinline__
+#endif
+#ifndef EMBC_ROLE
+#define EMBC_ROLE __device__
+#endif
+
 #include "decode_timeline.cuh"  // EMBC_DEBUG builds only: per-role device timestamps
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
@@ -263,7 +273,7 @@ __device__ __forceinline__ bool rd_varint(const uint8_t* p, uint64_t L, uint64_t
   return false;
 }
 
-__device__ __forceinline__ void k_dec_vlz_seq_cta(uint32_t bid, const DChunk* __restrict__ ch, DecState* __restrict__ st,
+EMBC_COLD void k_dec_vlz_seq_cta(uint32_t bid, const DChunk* __restrict__ ch, DecState* __restrict__ st,
                               const uint32_t* list, const volatile uint32_t* vflag) {
   if (threadIdx.x != 0) return;
   const uint32_t c = bid;
@@ -671,7 +681,7 @@ __device__ bool huff_tables_local(const DChunk& C, const uint8_t* hb, HTab& tb, 
   return true;
 }
 
-__device__ void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState& S,
+EMBC_COLD void huff_tables(uint32_t c, const DChunk* __restrict__ ch, DecState& S,
                             uint64_t* __restrict__ keys, uint8_t* __restrict__ tabs,
                             uint32_t* __restrict__ hflag, uint64_t* skey, uint32_t skey_cap) {
   __shared__ unsigned long long s_tmp64[33];
@@ -956,7 +966,7 @@ __device__ __forceinline__ uint32_t popc_below(uint64_t bm, uint32_t p) {
 }
 // Exact sequential walk (huffman.hpp:274-290) for flagged chunks: reproduces
 // the reference's first error (exhaustion / invalid prefix / count).
-__device__ __forceinline__ void k_dec_huff_seq_cta(uint32_t bid, const DChunk* __restrict__ ch, DecState* __restrict__ st,
+EMBC_COLD void k_dec_huff_seq_cta(uint32_t bid, const DChunk* __restrict__ ch, DecState* __restrict__ st,
                                const uint32_t* list, uint8_t* tabs, const volatile uint32_t* hflag) {
   if (threadIdx.x != 0) return;
   const uint32_t c = bid;
@@ -1005,7 +1015,7 @@ __device__ __forceinline__ void k_dec_huff_seq_cta(uint32_t bid, const DChunk* _
 // D9: fold the lowest failing chunk into the sticky record.
 // ---------------------------------------------------------------------------
 // The lowest failing chunk -> the sticky record (all threads of the CTA scan).
-__device__ void dec_fold(const DecState* __restrict__ st, uint32_t n, DevError* err) {
+EMBC_COLD void dec_fold(const DecState* __restrict__ st, uint32_t n, DevError* err) {
   __shared__ uint32_t s_first;
   if (threadIdx.x == 0) s_first = 0xFFFFFFFFu;
   __syncthreads();
@@ -1172,7 +1182,7 @@ __device__ void vlz_end_check(const DecArgs& a, uint32_t c);
 __device__ __forceinline__ bool vlz_roots_local(const DecArgs& a, const DChunk& C);
 __device__ void vlz_resolve_roots(const DecArgs& a, const DChunk& C, uint8_t* smem);
 
-__device__ void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
+EMBC_ROLE void vlz_segment(const DecArgs& a, uint32_t gseg, uint8_t* smem) {
   __shared__ uint32_t s_tmp32[33];
   __shared__ uint32_t s_bad, s_nlit, s_first_start;
   __shared__ unsigned long long s_in;
@@ -1572,7 +1582,7 @@ __device__ __forceinline__ unsigned long long huf_state(uint32_t term, uint32_t 
 //     the chunk's earlier blocks.
 //  C  with the true entry known, every subsequence decodes its symbols into
 //     shared memory; the block stores them coalesced.
-__device__ void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
+EMBC_ROLE void huff_block(const DecArgs& a, uint32_t gb, uint8_t* smem) {
   __shared__ HTab t;
   __shared__ uint32_t G[kMaxGroups][32], BM[32];
   __shared__ unsigned long long s_in;
@@ -2148,7 +2158,7 @@ __device__ void copy_ref_rows(const DChunk& C, const uint32_t* V, uint32_t r0, u
 
 // Reference rows <- their root rows, for one tile of a vlz chunk's rows, once
 // every segment of the chunk (and the roots tail) has finished.
-__device__ void copy_tile(const DecArgs& a, uint32_t b, uint8_t* smem) {
+EMBC_ROLE void copy_tile(const DecArgs& a, uint32_t b, uint8_t* smem) {
   {
     __shared__ int s_skip;
     const uint32_t c = a.ctile[3 * b];
@@ -2218,7 +2228,7 @@ __device__ void copy_tile(const DecArgs& a, uint32_t b, uint8_t* smem) {
 // Per chunk, once its parallel decode has finished: the exact sequential
 // walker when the chunk was planned sequential or the parallel path flagged
 // it; the last chunk to finish folds the first failure into the error record.
-__device__ void finish_chunk(const DecArgs& a, uint32_t c) {
+EMBC_ROLE void finish_chunk(const DecArgs& a, uint32_t c) {
   const uint8_t codec = a.ch[c].codec;
   if (threadIdx.x == 0) {
     wait_count(&a.ready[c], 1);
