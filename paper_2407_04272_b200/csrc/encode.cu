@@ -188,32 +188,38 @@ __device__ void book_warp(const DJob& J, JobState* Sp, const BookArgs& a, uint64
   for (uint32_t i = lane; i < nsym; i += 32) w32[i] = static_cast<uint32_t>(key[i] >> 32);
   __syncwarp();
   if (nsym > 1 && lane == 0) {
-    // the merged queue's weights are created in non-decreasing order; the two
-    // heads of each queue live in registers (wm == w32[mh] while mh < size,
-    // wm1 == w32[mh + 1] while mh + 1 < size), so no load is on the chain
+    // the merged queue's weights are created in non-decreasing order; three
+    // heads of each queue live in registers (wl_k == w32[lh + k] while
+    // lh + k < n, wm_k == w32[mh + k] while mh + k < size) and each pick
+    // loads the head three places on, so no load is on the chain; a merged
+    // head not yet created is set from the new node's weight when it is
     const uint32_t n = nsym, total = 2 * n - 1;
     uint32_t size = n, lh = 0, mh = n;
-    uint32_t wl = w32[0], wl_next = n > 1 ? w32[1] : 0, wm = 0, wm1 = 0;
+    uint32_t wl0 = w32[0], wl1 = w32[min(1u, n - 1)], wl2 = w32[min(2u, n - 1)], wm0 = 0, wm1 = 0, wm2 = 0;
     while (size < total) {
       uint32_t ab[2];
       uint32_t w2 = 0;
 #pragma unroll
       for (int k = 0; k < 2; ++k) {  // branch-free pick: selects, loads issued unconditionally
-        const bool tl = lh < n && (mh >= size || wl <= wm);
+        const bool tl = lh < n && (mh >= size || wl0 <= wm0);
         ab[k] = tl ? lh : mh;
-        w2 += tl ? wl : wm;
+        w2 += tl ? wl0 : wm0;
         lh += tl ? 1u : 0u;
         mh += tl ? 0u : 1u;
-        const uint32_t ln = w32[min(lh + 1, n - 1)];
-        const uint32_t mn = w32[min(mh + 1, total - 1)];
-        wl = tl ? wl_next : wl;
-        wl_next = tl ? ln : wl_next;
-        wm = tl ? wm : wm1;
-        wm1 = tl ? wm1 : mn;
+        const uint32_t ln = w32[min(lh + 2, n - 1)];
+        const uint32_t mn = w32[min(mh + 2, total - 1)];
+        wl0 = tl ? wl1 : wl0;
+        wl1 = tl ? wl2 : wl1;
+        wl2 = tl ? ln : wl2;
+        wm0 = tl ? wm0 : wm1;
+        wm1 = tl ? wm1 : wm2;
+        wm2 = tl ? wm2 : mn;
       }
       w32[size] = w2;
-      if (mh == size) wm = w2;  // the new node is the merged head
-      else if (mh + 1 == size) wm1 = w2;
+      const uint32_t d = size - mh;  // the new node's place among the merged heads
+      wm0 = d == 0 ? w2 : wm0;
+      wm1 = d == 1 ? w2 : wm1;
+      wm2 = d == 2 ? w2 : wm2;
       parent[ab[0]] = static_cast<int32_t>(size);
       parent[ab[1]] = static_cast<int32_t>(size);
       ++size;
@@ -223,15 +229,31 @@ __device__ void book_warp(const DJob& J, JobState* Sp, const BookArgs& a, uint64
   __syncwarp();
   TS1(9);
   // 4. lengths = leaf depth; the first leaf (sorted order) past 32 bits fails (huffman.hpp:110-118)
+  //    Each lane walks two leaves' parent chains side by side.
   unsigned long long cap = ~0ull, bits = 0;
-  for (uint32_t i = lane; i < nsym; i += 32) {
-    uint32_t depth = 0;
-    if (nsym == 1) depth = 1;
-    else
-      for (int32_t q = parent[i]; q != -1; q = parent[q]) ++depth;
-    if (depth > 32) cap = min(cap, (static_cast<unsigned long long>(i) << 32) | depth);
-    bits += (key[i] >> 32) * depth;  // count x code length: the payload bits
-    key[i] = (static_cast<uint64_t>(depth > 32 ? 63 : depth) << 32) | (key[i] & 0xFFFFFFFFull);
+  for (uint32_t i0 = 0; i0 < nsym; i0 += 64) {
+    const uint32_t ia = i0 + lane, ib = ia + 32;
+    uint32_t da = 0, db = 0;
+    if (nsym == 1) {
+      da = 1;
+    } else {
+      int32_t qa = ia < nsym ? parent[ia] : -1, qb = ib < nsym ? parent[ib] : -1;
+      while ((qa & qb) != -1) {  // either chain still below the root
+        const int32_t na = parent[qa < 0 ? 0 : qa], nb = parent[qb < 0 ? 0 : qb];
+        da += qa != -1 ? 1u : 0u;
+        db += qb != -1 ? 1u : 0u;
+        qa = qa != -1 ? na : -1;
+        qb = qb != -1 ? nb : -1;
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t i = h ? ib : ia, depth = h ? db : da;
+      if (i >= nsym) continue;
+      if (depth > 32) cap = min(cap, (static_cast<unsigned long long>(i) << 32) | depth);
+      bits += (key[i] >> 32) * depth;  // count x code length: the payload bits
+      key[i] = (static_cast<uint64_t>(depth > 32 ? 63 : depth) << 32) | (key[i] & 0xFFFFFFFFull);
+    }
   }
   cap = warp_min_u64(cap);
   if (cap != ~0ull) {
@@ -978,7 +1000,15 @@ __device__ __forceinline__ void stats_tile(const StatsArgs& a, const uint32_t ti
   if (MERGED) {  // the job's codebook (or its failure) is final
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t*>(&Sp->flags) = 1;
+    if (threadIdx.x == 0) {
+      // the codebook prices the whole payload (count x length per symbol), so
+      // the job's size is known here: publish it for the job look-back now
+      // rather than after every tile of the job has sized itself in E2 (which
+      // then finds it set).  Job 0 only ever publishes its inclusive offset.
+      if (T.job > 0 && *reinterpret_cast<const volatile unsigned long long*>(&Sp->err) == ~0ull)
+        atomicCAS(a.job_status + T.job * kJobStride, 0ull, kFlagAgg | (J.header + Sp->payload));
+      *reinterpret_cast<volatile uint32_t*>(&Sp->flags) = 1;
+    }
   }
   TS1(4);
 }
@@ -1052,7 +1082,7 @@ __device__ __forceinline__ uint64_t look_back(const unsigned long long* status, 
     if (zero & need) {  // a predecessor has not published yet: back off, re-read
       EMBC_DBG(if (lane == 0) atomicAdd(&g_dbg[stride == 1 ? 0 : 1], 1ull));
       __nanosleep(delay);
-      delay = min(delay * 2, 512u);
+      delay = min(delay * 2, kPollMaxNs);
       continue;
     }
     uint64_t v = (static_cast<int>(lane) <= fi) ? (s & kValMask) : 0;
