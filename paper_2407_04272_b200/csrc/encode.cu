@@ -405,6 +405,8 @@ __device__ void build_book(const DJob& J, JobState* Sp, const BookArgs& a, uint8
   uint8_t* book = a.books + hj * a.book_stride;
   uint64_t* L = a.lut + lut_off;
   TS1(7);
+  TS1V(12, nsym);
+  TS1V(13, span);
   if (p2 <= 256 && in_smem) {  // small alphabets: one warp, no block barriers
     if (threadIdx.x < 32) book_warp(J, Sp, a, key, wgt, parent, nsym, p2, gh, span, cmin, L, book, lut_off);
     return;

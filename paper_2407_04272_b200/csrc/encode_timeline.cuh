@@ -73,8 +73,9 @@ struct EmitEnd {
       for (int k = 0; k < 10; ++k) g_ts[t][k] = 0;
   }
 };
-__device__ unsigned long long g_ts1[16384][12];
+__device__ unsigned long long g_ts1[16384][14];
 #define TS1(k) do { if (threadIdx.x == 0 && blockIdx.x < 16384) g_ts1[blockIdx.x][k] = gtime(); } while (0)
+#define TS1V(k, v) do { if (threadIdx.x == 0 && blockIdx.x < 16384) g_ts1[blockIdx.x][k] = (v); } while (0)
 template <class A>
 __device__ void dbg_stats_report(const A& a) {
   if (threadIdx.x == 0 && atomicAdd(&g_dbg[2], 1ull) == a.ntiles - 1 && (g_dbg[2] = 0, a.ntiles > 100) &&
@@ -96,9 +97,22 @@ __device__ void dbg_stats_report(const A& a) {
     for (uint32_t t = 0; t < a.ntiles; ++t) {
       if (g_ts1[t][4] - g_ts1[t][3] != mb) continue;
       const unsigned long long* g = g_ts1[t];
-      printf("  slowest book: S %llu count %llu compact %llu sort %llu merge %llu depth %llu csort %llu rest %llu\n",
-             g[5] - g[3], g[6] - g[5], g[7] - g[6], g[8] - g[7], g[9] - g[8], g[10] - g[9], g[11] - g[10], g[4] - g[11]);
+      printf("  slowest book: S %llu count %llu compact %llu sort %llu merge %llu depth %llu csort %llu rest %llu"
+             " (nsym %llu span %llu)\n",
+             g[5] - g[3], g[6] - g[5], g[7] - g[6], g[8] - g[7], g[9] - g[8], g[10] - g[9], g[11] - g[10], g[4] - g[11],
+             g[12], g[13]);
     }
+    // book time by alphabet size
+    unsigned long long cnt[6] = {0}, tot[6] = {0}, mxb[6] = {0};
+    for (uint32_t t = 0; t < a.ntiles; ++t) {
+      if (g_ts1[t][4] == g_ts1[t][3]) continue;
+      const unsigned long long ns = g_ts1[t][12], d = g_ts1[t][4] - g_ts1[t][3];
+      const int b = ns <= 8 ? 0 : ns <= 32 ? 1 : ns <= 64 ? 2 : ns <= 128 ? 3 : ns <= 256 ? 4 : 5;
+      ++cnt[b]; tot[b] += d; mxb[b] = max(mxb[b], d);
+    }
+    printf("  books by nsym (<=8,<=32,<=64,<=128,<=256,more): n/mean/max");
+    for (int b = 0; b < 6; ++b) printf(" %llu/%llu/%llu", cnt[b], cnt[b] ? tot[b] / cnt[b] : 0, mxb[b]);
+    printf("\n");
   }
 }
 __device__ __forceinline__ void dbg_kspan_begin() {
@@ -121,4 +135,5 @@ __device__ __forceinline__ void dbg_kspan_end(uint32_t ntiles) {
 #define EMBC_DBG(...) do {} while (0)
 #define TS(k) do {} while (0)
 #define TS1(k) do {} while (0)
+#define TS1V(k, v) do {} while (0)
 #endif
