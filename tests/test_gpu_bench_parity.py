@@ -175,3 +175,80 @@ def test_select_codec_timed_eq2(ctx):
             assert chosen == want, (t, bw, sp)
             if bw < 1.0:
                 assert chosen == pinned
+
+
+def test_pipelined_chain_graph_equals_eager(ctx):
+    """The bench's pipelined schedule as a library user would run it: two codec
+    contexts on two streams, several steps captured in one CUDA graph with no
+    join between steps (compress of k+1 may overlap decode of k; decode of k
+    waits for compress of k only).  Every step's packed bytes and decoded
+    values equal the eager (serial) call's."""
+    prof = W.workload_profiles("kg")
+    T = 26
+    ebs, codecs = [prof[t].eb for t in range(T)], [prof[t].codec for t in range(T)]
+    S = 4
+    sets = []
+    for it in range(S):
+        x = [torch.from_numpy(a).to(DEV) for a in step_inputs("kg", it)]
+        jobs = [K.EncodeJob(x[t], ebs[t], codecs[t]) for t in range(T)]
+        r = K.encode_chunks(jobs, K.LAYOUT_PACKED)
+        want = bytes(r.buffer[: r.total].cpu().numpy().tobytes())
+        table = K.unpack_table(want)
+        y = [torch.empty_like(x[t]) for t in range(T)]
+        refs = []
+        for t, (o, ln) in enumerate(table):
+            cr = _lib.ChunkRef()
+            cr.offset, cr.length, cr.out, cr.dim, cr.count, cr.codec = o, ln, y[t].data_ptr(), 16, x[t].shape[0], codecs[t]
+            refs.append(cr)
+        out = torch.zeros(r.total + 256, dtype=torch.uint8, device=DEV)
+        sets.append({"x": x, "cj": [j.to_c() for j in jobs], "want": want, "y": y, "refs": refs, "out": out})
+    # eager decode of the reference bytes: the values every pipelined decode must reproduce
+    expect = []
+    for s in sets:
+        s["out"][: len(s["want"])].copy_(torch.frombuffer(bytearray(s["want"]), dtype=torch.uint8).to(DEV))
+        ctx.decode_raw(s["out"], s["refs"], K.OUT_F32, False)
+        ctx.sync()
+        expect.append([yy.clone() for yy in s["y"]])
+    for s in sets:
+        s["out"].zero_()
+        for yy in s["y"]:
+            yy.fill_(float("nan"))
+    ectx, dctx = K.Context(0), K.Context(0)
+    ectx.reserve_capture(64 << 20)
+    dctx.reserve_capture(64 << 20)
+    # size the decode context's scratch before capture (as the bench does)
+    for s in sets:
+        s["out"][: len(s["want"])].copy_(torch.frombuffer(bytearray(s["want"]), dtype=torch.uint8).to(DEV))
+        dctx.decode_raw(s["out"], s["refs"], K.OUT_F32, False)
+        ectx.encode_raw(s["cj"], K.LAYOUT_PACKED, s["out"])
+    torch.cuda.synchronize()
+    ectx.sync()
+    dctx.sync()
+    for s in sets:
+        s["out"].zero_()
+        for yy in s["y"]:
+            yy.fill_(float("nan"))
+    torch.cuda.synchronize()
+    s_enc, s_dec, s_cap = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s_cap):
+        s_enc.wait_stream(s_cap)
+        s_dec.wait_stream(s_cap)
+        for k in range(S + 1):  # compress k (k < S) beside decode k - 1 (k > 0)
+            if k < S:
+                ectx.encode_raw(sets[k]["cj"], K.LAYOUT_PACKED, sets[k]["out"], stream=s_enc)
+            if k > 0:
+                dctx.decode_raw(sets[k - 1]["out"], sets[k - 1]["refs"], K.OUT_F32, False, stream=s_dec)
+            if k < S:
+                ev = torch.cuda.Event()
+                ev.record(s_enc)
+                s_dec.wait_event(ev)
+        s_cap.wait_stream(s_enc)
+        s_cap.wait_stream(s_dec)
+    g.replay()
+    torch.cuda.synchronize()
+    for k, s in enumerate(sets):
+        assert bytes(s["out"][: len(s["want"])].cpu().numpy().tobytes()) == s["want"], k
+        for t in range(T):
+            assert torch.equal(s["y"][t], expect[k][t]), (k, t)
+            assert (s["y"][t].double() - s["x"][t].double()).abs().max().item() <= ebs[t]
