@@ -240,6 +240,30 @@ __device__ __forceinline__ void copy_out_staged(uint8_t* dst, const uint8_t* sta
   for (uint64_t k = tail0 + threadIdx.x; k < len; k += blockDim.x) dst[k] = stage[mis + k];
 }
 
+// stage[s0 + k] -> dst[k] for k < len, with a 16-B aligned stage and dst at
+// any alignment: 16-B stores of words funnel-shifted out of the stage.
+__device__ __forceinline__ void copy_out_shifted(uint8_t* dst, const uint8_t* stage, uint32_t s0, uint32_t len) {
+  if (len == 0) return;
+  const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 15);
+  const uint32_t head = min(len, (16u - mis) & 15u);
+  for (uint32_t k = threadIdx.x; k < head; k += blockDim.x) dst[k] = stage[s0 + k];
+  // whole 16-B stores whose five source words lie inside the staged bytes
+  const uint32_t nvec = len >= head + 20 ? (len - head - 4) / 16 : 0;
+  const uint32_t sb = s0 + head, sh = 8 * (sb & 3);
+  const uint32_t* sw = reinterpret_cast<const uint32_t*>(stage) + (sb >> 2);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  for (uint32_t v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const uint32_t x0 = sw[4 * v], x1 = sw[4 * v + 1], x2 = sw[4 * v + 2], x3 = sw[4 * v + 3], x4 = sw[4 * v + 4];
+    uint4 o;
+    o.x = __funnelshift_r(x0, x1, sh);
+    o.y = __funnelshift_r(x1, x2, sh);
+    o.z = __funnelshift_r(x2, x3, sh);
+    o.w = __funnelshift_r(x3, x4, sh);
+    d4[v] = o;
+  }
+  for (uint32_t k = head + 16 * nvec + threadIdx.x; k < len; k += blockDim.x) dst[k] = stage[s0 + k];
+}
+
 // Little-endian scalar stores into a byte array (header fields).
 __device__ __forceinline__ void st_le(uint8_t* p, uint64_t v, int nb) {
   for (int i = 0; i < nb; ++i) p[i] = static_cast<uint8_t>(v >> (8 * i));

@@ -1512,6 +1512,93 @@ __device__ __forceinline__ void emit_tile(const EmitArgs& a, const uint32_t tid,
   const uint64_t hdr = J.header;
   const uint64_t book_bytes = codec == EMBC_CODEC_HUFFMAN ? 12 + 5ull * S.nsym : 0;
   uint64_t pre = 0, start = 0;
+  // phase 2: vlz / huffman tiles stage their bytes (from stage byte 0) before the job look-back
+  constexpr bool prestage = PHASE == 2;
+  uint32_t pst = 0;
+  // vlz token stream (vlz.hpp:111-125) of the tile into stage + mis; returns its bytes
+  auto stage_vlz = [&](uint32_t mis) -> uint32_t {
+    uint32_t* roff = lits;  // token sizes -> byte offsets inside the tile (in place)
+    const uint32_t per = (T.rows + kBlock - 1) / kBlock;
+    const uint32_t r0 = threadIdx.x * per, r1 = min(r0 + per, T.rows);
+    uint32_t sum = 0;
+    for (uint32_t r = r0; r < r1; ++r) sum += lits[r];
+    __syncthreads();
+    uint32_t tot;
+    uint32_t q0 = block_excl_scan<uint32_t>(sum, s_tmp32, &tot);
+    for (uint32_t r = r0; r < r1; ++r) {
+      const uint32_t sz = roff[r];
+      roff[r] = q0;
+      const uint32_t o = dec[r];
+      if (o) {  // reference token: 0x01, varint(offset)
+        uint8_t* q = stage + mis + q0;
+        *q++ = 0x01;
+        put_varint(q, o);
+      }
+      q0 += sz;
+    }
+    __syncthreads();
+    // literal tokens: 0x00 then dim zigzag varints, one warp per row
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t r = warp; r < T.rows; r += kBlock / 32) {
+      if (dec[r]) continue;
+      uint8_t* q = stage + mis + roff[r];
+      if (lane == 0) q[0] = 0x00;
+      uint32_t carry = 1;
+      const int32_t* row = codes + r * stride;
+      for (uint32_t j0 = 0; j0 < dim; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        uint32_t z = 0, len = 0;
+        if (j < dim) {
+          z = zigzag(row[j]);
+          len = varint_len(z);
+        }
+        const uint32_t inc = warp_incl_scan<uint32_t>(len);
+        if (j < dim) put_varint(q + carry + inc - len, z);
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+    }
+    __syncthreads();
+    return tot;
+  };
+  // huffman bitstream (bitstream.hpp:32-51) of the tile, MSB-first, into
+  // stage from bit 8 * mis + (pre & 7); returns the staged bytes
+  auto stage_huff = [&](uint32_t mis) -> uint32_t {
+    uint32_t* words = reinterpret_cast<uint32_t*>(stage);
+    const uint32_t lead = 8 * mis + static_cast<uint32_t>(pre & 7);
+    const uint32_t endbit = lead + static_cast<uint32_t>(my_bits);
+    const uint32_t nwords = (endbit + 31) / 32;
+    for (uint32_t w = threadIdx.x; w < nwords + 1; w += kBlock) words[w] = 0;
+    __syncthreads();
+    {  // this thread's codes, assembled in a register and stored word by word
+      const uint32_t l0 = threadIdx.x * per_h, l1 = min(l0 + per_h, ne);
+      uint32_t q = lead + pos_thread;
+      uint32_t wi = q >> 5, used = q & 31;
+      uint64_t buf = 0;
+      bool shared_word = true;  // the first word may be shared with the previous thread
+      for (uint32_t l = l0; l < l1; ++l) {
+        const uint32_t sy = static_cast<uint32_t>(codes[l + (l >> 5)] - cmin);
+        const uint64_t e = lut_staged ? sl[sy] : ldL(sy);
+        const uint32_t len = static_cast<uint32_t>(e & 0xFF);
+        buf |= (e >> 8) << (64 - used - len);
+        used += len;
+        if (used >= 32) {
+          const uint32_t w = static_cast<uint32_t>(buf >> 32);
+          if (shared_word) atomicOr(&words[wi], w);
+          else words[wi] = w;
+          shared_word = false;
+          buf <<= 32;
+          used -= 32;
+          ++wi;
+        }
+      }
+      if (used) atomicOr(&words[wi], static_cast<uint32_t>(buf >> 32));  // may be shared with the next thread
+    }
+    __syncthreads();
+    const uint32_t nbytes_stage = (endbit + 7) / 8;
+    for (uint32_t w = threadIdx.x; w < (nbytes_stage + 3) / 4; w += kBlock) words[w] = __byte_perm(words[w], 0, 0x0123);
+    __syncthreads();
+    return nbytes_stage;
+  };
   if (phase == 2) {
     // ---- 3c. fused: decoupled look-back over the job's tiles (bits), then over jobs (bytes)
     if (threadIdx.x == 0 && jid > 0) {
@@ -1528,8 +1615,8 @@ __device__ __forceinline__ void emit_tile(const EmitArgs& a, const uint32_t tid,
       }
     }
 
+    uint64_t p = 0;
     if (threadIdx.x < 32) {
-      uint64_t p = 0;
       if (first) {
         if (threadIdx.x == 0) st_status(a.tile_status + tid, kFlagInc | my_bits);
       } else {
@@ -1537,6 +1624,19 @@ __device__ __forceinline__ void emit_tile(const EmitArgs& a, const uint32_t tid,
         p = look_back(a.tile_status, J.tile0, tid, 0);
         if (threadIdx.x == 0) st_status(a.tile_status + tid, kFlagInc | (p + my_bits));
       }
+      if (threadIdx.x == 0) s_pre = p;
+    }
+    if constexpr (PHASE == 2) {
+      // the tile's bytes need only its bit offset inside the job: stage them
+      // now (from stage byte 0) while the job look-back may still wait on an
+      // earlier job's codebook; after it only the copy out remains
+      if (codec != EMBC_CODEC_RAW && !no_book) {
+        __syncthreads();
+        pre = s_pre;
+        pst = codec == EMBC_CODEC_VLZ ? stage_vlz(0) : stage_huff(0);
+      }
+    }
+    if (threadIdx.x < 32) {
       const uint64_t job_bytes = hdr + book_bytes + (p + my_bits + 7) / 8;
       const uint64_t base = a.layout == EMBC_LAYOUT_PACKED ? 4 + 16ull * a.njobs : 0;
       const uint64_t st0 = jid == 0 ? base : look_back(a.job_status, 0, jid, 0, kJobStride);
@@ -1633,50 +1733,15 @@ __device__ __forceinline__ void emit_tile(const EmitArgs& a, const uint32_t tid,
   if (codec == EMBC_CODEC_VLZ) {  // token stream (vlz.hpp:111-125)
     if (!fits) return;
     uint8_t* dst = pay + pre / 8;
-    const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 15);
-    uint32_t* roff = lits;  // token sizes -> byte offsets inside the tile (in place)
-    const uint32_t per = (T.rows + kBlock - 1) / kBlock;
-    const uint32_t r0 = threadIdx.x * per, r1 = min(r0 + per, T.rows);
-    uint32_t sum = 0;
-    for (uint32_t r = r0; r < r1; ++r) sum += lits[r];
-    __syncthreads();
-    uint32_t tot;
-    uint32_t p = block_excl_scan<uint32_t>(sum, s_tmp32, &tot);
-    for (uint32_t r = r0; r < r1; ++r) {
-      const uint32_t sz = roff[r];
-      roff[r] = p;
-      const uint32_t o = dec[r];
-      if (o) {  // reference token: 0x01, varint(offset)
-        uint8_t* q = stage + mis + p;
-        *q++ = 0x01;
-        put_varint(q, o);
-      }
-      p += sz;
+    if constexpr (prestage) {
+      TS(4);
+      copy_out_shifted(dst, stage, 0, pst);
+    } else {
+      const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 15);
+      const uint32_t tot = stage_vlz(mis);
+      TS(4);
+      copy_out_staged(dst, stage, tot);
     }
-    __syncthreads();
-    // literal tokens: 0x00 then dim zigzag varints, one warp per row
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t r = warp; r < T.rows; r += kBlock / 32) {
-      if (dec[r]) continue;
-      uint8_t* q = stage + mis + roff[r];
-      if (lane == 0) q[0] = 0x00;
-      uint32_t carry = 1;
-      const int32_t* row = codes + r * stride;
-      for (uint32_t j0 = 0; j0 < dim; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        uint32_t z = 0, len = 0;
-        if (j < dim) {
-          z = zigzag(row[j]);
-          len = varint_len(z);
-        }
-        const uint32_t inc = warp_incl_scan<uint32_t>(len);
-        if (j < dim) put_varint(q + carry + inc - len, z);
-        carry += __shfl_sync(0xffffffffu, inc, 31);
-      }
-    }
-    __syncthreads();
-    TS(4);
-    copy_out_staged(dst, stage, tot);
     return;
   }
 
@@ -1687,47 +1752,25 @@ __device__ __forceinline__ void emit_tile(const EmitArgs& a, const uint32_t tid,
     for (uint64_t k = threadIdx.x; k < book_bytes; k += kBlock) pay[k] = bk[k];
   }
   uint8_t* dst = bstream + (pre >> 3);
-  const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 15);
   const uint32_t b0 = static_cast<uint32_t>(pre & 7);
-  uint32_t* words = reinterpret_cast<uint32_t*>(stage);
-  const uint32_t lead = 8 * mis + b0;
-  const uint32_t endbit = lead + static_cast<uint32_t>(my_bits);
-  const uint32_t nwords = (endbit + 31) / 32;
-  for (uint32_t w = threadIdx.x; w < nwords + 1; w += kBlock) words[w] = 0;
-  __syncthreads();
-  {  // this thread's codes, assembled in a register and stored word by word
-    const uint32_t l0 = threadIdx.x * per_h, l1 = min(l0 + per_h, ne);
-    uint32_t p = lead + pos_thread;
-    uint32_t wi = p >> 5, used = p & 31;
-    uint64_t buf = 0;
-    bool shared_word = true;  // the first word may be shared with the previous thread
-    for (uint32_t l = l0; l < l1; ++l) {
-      const uint32_t s = static_cast<uint32_t>(codes[l + (l >> 5)] - cmin);
-      const uint64_t e = lut_staged ? sl[s] : ldL(s);
-      const uint32_t len = static_cast<uint32_t>(e & 0xFF);
-      buf |= (e >> 8) << (64 - used - len);
-      used += len;
-      if (used >= 32) {
-        const uint32_t w = static_cast<uint32_t>(buf >> 32);
-        if (shared_word) atomicOr(&words[wi], w);
-        else words[wi] = w;
-        shared_word = false;
-        buf <<= 32;
-        used -= 32;
-        ++wi;
-      }
-    }
-    if (used) atomicOr(&words[wi], static_cast<uint32_t>(buf >> 32));  // may be shared with the next thread
-  }
-  __syncthreads();
-  const uint32_t nbytes_stage = (endbit + 7) / 8;
-  for (uint32_t w = threadIdx.x; w < (nbytes_stage + 3) / 4; w += kBlock) words[w] = __byte_perm(words[w], 0, 0x0123);
-  __syncthreads();
+  // phase 2: staged from byte 0 before the job look-back; else aligned with dst
+  const uint32_t mis = prestage ? 0u : static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 15);
+  uint32_t nbytes_stage;
+  if constexpr (prestage) nbytes_stage = pst;
+  else nbytes_stage = stage_huff(mis);
+  const uint32_t endbit = 8 * mis + b0 + static_cast<uint32_t>(my_bits);
   TS(4);
   const uint32_t nbytes = nbytes_stage - mis;  // output bytes touched by this tile
   const bool head_shared = b0 != 0;
   const bool tail_shared = !last && (endbit & 7) != 0;
-  if (fits) copy_range(dst, stage, mis, head_shared ? 1 : 0, nbytes - (tail_shared ? 1 : 0));
+  if (fits) {
+    const uint32_t lo = head_shared ? 1 : 0, hi = nbytes - (tail_shared ? 1 : 0);
+    if constexpr (prestage) {
+      if (hi > lo) copy_out_shifted(dst + lo, stage, lo, hi - lo);
+    } else {
+      copy_range(dst, stage, mis, lo, hi);
+    }
+  }
   // bytes shared with the neighbouring tiles: the second of the two to arrive
   // writes the OR of both halves and re-arms the slot (kept zero between calls)
   if (threadIdx.x == 0) {
