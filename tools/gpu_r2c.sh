@@ -1,6 +1,6 @@
 # Round-2 evidence: GPU tests, smoke, bench lines for every workload, reference arm,
 # ncu launch lists (KG, TB) and --set full captures of one KG and one TB step.
-TAG=${1:-r2i}
+TAG=${1:-r2j}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
 timeout 1200 python -m pytest tests -q -m gpu -x --timeout 300 2>&1 | tail -30 > gpurun_out/ev_${TAG}_pytest_gpu.log
