@@ -1626,7 +1626,7 @@ __device__ __forceinline__ void emit_tile(const EmitArgs& a, const uint32_t tid,
       }
       if (threadIdx.x == 0) s_pre = p;
     }
-    if constexpr (PHASE == 2) {
+    if constexpr (prestage) {
       // the tile's bytes need only its bit offset inside the job: stage them
       // now (from stage byte 0) while the job look-back may still wait on an
       // earlier job's codebook; after it only the copy out remains
